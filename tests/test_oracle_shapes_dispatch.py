@@ -1,0 +1,154 @@
+"""Pins for oracle O1 (shape functions) and O2 (dispatch rule).
+
+O1 is pinned to the broadcast rules printed at PAPER.md:230-235 (golden file), to
+numpy's broadcasting (the footnote at PAPER.md:228 cites it) by exhaustive
+enumeration, and to invariants (symmetry, error iff static mismatch).
+O2 is pinned to the paper's residue identity x = t*k + r, the SPEC
+worked examples (golden file), and the totality/uniqueness invariants.
+"""
+import itertools
+import os
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ANY = -1
+
+
+def _read_golden(name):
+    rows = []
+    for line in open(os.path.join(HERE, "golden", name)):
+        line = line.split("#")[0].strip()
+        if line:
+            rows.append(line.split())
+    return rows
+
+
+def _tok(v):
+    return ANY if v == "ANY" else int(v)
+
+
+def test_broadcast_rel_golden(orc):
+    for a, b, e in _read_golden("broadcast_rel.txt"):
+        st, out = orc.bcast(_tok(a), _tok(b))
+        assert st == 0 and out == _tok(e), (a, b, e, out)
+
+
+def test_broadcast_static_matches_numpy(orc):
+    # brute force over static dims 1..8: the oracle agrees with numpy broadcasting
+    for a, b in itertools.product(range(1, 9), repeat=2):
+        st, out = orc.bcast(a, b)
+        try:
+            ref = np.broadcast_shapes((a,), (b,))[0]
+            assert st == 0 and out == ref
+        except ValueError:
+            assert st == -3 and a != b and a > 1 and b > 1
+
+
+def test_broadcast_symmetric_and_any(orc):
+    dims = [ANY] + list(range(1, 9))
+    for a, b in itertools.product(dims, repeat=2):
+        s1, o1 = orc.bcast(a, b)
+        s2, o2 = orc.bcast(b, a)
+        assert (s1, o1) == (s2, o2)
+        if ANY in (a, b):
+            assert s1 == 0          # Any never fails statically (gradual typing)
+
+
+def test_shape_dense_rules(orc):
+    # config 3 QKV: (L,768) x (2304,768) -> (L,2304); Any propagates
+    assert orc.shape_dense((37, 768), (2304, 768)) == (0, (37, 2304))
+    assert orc.shape_dense((ANY, 768), (2304, 768)) == (0, (ANY, 2304))
+    assert orc.shape_dense((5, ANY), (7, 3)) == (0, (5, 7))            # deferred K check
+    assert orc.shape_dense((5, 4), (7, 3))[0] == -3                    # runtime K mismatch
+    assert orc.shape_dense((0, 4), (7, 4))[0] == -4                    # extent 0
+    # exhaustive: error iff both K static and different
+    dims = [ANY] + list(range(1, 6))
+    for a0, a1, w0, w1 in itertools.product(dims, repeat=4):
+        st, out = orc.shape_dense((a0, a1), (w0, w1))
+        if a1 != ANY and w1 != ANY and a1 != w1:
+            assert st == -3
+        else:
+            assert st == 0 and out == (a0, w0)
+
+
+def test_shape_bmm_rules(orc):
+    # config 3 scores: (12,L,64) x (12,L,64) -> (12,L,L); context with trans_b
+    assert orc.shape_bmm((12, 50, 64), (12, 50, 64), 0) == (0, (12, 50, 50))
+    assert orc.shape_bmm((12, 50, 50), (12, 50, 64), 1) == (0, (12, 50, 64))
+    assert orc.shape_bmm((12, ANY, 64), (12, ANY, 64), 0) == (0, (12, ANY, ANY))
+    assert orc.shape_bmm((1, 5, 3), (4, 6, 3), 0) == (0, (4, 5, 6))    # batch broadcast
+    assert orc.shape_bmm((2, 5, 3), (4, 6, 3), 0)[0] == -3
+    assert orc.shape_bmm((2, 5, 3), (2, 6, 4), 0)[0] == -3
+    dims = [ANY, 1, 2, 3]
+    for p0, p2, q0, q1, q2 in itertools.product(dims, repeat=5):
+        for tb in (0, 1):
+            st, out = orc.shape_bmm((p0, 4, p2), (q0, q1, q2), tb)
+            kb = q1 if tb else q2
+            kbad = p2 != ANY and kb != ANY and p2 != kb
+            bbad = p0 != ANY and q0 != ANY and p0 != q0 and p0 > 1 and q0 > 1
+            if kbad or bbad:
+                assert st == -3
+            else:
+                assert st == 0
+                assert out[1] == 4 and out[2] == (q2 if tb else q1)
+
+
+def test_sub_shape_example(orc):
+    # Tensor[(128,128)] is a sub-type of Tensor[(Any,128)] -- instantiating Any
+    # by 128 in the type relation must give the same output shape as the static one.
+    st1, o1 = orc.shape_dense((ANY, 128), (64, 128))
+    st2, o2 = orc.shape_dense((128, 128), (64, 128))
+    assert st1 == st2 == 0 and o1 == (ANY, 64) and o2 == (128, 64)
+
+
+def test_dispatch_worked_examples(orc):
+    for M, c, k, r, v in _read_golden("residue_examples.txt"):
+        st, d = orc.dispatch_dense(int(M), 128, 128, 0, int(c))
+        assert st == 0
+        assert (d["k"], d["r"], d["variant"]) == (int(k), int(r), int(v)), (M, c, d)
+
+
+@pytest.mark.parametrize("dt", [0, 1])
+def test_dispatch_invariants(orc, dt):
+    t = 8 if dt == 0 else 256
+    for M in list(range(1, 2049)) + [4095, 4096, 4097, 65535, 65536]:
+        for c in (0, 1, 2, 5, 8, 17):
+            st, d = orc.dispatch_dense(M, 1024, 1024, dt, c)
+            assert st == 0
+            assert d["tile_t"] == t
+            assert d["k"] * t + d["r"] == M and 0 <= d["r"] < t           # x = t k + r
+            assert d["grid"][1] == d["k"] + (d["r"] > 0)                  # every row covered once
+            n = d["n_classes"]
+            if c in (0,) or c >= n:
+                assert d["variant"] == d["residue_class"]                   # full dispatch
+            if c == 1:
+                assert d["variant"] == -1                                   # no dispatch
+            if dt == 1 and d["r"] > 0:
+                # the tail UMMA width covers the residue with < 16 wasted columns when specialised
+                if d["variant"] >= 0:
+                    assert d["r"] <= d["umma_n_tail"] < d["r"] + 16 and d["umma_n_tail"] % 16 == 0
+                else:
+                    assert d["umma_n_tail"] == 256
+            if dt == 1:
+                s = d["split_k"]
+                assert s in (1, 2, 4, 8) and d["cluster"] == (1, 1, s)
+                assert (1024 // 64) // s >= 4 or s == 1
+
+
+def test_dispatch_errors(orc):
+    assert orc.dispatch_dense(0, 128, 128, 0)[0] == -4
+    assert orc.dispatch_dense(5, 0, 128, 0)[0] == -4
+    assert orc.dispatch_dense(5, 128, 128, 7)[0] == -5
+    assert orc.dispatch_dense(5, 128, 128, 0, -1)[0] == -4
+    assert orc.dispatch_bmm(12, 5, 5, 64, 0, 0)[0] == -7
+    assert orc.dispatch_bmm(0, 5, 5, 64, 0, 1)[0] == -4
+
+
+def test_dispatch_bmm_families(orc):
+    st, d = orc.dispatch_bmm(16, 300, 300, 64, 0, 1)
+    assert st == 0 and d["family"] == 1 and d["grid"][0] == 3 and d["grid"][1] == 2
+    st, d = orc.dispatch_bmm(16, 300, 64, 300, 1, 1)
+    assert st == 0 and d["family"] == 2 and d["k"] == 2 and d["r"] == 44
+    assert d["umma_n_full"] == 64 and d["umma_n_tail"] == 64 and d["grid"][1] == 1
