@@ -1,0 +1,201 @@
+/*
+ * include/nimble.h — C ABI of libnimble.so, the B200 (sm_100a) hot path of Nimble
+ * (arXiv 2006.03031): shape functions, residue dispatch and dynamic-shape kernels.
+ *
+ * Citation key: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n,
+ * BJ:n = BASELINE.json line n.  The residue-dispatch rule is DISPATCH.md.
+ *
+ * Conventions (all entry points):
+ *  - Every symbol is extern "C"; no C++ exception crosses the boundary.  Every
+ *    entry point returns a nimble_status (0 = OK); on error the outputs are
+ *    untouched, nothing is launched, and nimble_last_error() returns a
+ *    thread-local message.
+ *  - Ownership: the CALLER owns every buffer (inputs, outputs, workspace), sized
+ *    from the shape functions BEFORE the call — the paper's shape_func -> alloc ->
+ *    invoke_mut order (App. A; destination passing).  The
+ *    library never allocates device memory on the hot path.
+ *  - Device pointers are plain device addresses (cudaMalloc / torch storage).
+ *    `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Kernels are asynchronous on `stream`; buffers must outlive the work.
+ *    Asynchronous device faults surface at the caller's next synchronisation.
+ *  - Layout: row-major with explicit leading dimensions `ld*` in ELEMENTS.
+ *    bf16 paths use TMA: base pointers 16-byte aligned and ld*sizeof(elem) a
+ *    multiple of 16, else NIMBLE_E_ALIGN.  fp32 paths require 16-byte aligned
+ *    bases and ld % 4 == 0 (float4 loads), else NIMBLE_E_ALIGN.
+ *  - The symbolic (Any) extent is M (dense), M/N/K (bmm, one symbol L),
+ *    T (LSTM) or the level size (Tree-LSTM).  Extents must be >= 1 (SPEC S:170,
+ *    S:438), else NIMBLE_E_EXTENT.  There is no CPU fallback: without a usable
+ *    CUDA device the kernels return NIMBLE_E_CUDA.
+ *  - Determinism: for a fixed dispatch the result is bitwise reproducible
+ *    (split-K partials are reduced in rank order inside a thread-block cluster;
+ *    no floating-point atomics).
+ *  - Thread safety: all entry points are re-entrant; nimble_set_variant_limit is
+ *    process-global and must be set before concurrent use.
+ */
+#ifndef NIMBLE_H_
+#define NIMBLE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NIMBLE_ANY (-1) /* statically unknown extent, `Any` */
+
+typedef enum {
+    NIMBLE_OK = 0,
+    NIMBLE_E_NULL = -1,        /* a required pointer is NULL */
+    NIMBLE_E_RANK = -2,        /* wrong rank (reserved; ranks are fixed by the signatures) */
+    NIMBLE_E_SHAPE = -3,       /* runtime type-relation violation: K or batch mismatch */
+    NIMBLE_E_EXTENT = -4,      /* an extent < 1 or > 2^31-1 */
+    NIMBLE_E_DTYPE = -5,       /* unknown dtype / epilogue code */
+    NIMBLE_E_ALIGN = -6,       /* base or leading dimension misaligned for TMA / vector loads */
+    NIMBLE_E_UNSUPPORTED = -7, /* a combination this build does not implement */
+    NIMBLE_E_CUDA = -8         /* a CUDA runtime/driver call failed (message in nimble_last_error) */
+} nimble_status;
+
+typedef enum { NIMBLE_F32 = 0, NIMBLE_BF16 = 1 } nimble_dtype;
+
+/* Fused epilogues (operator fusion of data-independent ops). */
+typedef enum {
+    NIMBLE_EPI_NONE = 0,          /* y = x W^T */
+    NIMBLE_EPI_BIAS = 1,          /* y = x W^T + b */
+    NIMBLE_EPI_BIAS_GELU = 2,     /* y = GELU_erf(x W^T + b)  (BERT FFN1) */
+    NIMBLE_EPI_BIAS_RESIDUAL = 3  /* y = x W^T + b + residual (BERT O-proj, FFN2) */
+} nimble_epilogue;
+
+/* The dispatch record: exactly what the matching kernel entry point launches.
+ * Field meanings are DISPATCH.md's.  family: 0 SIMT8 (fp32), 1 UMMA_T (bf16,
+ * tokens on the UMMA-N slot), 2 UMMA_D (bf16 bmm with trans_b).  variant -1 is
+ * the guarded fallback.  x = tile_t*k + r. */
+typedef struct {
+    int32_t family, tile_t, granule, n_classes, residue_class, variant, split_k;
+    int32_t umma_m, umma_n_full, umma_n_tail;
+    int64_t k, r;
+    int32_t grid[3], cluster[3];
+} nimble_dispatch;
+
+/* ---------------------------------------------------------------------------
+ * Shape functions — host, pure, data-independent mode.  They compute
+ * the output shape for allocation and check the type relation at run time.
+ * In/out are host int64 arrays.  A dim of NIMBLE_ANY switches to the compile-time
+ * type relation: Any propagates, checks involving Any are deferred (gradual
+ * typing); the bmm batch dim follows broadcast_rel.
+ * dense:  x (M,K) x W (N,K)             -> (M,N)          K mismatch -> E_SHAPE
+ * bmm:    A (B1,M,K) x B (B2,N,K)        -> (bcast(B1,B2),M,N)   trans_b = 0
+ *         A (B1,M,K) x B (B2,K,N)        -> (bcast(B1,B2),M,N)   trans_b = 1
+ * ------------------------------------------------------------------------- */
+int nimble_shape_dense(const int64_t x_shape[2], const int64_t w_shape[2], int64_t out_shape[2]);
+int nimble_shape_bmm(const int64_t a_shape[3], const int64_t b_shape[3], int trans_b,
+                     int64_t out_shape[3]);
+
+/* ---------------------------------------------------------------------------
+ * Residue dispatch — host, pure (the generated dispatch function).  Returns
+ * exactly the record the kernel entry point below will launch for these extents
+ * under the current variant limit.  dt is a nimble_dtype.
+ * ------------------------------------------------------------------------- */
+int nimble_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, nimble_dispatch *out);
+int nimble_dispatch_bmm(int64_t batch, int64_t M, int64_t N, int64_t K, int trans_b, int dt,
+                        nimble_dispatch *out);
+/* c = total number of generated kernels ("dispatch/k"); 0 = all (default).
+ * c < 0 -> E_EXTENT.  Process-global. */
+int nimble_set_variant_limit(int c);
+int nimble_get_variant_limit(void);
+/* The dispatch record of the last successful kernel launch on the calling thread
+ * ("instrumented variant-hit log"); E_NULL if none yet. */
+int nimble_last_dispatch(nimble_dispatch *out);
+
+/* ---------------------------------------------------------------------------
+ * nimble_dense_dyn — y[M x N] = ep( x[M x K] . W[N x K]^T + bias ) (+ residual),
+ * with M symbolic.  Device pointers; bias fp32 [N] (may be NULL only
+ * for EPI_NONE); residual [M x ldr] of the output dtype (EPI_BIAS_RESIDUAL only).
+ * dt = NIMBLE_F32: fp32 in/out, CUDA-core FFMA (SIMT8, t = 8 residue variants).
+ * dt = NIMBLE_BF16: bf16 in/out, fp32 accumulation in TMEM (tcgen05 + TMA),
+ *      output rounded to bf16 (RNE); rows >= M are never read (TMA bounds) nor
+ *      written.  The dynamic extent is never padded.
+ * ------------------------------------------------------------------------- */
+int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+                     const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
+                     int64_t K, int dt, int epi, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * nimble_bmm_dyn — C[b] = alpha . A[b] . Bhat[b] over a strided batch (attention
+ * heads), bf16 inputs, fp32 accumulation; out_dt = NIMBLE_F32 or NIMBLE_BF16.
+ *   trans_b = 0: B[b] is [N x K] (row stride ldb), Bhat = B^T   (Q.K^T)
+ *   trans_b = 1: B[b] is [K x N] (row stride ldb), Bhat = B     (P.V, MN-major B)
+ * A[b] = A + b*strideA ([M x K], row stride lda); C[b] = C + b*strideC ([M x N],
+ * row stride ldc); strides in elements, 16-byte multiples.  M, N, K may all be
+ * the one symbol L; partial K tiles are zero-filled by TMA.  in_dt must
+ * be NIMBLE_BF16 (E_UNSUPPORTED otherwise).
+ * ------------------------------------------------------------------------- */
+int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const void *B, int64_t ldb,
+                   int64_t strideB, int trans_b, void *C, int64_t ldc, int64_t strideC,
+                   int64_t batch, int64_t M, int64_t N, int64_t K, float alpha, int in_dt,
+                   int out_dt, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Row ops used around bmm_dyn in BERT (the paper is silent: DESIGN.md readings 8-10).
+ * nimble_softmax_rows: P[b][i][j] = softmax_j(S[b][i][j]) over j < L, for i < rows;
+ *   S fp32, P bf16; columns L..ldP-1 of P are written with 0 (so a following
+ *   bmm may read up to a 64-aligned K without NaNs).  ldP >= L.
+ * nimble_layernorm: Y = gamma (X - mean) / sqrt(var + eps) + beta over rows of
+ *   length d, bf16 in/out, fp32 statistics, biased variance.
+ * ------------------------------------------------------------------------- */
+int nimble_softmax_rows(const float *S, int64_t ldS, int64_t strideS, void *P, int64_t ldP,
+                        int64_t strideP, int64_t batch, int64_t rows, int64_t L, void *stream);
+int nimble_layernorm(const void *X, int64_t ldx, const float *gamma, const float *beta, float eps,
+                     void *Y, int64_t ldy, int64_t rows, int64_t d, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Fused dynamic-length LSTM layer (control flow as a device loop).
+ * G [T x ldg] fp32 = X W_ih^T + (b_ih + b_hh), computed beforehand by
+ * nimble_dense_dyn (the hoisted input GEMM).  W_hh [4H x ldw] fp32 in
+ * PyTorch row blocks (i, f, g, o).  h0, c0 [H] (NULL -> zeros).  Writes
+ * H_seq [T x ldh] (every h_t) and hT, cT [H].  One persistent cooperative kernel
+ * runs all T steps with W_hh resident in shared memory and a grid barrier per
+ * step.  workspace: device buffer of nimble_lstm_workspace_bytes(H) bytes.
+ * ------------------------------------------------------------------------- */
+size_t nimble_lstm_workspace_bytes(int64_t H);
+int nimble_lstm_seq(const float *G, int64_t ldg, const float *W_hh, int64_t ldw, const float *h0,
+                    const float *c0, float *H_seq, int64_t ldh, float *hT, float *cT, int64_t T,
+                    int64_t H, void *workspace, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * One Tree-LSTM level (binary N-ary cell; reading 13):
+ * a level-batched dense_dyn over the M nodes of one height plus the cell epilogue.
+ *   is_leaf = 1: A row of node m = A + a_rows[m]*lda (word vectors, K = I);
+ *                W = W_l [3H x K] (gates i, o, u); c = s(i) tanh(u); h = s(o) tanh(c)
+ *   is_leaf = 0: A row = A + a_rows[m]*lda holding [h_l | h_r] (K = 2H);
+ *                W = U [5H x 2H] (gates i, f_l, f_r, o, u);
+ *                c = s(i) tanh(u) + s(f_l) c_l + s(f_r) c_r,  [c_l | c_r] read from
+ *                ccat + nodes[m]*ldcat;  h = s(o) tanh(c)
+ * Writes h_out/c_out row nodes[m] (ld ldo) and, when parent_slot[m] = p*2+side >= 0,
+ * h into hcat[p][side*H ...] and c into ccat[p][side*H ...] (ld ldcat): the
+ * epilogue fills the parent's input row, so the next level needs no gather.
+ * All fp32 device buffers; nodes, a_rows, parent_slot are device int32 [M].
+ * ------------------------------------------------------------------------- */
+int nimble_treelstm_level(const int32_t *nodes, const float *A, int64_t lda, const int32_t *a_rows,
+                          const float *W, int64_t ldw, const float *bias, const int32_t *parent_slot,
+                          float *hcat, float *ccat, int64_t ldcat, float *h_out, float *c_out,
+                          int64_t ldo, int64_t M, int64_t K, int64_t H, int is_leaf, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Request sharding (BJ:5): deterministic LPT partition of R requests of lengths
+ * lens[R] over G ranks on cost(L) = 24 (25165824 L + 4096 L^2) (BERT-large flops):
+ * sort by (cost desc, id asc), give each to the least-loaded rank (ties -> lowest).
+ * Host arrays; owner[R] receives the rank of each request.
+ * ------------------------------------------------------------------------- */
+int64_t nimble_request_cost(int64_t L);
+int nimble_partition_lpt(const int64_t *lens, int64_t R, int32_t G, int32_t *owner);
+
+/* Thread-local message for the last non-OK status ("" if none). */
+const char *nimble_last_error(void);
+/* Library version string. */
+const char *nimble_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NIMBLE_H_ */

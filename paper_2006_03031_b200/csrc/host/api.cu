@@ -1,0 +1,313 @@
+// libnimble C ABI entry points (include/nimble.h): argument validation, the
+// shape-function -> dispatch -> launch sequence of Nimble's InvokePacked path
+// (App. A; §3.5 dispatch PAPER.md:387), TMA tensor-map
+// encoding and asynchronous launches on the caller's stream.
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../kernels/launch.h"
+#include "internal.h"
+
+namespace nimble {
+
+static thread_local std::string t_err;
+static thread_local nimble_dispatch t_last;
+static thread_local bool t_has_last = false;
+
+int fail(int status, const std::string &msg) {
+    t_err = msg;
+    return status;
+}
+void clear_error() { t_err.clear(); }
+void record_dispatch(const nimble_dispatch &d) {
+    t_last = d;
+    t_has_last = true;
+}
+
+namespace {
+
+int cuda_fail(const char *where, cudaError_t e) {
+    return fail(NIMBLE_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---------------------------------------------------------------- TMA encoding
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+cudaError_t g_encode_err = cudaSuccess;
+
+cudaError_t get_encoder() {
+    std::call_once(g_encode_once, [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        g_encode_err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (g_encode_err == cudaSuccess && (q != cudaDriverEntryPointSuccess || !fn))
+            g_encode_err = cudaErrorNotSupported;
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    return g_encode_err;
+}
+
+// bf16 operand with inner (contiguous) dim `inner`, `rows` rows of stride `ld` elements,
+// `batch` slices of stride `bstride` elements.  Dims are ordered by stride so heads that
+// are interleaved inside a row (QKV views) become the middle dimension.
+// box = {64 inner, box_rows rows, 1 slice}.  Returns whether batch is the middle dim.
+int encode_operand(CUtensorMap *m, const void *base, int64_t inner, int64_t rows, int64_t ld, int64_t batch,
+                   int64_t bstride, int box_rows, int *batch_mid) {
+    cudaError_t e = get_encoder();
+    if (e != cudaSuccess) return cuda_fail("cuTensorMapEncodeTiled lookup", e);
+    cuuint64_t dims[3], strides[2];
+    cuuint32_t box[3], estr[3] = {1, 1, 1};
+    const bool mid = (batch > 1) && (bstride < ld);
+    dims[0] = (cuuint64_t)inner;
+    box[0] = 64;
+    if (mid) {
+        dims[1] = (cuuint64_t)batch; strides[0] = (cuuint64_t)bstride * 2; box[1] = 1;
+        dims[2] = (cuuint64_t)rows;  strides[1] = (cuuint64_t)ld * 2;      box[2] = (cuuint32_t)box_rows;
+    } else {
+        dims[1] = (cuuint64_t)rows;  strides[0] = (cuuint64_t)ld * 2;      box[1] = (cuuint32_t)box_rows;
+        dims[2] = (cuuint64_t)batch;
+        strides[1] = (cuuint64_t)(batch > 1 ? bstride : ld * rows) * 2;
+        box[2] = 1;
+    }
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(NIMBLE_E_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+    *batch_mid = mid ? 1 : 0;
+    return NIMBLE_OK;
+}
+
+bool ext_ok(int64_t x) { return x >= 1 && x <= kMaxExtent; }
+
+// Fill the stage count / smem for a UMMA launch from the dispatch record.
+void plan_pipeline(UmmaLaunch &L, int kb_per_split) {
+    const int maxst = umma_max_stages(L.p.box_n, L.b_mn_major);
+    int st = kb_per_split < maxst ? kb_per_split : maxst;
+    if (st > 8) st = 8;
+    if (st < 1) st = 1;
+    L.p.stages = st;
+    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.n_full, L.p.split);
+}
+
+}  // namespace
+}  // namespace nimble
+
+using namespace nimble;
+
+extern "C" const char *nimble_last_error(void) { return t_err.c_str(); }
+extern "C" const char *nimble_version(void) { return "nimble-b200 0.1 (sm_100a)"; }
+
+extern "C" int nimble_last_dispatch(nimble_dispatch *out) {
+    if (!out) return fail(NIMBLE_E_NULL, "nimble_last_dispatch: out is NULL");
+    if (!t_has_last) return fail(NIMBLE_E_NULL, "nimble_last_dispatch: no launch yet on this thread");
+    *out = t_last;
+    return NIMBLE_OK;
+}
+
+// ------------------------------------------------------------------ dense_dyn
+extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+                                const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
+                                int64_t K, int dt, int epi, void *stream) {
+    // 1. shape function (runtime type-relation check)
+    const int64_t xs[2] = {M, K}, ws[2] = {N, K};
+    int64_t os[2];
+    if (!ext_ok(M) || !ext_ok(N) || !ext_ok(K)) return fail(NIMBLE_E_EXTENT, "nimble_dense_dyn: extents must be in [1, 2^31-1]");
+    int st = nimble_shape_dense(xs, ws, os);
+    if (st != NIMBLE_OK) return st;
+    if (!x || !W || !y) return fail(NIMBLE_E_NULL, "nimble_dense_dyn: x, W and y must be non-NULL");
+    if (epi < NIMBLE_EPI_NONE || epi > NIMBLE_EPI_BIAS_RESIDUAL) return fail(NIMBLE_E_DTYPE, "nimble_dense_dyn: unknown epilogue");
+    if (epi >= NIMBLE_EPI_BIAS && !bias) return fail(NIMBLE_E_NULL, "nimble_dense_dyn: bias required by the epilogue");
+    if (epi == NIMBLE_EPI_BIAS_RESIDUAL && !residual) return fail(NIMBLE_E_NULL, "nimble_dense_dyn: residual required");
+    if (ldx < K || ldw < K || ldy < N || (epi == NIMBLE_EPI_BIAS_RESIDUAL && ldr < N))
+        return fail(NIMBLE_E_SHAPE, "nimble_dense_dyn: leading dimension smaller than the row length");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    nimble_dispatch d;
+
+    if (dt == NIMBLE_F32) {
+        if (!aligned16(x) || !aligned16(W) || ldx % 4 || ldw % 4 || K % 4)
+            return fail(NIMBLE_E_ALIGN, "nimble_dense_dyn(f32): x/W need 16-B alignment, ldx, ldw, K multiples of 4");
+        dispatch_simt8(M, N, &d);                     // 2. dispatch by residue
+        Simt8Params p{static_cast<const float *>(x), ldx, static_cast<const float *>(W), ldw, bias,
+                      static_cast<const float *>(residual), ldr, static_cast<float *>(y), ldy,
+                      (int32_t)M, (int32_t)N, (int32_t)K, epi, (int32_t)d.k};
+        cudaError_t e = launch_simt8(p, d.variant, dim3(d.grid[0], d.grid[1], d.grid[2]), s);
+        if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn(f32) launch", e);
+        record_dispatch(d);
+        clear_error();
+        return NIMBLE_OK;
+    }
+    if (dt != NIMBLE_BF16) return fail(NIMBLE_E_DTYPE, "nimble_dense_dyn: unknown dtype");
+    if (!aligned16(x) || !aligned16(W) || ((ldx * 2) % 16) || ((ldw * 2) % 16))
+        return fail(NIMBLE_E_ALIGN, "nimble_dense_dyn(bf16): TMA needs 16-B aligned bases and ld*2 % 16 == 0");
+    dispatch_umma_t(1, M, N, K, &d);
+    UmmaLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    L.b_mn_major = 0;
+    L.p.rows_a = (int32_t)N;             // weights on the UMMA-M slot
+    L.p.rows_b = (int32_t)M;             // tokens on the UMMA-N slot (symbolic)
+    L.p.n_full = d.umma_n_full;
+    L.p.n_tiles = d.grid[1];
+    L.p.n_tail = d.r ? d.umma_n_tail : d.umma_n_full;
+    L.p.box_n = (L.p.n_tiles == 1) ? L.p.n_tail : d.umma_n_full;
+    L.p.kb_total = (int32_t)((K + 63) / 64);
+    L.p.split = d.split_k;
+    L.p.guard_all = d.variant < 0;
+    L.p.epi = epi;
+    L.p.out_f32 = 0;
+    L.p.transposed = 1;
+    L.p.alpha = 1.f;
+    L.p.out = y;
+    L.p.ld_out = ldy;
+    L.p.stride_out = 0;
+    L.p.bias = bias;
+    L.p.res = residual;
+    L.p.ld_res = ldr;
+    if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
+    if ((st = encode_operand(&L.tmB, x, K, M, ldx, 1, 0, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+    plan_pipeline(L, (L.p.kb_total + L.p.split - 1) / L.p.split);
+    L.grid = dim3(d.grid[0], d.grid[1], d.grid[2]);
+    L.stream = s;
+    cudaError_t e = launch_umma_gemm(L);
+    if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn(bf16) launch", e);
+    record_dispatch(d);
+    clear_error();
+    return NIMBLE_OK;
+}
+
+// ------------------------------------------------------------------ bmm_dyn
+extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const void *B, int64_t ldb,
+                              int64_t strideB, int trans_b, void *Cout, int64_t ldc, int64_t strideC, int64_t batch,
+                              int64_t M, int64_t N, int64_t K, float alpha, int in_dt, int out_dt, void *stream) {
+    if (!ext_ok(batch) || !ext_ok(M) || !ext_ok(N) || !ext_ok(K))
+        return fail(NIMBLE_E_EXTENT, "nimble_bmm_dyn: extents must be in [1, 2^31-1]");
+    const int64_t as[3] = {batch, M, K};
+    const int64_t bs[3] = {batch, trans_b ? K : N, trans_b ? N : K};
+    int64_t os[3];
+    int st = nimble_shape_bmm(as, bs, trans_b, os);
+    if (st != NIMBLE_OK) return st;
+    if (!A || !B || !Cout) return fail(NIMBLE_E_NULL, "nimble_bmm_dyn: A, B and C must be non-NULL");
+    if (in_dt == NIMBLE_F32) return fail(NIMBLE_E_UNSUPPORTED, "nimble_bmm_dyn: fp32 inputs are not built (bf16 only)");
+    if (in_dt != NIMBLE_BF16 || (out_dt != NIMBLE_BF16 && out_dt != NIMBLE_F32))
+        return fail(NIMBLE_E_DTYPE, "nimble_bmm_dyn: unknown dtype");
+    if (lda < K || ldb < (trans_b ? N : K) || ldc < N) return fail(NIMBLE_E_SHAPE, "nimble_bmm_dyn: leading dimension too small");
+    const int osz = out_dt == NIMBLE_F32 ? 4 : 2;
+    if (!aligned16(A) || !aligned16(B) || !aligned16(Cout) || (lda * 2) % 16 || (ldb * 2) % 16 ||
+        (strideA * 2) % 16 || (strideB * 2) % 16 || (ldc * osz) % 16 || (strideC * osz) % 16)
+        return fail(NIMBLE_E_ALIGN, "nimble_bmm_dyn: bases, leading dims and batch strides must be 16-B multiples");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    nimble_dispatch d;
+    nimble_dispatch_bmm(batch, M, N, K, trans_b, in_dt, &d);
+    UmmaLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    L.p.kb_total = (int32_t)((K + 63) / 64);
+    L.p.split = d.split_k;
+    L.p.guard_all = d.variant < 0;
+    L.p.epi = 0;
+    L.p.out_f32 = out_dt == NIMBLE_F32;
+    L.p.alpha = alpha;
+    L.p.out = Cout;
+    L.p.ld_out = ldc;
+    L.p.stride_out = strideC;
+    L.p.n_full = d.umma_n_full;
+    L.p.n_tiles = d.grid[1];
+    if (!trans_b) {
+        // family 1: B rows (N) on the UMMA-M slot, A rows (M, symbolic) on the UMMA-N slot
+        L.b_mn_major = 0;
+        L.p.rows_a = (int32_t)N;
+        L.p.rows_b = (int32_t)M;
+        L.p.n_tail = d.r ? d.umma_n_tail : d.umma_n_full;
+        L.p.box_n = (L.p.n_tiles == 1) ? L.p.n_tail : d.umma_n_full;
+        L.p.transposed = 1;
+        if ((st = encode_operand(&L.tmA, B, K, N, ldb, batch, strideB, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
+        if ((st = encode_operand(&L.tmB, A, K, M, lda, batch, strideA, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+    } else {
+        // family 2: A rows (M) on the UMMA-M slot, columns of B (N) MN-major on the UMMA-N slot
+        L.b_mn_major = 1;
+        L.p.rows_a = (int32_t)M;
+        L.p.rows_b = (int32_t)N;
+        L.p.n_tail = d.umma_n_tail;
+        L.p.box_n = d.umma_n_full;
+        L.p.transposed = 0;
+        if ((st = encode_operand(&L.tmA, A, K, M, lda, batch, strideA, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
+        // B is [K x N]: inner dim N (contiguous), K rows; box {64 cols, 64 k-rows}
+        if ((st = encode_operand(&L.tmB, B, N, K, ldb, batch, strideB, 64, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+    }
+    plan_pipeline(L, (L.p.kb_total + L.p.split - 1) / L.p.split);
+    L.grid = dim3(d.grid[0], d.grid[1], d.grid[2]);
+    L.stream = s;
+    cudaError_t e = launch_umma_gemm(L);
+    if (e != cudaSuccess) return cuda_fail("nimble_bmm_dyn launch", e);
+    record_dispatch(d);
+    clear_error();
+    return NIMBLE_OK;
+}
+
+// ------------------------------------------------------------------ row ops
+extern "C" int nimble_softmax_rows(const float *S, int64_t ldS, int64_t strideS, void *P, int64_t ldP, int64_t strideP,
+                                   int64_t batch, int64_t rows, int64_t L, void *stream) {
+    if (!S || !P) return fail(NIMBLE_E_NULL, "nimble_softmax_rows: NULL pointer");
+    if (!ext_ok(batch) || !ext_ok(rows) || !ext_ok(L)) return fail(NIMBLE_E_EXTENT, "nimble_softmax_rows: extents must be >= 1");
+    if (ldS < L || ldP < L) return fail(NIMBLE_E_SHAPE, "nimble_softmax_rows: ld < L");
+    if (L > 1024) return fail(NIMBLE_E_UNSUPPORTED, "nimble_softmax_rows: L > 1024 not built");
+    cudaError_t e = launch_softmax_rows(S, ldS, strideS, static_cast<__nv_bfloat16 *>(P), ldP, strideP, batch, rows, L,
+                                        static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("nimble_softmax_rows launch", e);
+    clear_error();
+    return NIMBLE_OK;
+}
+
+extern "C" int nimble_layernorm(const void *X, int64_t ldx, const float *gamma, const float *beta, float eps, void *Y,
+                                int64_t ldy, int64_t rows, int64_t d, void *stream) {
+    if (!X || !gamma || !beta || !Y) return fail(NIMBLE_E_NULL, "nimble_layernorm: NULL pointer");
+    if (!ext_ok(rows) || !ext_ok(d)) return fail(NIMBLE_E_EXTENT, "nimble_layernorm: extents must be >= 1");
+    if (d > 4096) return fail(NIMBLE_E_UNSUPPORTED, "nimble_layernorm: d > 4096 not built");
+    if (d % 8 || ldx % 8 || ldy % 8 || !aligned16(X) || !aligned16(Y))
+        return fail(NIMBLE_E_ALIGN, "nimble_layernorm: d, ldx, ldy must be multiples of 8 and bases 16-B aligned");
+    cudaError_t e = launch_layernorm(static_cast<const __nv_bfloat16 *>(X), ldx, gamma, beta, eps,
+                                     static_cast<__nv_bfloat16 *>(Y), ldy, rows, d, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("nimble_layernorm launch", e);
+    clear_error();
+    return NIMBLE_OK;
+}
+
+// ------------------------------------------------------------------ LSTM
+extern "C" size_t nimble_lstm_workspace_bytes(int64_t H) { return H >= 1 ? lstm_workspace_bytes(H) : 0; }
+
+extern "C" int nimble_lstm_seq(const float *G, int64_t ldg, const float *W_hh, int64_t ldw, const float *h0,
+                               const float *c0, float *H_seq, int64_t ldh, float *hT, float *cT, int64_t T, int64_t H,
+                               void *workspace, void *stream) {
+    if (!G || !W_hh || !H_seq || !hT || !cT || !workspace) return fail(NIMBLE_E_NULL, "nimble_lstm_seq: NULL pointer");
+    if (!ext_ok(T) || !ext_ok(H)) return fail(NIMBLE_E_EXTENT, "nimble_lstm_seq: T and H must be >= 1");
+    if (ldg < 4 * H || ldw < H || ldh < H) return fail(NIMBLE_E_SHAPE, "nimble_lstm_seq: leading dimension too small");
+    if (H > 4096) return fail(NIMBLE_E_UNSUPPORTED, "nimble_lstm_seq: H > 4096 not built");
+    cudaError_t e = launch_lstm_seq(G, ldg, W_hh, ldw, h0, c0, H_seq, ldh, hT, cT, T, H, workspace,
+                                    static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("nimble_lstm_seq launch", e);
+    clear_error();
+    return NIMBLE_OK;
+}
+
+// ------------------------------------------------------------------ Tree-LSTM
+extern "C" int nimble_treelstm_level(const int32_t *nodes, const float *A, int64_t lda, const int32_t *a_rows,
+                                     const float *W, int64_t ldw, const float *bias, const int32_t *parent_slot,
+                                     float *hcat, float *ccat, int64_t ldcat, float *h_out, float *c_out, int64_t ldo,
+                                     int64_t M, int64_t K, int64_t H, int is_leaf, void *stream) {
+    if (!nodes || !A || !a_rows || !W || !bias || !parent_slot || !hcat || !ccat || !h_out || !c_out)
+        return fail(NIMBLE_E_NULL, "nimble_treelstm_level: NULL pointer");
+    if (!ext_ok(M) || !ext_ok(K) || !ext_ok(H)) return fail(NIMBLE_E_EXTENT, "nimble_treelstm_level: extents must be >= 1");
+    if (!is_leaf && K != 2 * H) return fail(NIMBLE_E_SHAPE, "nimble_treelstm_level: internal nodes need K == 2H");
+    if (lda < K || ldw < K || ldcat < 2 * H || ldo < H) return fail(NIMBLE_E_SHAPE, "nimble_treelstm_level: ld too small");
+    if (!aligned16(A) || !aligned16(W) || lda % 4 || ldw % 4 || K % 4)
+        return fail(NIMBLE_E_ALIGN, "nimble_treelstm_level: A/W need 16-B alignment, lda, ldw, K multiples of 4");
+    TreeParams p{nodes, A, lda, a_rows, W, ldw, bias, parent_slot, hcat, ccat, ldcat, h_out, c_out, ldo,
+                 (int32_t)M, (int32_t)K, (int32_t)H, is_leaf};
+    cudaError_t e = launch_treelstm_level(p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("nimble_treelstm_level launch", e);
+    clear_error();
+    return NIMBLE_OK;
+}

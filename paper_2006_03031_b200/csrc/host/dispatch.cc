@@ -1,0 +1,145 @@
+// The generated dispatch function of Nimble §3.5: the symbolic
+// extent x is split as x = t*k + r and the residue picks a specialised kernel;
+// with a variant limit c < n_classes "fewer kernels than the tiling factor" exist
+// (fig:sym-codegen PAPER.md:699) and the rest take the guarded
+// fallback.  The rule is DISPATCH.md; the oracle implements it independently.
+#include <atomic>
+
+#include "internal.h"
+
+namespace nimble {
+
+static std::atomic<int> g_variant_limit{0};
+
+int variant_limit() { return g_variant_limit.load(std::memory_order_relaxed); }
+
+namespace {
+
+struct ResidueFamily {
+    int32_t id, t, granule, n_classes;
+};
+constexpr ResidueFamily kSIMT8{0, 8, 1, 8};      // fp32 CUDA-core dense, the paper's t = 8
+constexpr ResidueFamily kUMMA_T{1, 256, 16, 17}; // bf16 tcgen05, tokens on UMMA-N
+constexpr ResidueFamily kUMMA_D{2, 128, 128, 2}; // bf16 tcgen05 bmm with MN-major B
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// class -> specialised variant, or -1 when the variant limit leaves it to the fallback
+int32_t select_variant(const ResidueFamily &f, int32_t cls) {
+    const int c = variant_limit();
+    const int kernels = (c <= 0 || c > f.n_classes) ? f.n_classes : c;
+    const bool specialised = (kernels == f.n_classes) || (cls <= kernels - 2);
+    return specialised ? cls : -1;
+}
+
+// split-K factor (cluster size along K): grow while the grid is below one wave
+// and every split keeps >= 4 k-blocks of 64.
+int32_t choose_split(int64_t ctas, int64_t K) {
+    const int64_t kblocks = cdiv(K, 64);
+    int32_t s = 1;
+    for (;;) {
+        const int32_t next = s * 2;
+        if (next > 8 || ctas * s >= kNumSMs || kblocks / next < 4) break;
+        s = next;
+    }
+    return s;
+}
+
+void split_residue(const ResidueFamily &f, int64_t x, nimble_dispatch *d) {
+    d->family = f.id;
+    d->tile_t = f.t;
+    d->granule = f.granule;
+    d->n_classes = f.n_classes;
+    d->k = x / f.t;                 // x = t*k + r
+    d->r = x - d->k * f.t;
+}
+
+}  // namespace
+
+int dispatch_simt8(int64_t M, int64_t N, nimble_dispatch *d) {
+    *d = nimble_dispatch{};
+    split_residue(kSIMT8, M, d);
+    d->residue_class = static_cast<int32_t>(d->r);
+    d->variant = select_variant(kSIMT8, d->residue_class);
+    d->split_k = 1;
+    d->grid[0] = static_cast<int32_t>(cdiv(N, 128));
+    d->grid[1] = static_cast<int32_t>(d->k + (d->r ? 1 : 0));
+    d->grid[2] = 1;
+    d->cluster[0] = d->cluster[1] = d->cluster[2] = 1;
+    return NIMBLE_OK;
+}
+
+int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, nimble_dispatch *d) {
+    *d = nimble_dispatch{};
+    split_residue(kUMMA_T, M_tokens, d);
+    d->residue_class = static_cast<int32_t>(cdiv(d->r, kUMMA_T.granule));
+    d->variant = select_variant(kUMMA_T, d->residue_class);
+    d->umma_m = 128;
+    d->umma_n_full = kUMMA_T.t;
+    d->umma_n_tail = d->r == 0 ? 0 : (d->variant < 0 ? kUMMA_T.t : kUMMA_T.granule * d->residue_class);
+    const int64_t m_tiles = cdiv(N_rows, 128);
+    const int64_t n_tiles = d->k + (d->r ? 1 : 0);
+    d->split_k = choose_split(m_tiles * n_tiles * batch, K);
+    d->grid[0] = static_cast<int32_t>(m_tiles);
+    d->grid[1] = static_cast<int32_t>(n_tiles);
+    d->grid[2] = static_cast<int32_t>(batch * d->split_k);
+    d->cluster[0] = 1;
+    d->cluster[1] = 1;
+    d->cluster[2] = d->split_k;
+    return NIMBLE_OK;
+}
+
+int dispatch_umma_d(int64_t batch, int64_t M, int64_t N, int64_t K, nimble_dispatch *d) {
+    *d = nimble_dispatch{};
+    split_residue(kUMMA_D, M, d);
+    d->residue_class = d->r ? 1 : 0;
+    d->variant = select_variant(kUMMA_D, d->residue_class);
+    d->umma_m = 128;
+    const int64_t n_tiles = cdiv(N, 256);
+    d->umma_n_full = static_cast<int32_t>(N >= 256 ? 256 : 16 * cdiv(N, 16));
+    d->umma_n_tail = static_cast<int32_t>(16 * cdiv(N - 256 * (n_tiles - 1), 16));
+    const int64_t m_tiles = d->k + (d->r ? 1 : 0);
+    d->split_k = choose_split(m_tiles * n_tiles * batch, K);
+    d->grid[0] = static_cast<int32_t>(m_tiles);
+    d->grid[1] = static_cast<int32_t>(n_tiles);
+    d->grid[2] = static_cast<int32_t>(batch * d->split_k);
+    d->cluster[0] = 1;
+    d->cluster[1] = 1;
+    d->cluster[2] = d->split_k;
+    return NIMBLE_OK;
+}
+
+}  // namespace nimble
+
+using namespace nimble;
+
+static bool extents_valid(std::initializer_list<int64_t> xs) {
+    for (int64_t x : xs)
+        if (x < 1 || x > kMaxExtent) return false;
+    return true;
+}
+
+extern "C" int nimble_set_variant_limit(int c) {
+    if (c < 0) return fail(NIMBLE_E_EXTENT, "nimble_set_variant_limit: c must be >= 0");
+    g_variant_limit.store(c);
+    return NIMBLE_OK;
+}
+
+extern "C" int nimble_get_variant_limit(void) { return variant_limit(); }
+
+extern "C" int nimble_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, nimble_dispatch *out) {
+    if (!out) return fail(NIMBLE_E_NULL, "nimble_dispatch_dense: out is NULL");
+    if (!extents_valid({M, N, K})) return fail(NIMBLE_E_EXTENT, "nimble_dispatch_dense: extents must be in [1, 2^31-1]");
+    if (dt == NIMBLE_F32) return dispatch_simt8(M, N, out);
+    if (dt == NIMBLE_BF16) return dispatch_umma_t(1, M, N, K, out);
+    return fail(NIMBLE_E_DTYPE, "nimble_dispatch_dense: unknown dtype");
+}
+
+extern "C" int nimble_dispatch_bmm(int64_t batch, int64_t M, int64_t N, int64_t K, int trans_b, int dt,
+                                   nimble_dispatch *out) {
+    if (!out) return fail(NIMBLE_E_NULL, "nimble_dispatch_bmm: out is NULL");
+    if (!extents_valid({batch, M, N, K})) return fail(NIMBLE_E_EXTENT, "nimble_dispatch_bmm: extents must be in [1, 2^31-1]");
+    if (dt == NIMBLE_F32) return fail(NIMBLE_E_UNSUPPORTED, "nimble_dispatch_bmm: fp32 bmm is not built (bf16 only)");
+    if (dt != NIMBLE_BF16) return fail(NIMBLE_E_DTYPE, "nimble_dispatch_bmm: unknown dtype");
+    return trans_b ? dispatch_umma_d(batch, M, N, K, out) : dispatch_umma_t(batch, M, N, K, out);
+}

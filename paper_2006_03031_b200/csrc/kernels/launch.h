@@ -1,0 +1,89 @@
+// Host-side launch descriptors shared between api.cu and the kernel translation units.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace nimble {
+
+// Parameters of one tcgen05 GEMM launch (families UMMA_T / UMMA_D, DISPATCH.md).
+//   D[i][j] = sum_k A[i][k] * B[j][k]   (i on the UMMA-M slot, j on the UMMA-N slot)
+// transposed = 1: out[b*stride + j*ld + i]  (lane = i = output feature: coalesced)
+// transposed = 0: out[b*stride + i*ld + j]  (row-major in i)
+struct UmmaParams {
+    int32_t rows_a;      // valid extent of the UMMA-M slot (guard)
+    int32_t rows_b;      // valid extent of the UMMA-N slot (guard)
+    int32_t n_full;      // UMMA N of full tiles
+    int32_t n_tail;      // UMMA N of the last tile along the N slot
+    int32_t n_tiles;     // tiles along the N slot (grid.y)
+    int32_t box_n;       // B rows (K-major) / B columns (MN-major) per TMA stage
+    int32_t kb_total;    // ceil(K / 64)
+    int32_t split;       // split-K factor (= cluster size along z)
+    int32_t stages;      // smem pipeline depth
+    int32_t guard_all;   // 1: fallback variant — guard every tile, tail at full width
+    int32_t epi;         // nimble_epilogue (family 1); 0 for bmm
+    int32_t out_f32;     // 1: fp32 output, 0: bf16 output
+    int32_t transposed;  // see above
+    int32_t a_batch_mid; // tensor-map dim order: 1 -> {K, batch, rows}, 0 -> {K, rows, batch}
+    int32_t b_batch_mid;
+    int32_t a_bcast;     // 1: A batch is broadcast (coordinate 0)
+    int32_t b_bcast;
+    float alpha;
+    void *out;
+    int64_t ld_out;
+    int64_t stride_out;
+    const float *bias;
+    const void *res;
+    int64_t ld_res;
+};
+
+struct UmmaLaunch {
+    CUtensorMap tmA, tmB;
+    UmmaParams p;
+    dim3 grid;
+    int b_mn_major;
+    size_t smem_bytes;
+    cudaStream_t stream;
+};
+
+cudaError_t launch_umma_gemm(const UmmaLaunch &L);
+size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int n_full, int split);
+int umma_max_stages(int box_n, int b_mn_major);
+
+// fp32 SIMT8 dense (family 0)
+struct Simt8Params {
+    const float *x; int64_t ldx;
+    const float *W; int64_t ldw;
+    const float *bias;
+    const float *res; int64_t ldr;
+    float *y; int64_t ldy;
+    int32_t M, N, K, epi;
+    int32_t k_tiles;      // k = floor(M / 8)
+};
+cudaError_t launch_simt8(const Simt8Params &p, int variant, dim3 grid, cudaStream_t s);
+
+cudaError_t launch_softmax_rows(const float *S, int64_t ldS, int64_t strideS, __nv_bfloat16 *P, int64_t ldP,
+                                int64_t strideP, int64_t batch, int64_t rows, int64_t L, cudaStream_t s);
+cudaError_t launch_layernorm(const __nv_bfloat16 *X, int64_t ldx, const float *g, const float *b, float eps,
+                             __nv_bfloat16 *Y, int64_t ldy, int64_t rows, int64_t d, cudaStream_t s);
+
+size_t lstm_workspace_bytes(int64_t H);
+cudaError_t launch_lstm_seq(const float *G, int64_t ldg, const float *W_hh, int64_t ldw, const float *h0,
+                            const float *c0, float *H_seq, int64_t ldh, float *hT, float *cT, int64_t T,
+                            int64_t H, void *workspace, cudaStream_t s);
+
+struct TreeParams {
+    const int32_t *nodes;
+    const float *A; int64_t lda;
+    const int32_t *a_rows;
+    const float *W; int64_t ldw;
+    const float *bias;
+    const int32_t *parent_slot;
+    float *hcat, *ccat; int64_t ldcat;
+    float *h_out, *c_out; int64_t ldo;
+    int32_t M, K, H, is_leaf;
+};
+cudaError_t launch_treelstm_level(const TreeParams &p, cudaStream_t s);
+
+}  // namespace nimble

@@ -1,0 +1,146 @@
+// Row ops around bmm_dyn in a BERT encoder layer: softmax over the dynamic
+// sequence length L and LayerNorm (the paper is silent on both; DESIGN.md
+// readings 9-10).  Memory-bound; 16-B vector loads where the layout allows.
+#include "launch.h"
+#include "ptx.cuh"
+
+namespace nimble {
+
+namespace {
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// One warp per row; the row is held in registers (L <= 32 * kMaxPerLane).
+constexpr int kMaxPerLane = 32;   // L <= 1024
+
+__global__ void __launch_bounds__(256) softmax_rows_kernel(const float *__restrict__ S, int64_t ldS, int64_t strideS,
+                                                           __nv_bfloat16 *__restrict__ P, int64_t ldP,
+                                                           int64_t strideP, int64_t batch, int64_t rows, int L) {
+    const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (gw >= batch * rows) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t b = gw / rows, i = gw % rows;
+    const float *s = S + b * strideS + i * ldS;
+    __nv_bfloat16 *pr = P + b * strideP + i * ldP;
+    float v[kMaxPerLane];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < kMaxPerLane; ++q) {
+        const int j = lane + 32 * q;
+        v[q] = (j < L) ? s[j] : -INFINITY;
+        mx = fmaxf(mx, v[q]);
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < kMaxPerLane; ++q) {
+        const int j = lane + 32 * q;
+        v[q] = (j < L) ? __expf(v[q] - mx) : 0.f;
+        sum += v[q];
+    }
+    sum = warp_sum(sum);
+    const float inv = 1.f / sum;
+#pragma unroll
+    for (int q = 0; q < kMaxPerLane; ++q) {
+        const int j = lane + 32 * q;
+        if (j < L) pr[j] = __float2bfloat16_rn(v[q] * inv);
+    }
+    for (int64_t j = L + lane; j < ldP; j += 32) pr[j] = __float2bfloat16_rn(0.f);
+}
+
+// One 128-thread CTA per row; each thread keeps <= 32 values (d <= 4096, d % 8 == 0).
+__global__ void __launch_bounds__(128) layernorm_kernel(const __nv_bfloat16 *__restrict__ X, int64_t ldx,
+                                                        const float *__restrict__ g, const float *__restrict__ be,
+                                                        float eps, __nv_bfloat16 *__restrict__ Y, int64_t ldy,
+                                                        int d) {
+    __shared__ float red[4];
+    const int64_t row = blockIdx.x;
+    const __nv_bfloat16 *x = X + row * ldx;
+    float v[32];
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int j = (threadIdx.x + 128 * q) * 8;
+        if (j < d) {
+            uint4 u = *reinterpret_cast<const uint4 *>(x + j);
+            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float2 f = __bfloat1622float2(h[e]);
+                v[8 * q + 2 * e] = f.x;
+                v[8 * q + 2 * e + 1] = f.y;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[8 * q + e] = 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s += v[8 * q + e];
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    const float mean = (red[0] + red[1] + red[2] + red[3]) / (float)d;
+    __syncthreads();
+    float ss = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int j = (threadIdx.x + 128 * q) * 8;
+        if (j < d) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float t = v[8 * q + e] - mean;
+                ss += t * t;
+            }
+        }
+    }
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    const float var = (red[0] + red[1] + red[2] + red[3]) / (float)d;
+    const float inv = rsqrtf(var + eps);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int j = (threadIdx.x + 128 * q) * 8;
+        if (j < d) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int jj = j + 2 * e;
+                __nv_bfloat162 h2 = __floats2bfloat162_rn((v[8 * q + 2 * e] - mean) * inv * g[jj] + be[jj],
+                                                          (v[8 * q + 2 * e + 1] - mean) * inv * g[jj + 1] + be[jj + 1]);
+                w[e] = *reinterpret_cast<uint32_t *>(&h2);
+            }
+            *reinterpret_cast<uint4 *>(Y + row * ldy + j) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_softmax_rows(const float *S, int64_t ldS, int64_t strideS, __nv_bfloat16 *P, int64_t ldP,
+                                int64_t strideP, int64_t batch, int64_t rows, int64_t L, cudaStream_t s) {
+    if (L > 32 * kMaxPerLane) return cudaErrorInvalidValue;
+    const int64_t warps = batch * rows;
+    softmax_rows_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(S, ldS, strideS, P, ldP, strideP, batch, rows,
+                                                                     (int)L);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_layernorm(const __nv_bfloat16 *X, int64_t ldx, const float *g, const float *b, float eps,
+                             __nv_bfloat16 *Y, int64_t ldy, int64_t rows, int64_t d, cudaStream_t s) {
+    if (d > 4096 || d % 8) return cudaErrorInvalidValue;
+    layernorm_kernel<<<(unsigned)rows, 128, 0, s>>>(X, ldx, g, b, eps, Y, ldy, (int)d);
+    return cudaGetLastError();
+}
+
+}  // namespace nimble

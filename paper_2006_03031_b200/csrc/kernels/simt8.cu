@@ -1,0 +1,104 @@
+// fp32 CUDA-core dense with the paper's residue-specialised symbolic tiling
+// (Nimble §3.5): the symbolic row extent M is tiled by t = 8
+// (the factor the paper's tuner chose) and rewritten M = 8k + r.
+// Each CTA owns 128 output features (one per thread) and one 8-row tile:
+// CTAs blockIdx.y < k run the full tile with no guards; the single tail CTA
+// (blockIdx.y == k) runs a loop compiled for exactly r rows (variant r, no
+// guards).  The FALLBACK variant (-1) is the "fully guarded symbolic kernel":
+// every row of every tile is checked against M at run time.  The static twin
+// is the same body with M a compile-time constant (the paper's static codegen
+// baseline, fig:sym-codegen PAPER.md:696-703).
+#include "launch.h"
+#include "ptx.cuh"
+
+namespace nimble {
+
+namespace {
+
+constexpr int kChunk = 64;
+
+// ROWS >= 0: compile-time row count (no guards); ROWS < 0: runtime-guarded rows.
+template <int ROWS>
+__device__ __forceinline__ void simt8_tile(const Simt8Params &p, int row0, int rows_rt) {
+    __shared__ float xs[8][kChunk];
+    const int n = blockIdx.x * 128 + threadIdx.x;
+    const bool n_ok = n < p.N;
+    float acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[r] = 0.f;
+
+    for (int k0 = 0; k0 < p.K; k0 += kChunk) {
+        __syncthreads();
+        // stage the 8 x 64 x-chunk (rows beyond the tile / K are zeros, never read from memory)
+        for (int e = threadIdx.x; e < 8 * kChunk; e += 128) {
+            const int r = e / kChunk, kk = e % kChunk;
+            const bool live = (ROWS >= 0 ? r < ROWS : r < rows_rt) && (k0 + kk < p.K);
+            xs[r][kk] = live ? p.x[(int64_t)(row0 + r) * p.ldx + k0 + kk] : 0.f;
+        }
+        float w[kChunk];
+        const float *wrow = p.W + (int64_t)n * p.ldw + k0;
+#pragma unroll
+        for (int q = 0; q < kChunk / 4; ++q) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (n_ok && k0 + 4 * q < p.K) v = *reinterpret_cast<const float4 *>(wrow + 4 * q);
+            w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+        }
+        __syncthreads();
+        if (ROWS >= 0) {
+#pragma unroll
+            for (int r = 0; r < (ROWS >= 0 ? ROWS : 0); ++r)
+#pragma unroll
+                for (int kk = 0; kk < kChunk; ++kk) acc[r] = fmaf(w[kk], xs[r][kk], acc[r]);
+        } else {
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (r < rows_rt)                                   // the boundary check residue
+#pragma unroll                                                     // specialisation removes
+                    for (int kk = 0; kk < kChunk; ++kk) acc[r] = fmaf(w[kk], xs[r][kk], acc[r]);
+        }
+    }
+    if (!n_ok) return;
+    const float b = (p.epi >= 1) ? p.bias[n] : 0.f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        if (ROWS >= 0 ? r >= ROWS : r >= rows_rt) break;
+        const int64_t row = row0 + r;
+        float v = acc[r] + b;
+        if (p.epi == 2) v = ptx::gelu_erf(v);
+        if (p.epi == 3) v += p.res[row * p.ldr + n];
+        p.y[row * p.ldy + n] = v;
+    }
+}
+
+// Variant TAIL in 0..7: full tiles unguarded, tail compiled for exactly TAIL rows.
+template <int TAIL>
+__global__ void __launch_bounds__(128) simt8_dense_kernel(const Simt8Params p) {
+    const int row0 = blockIdx.y * 8;
+    if ((int)blockIdx.y < p.k_tiles) simt8_tile<8>(p, row0, 8);
+    else simt8_tile<TAIL>(p, row0, TAIL);
+}
+
+// FALLBACK: every tile guarded at run time.
+__global__ void __launch_bounds__(128) simt8_dense_fallback(const Simt8Params p) {
+    const int row0 = blockIdx.y * 8;
+    simt8_tile<-1>(p, row0, min(8, p.M - row0));
+}
+
+}  // namespace
+
+cudaError_t launch_simt8(const Simt8Params &p, int variant, dim3 grid, cudaStream_t s) {
+    switch (variant) {
+        case 0: simt8_dense_kernel<0><<<grid, 128, 0, s>>>(p); break;
+        case 1: simt8_dense_kernel<1><<<grid, 128, 0, s>>>(p); break;
+        case 2: simt8_dense_kernel<2><<<grid, 128, 0, s>>>(p); break;
+        case 3: simt8_dense_kernel<3><<<grid, 128, 0, s>>>(p); break;
+        case 4: simt8_dense_kernel<4><<<grid, 128, 0, s>>>(p); break;
+        case 5: simt8_dense_kernel<5><<<grid, 128, 0, s>>>(p); break;
+        case 6: simt8_dense_kernel<6><<<grid, 128, 0, s>>>(p); break;
+        case 7: simt8_dense_kernel<7><<<grid, 128, 0, s>>>(p); break;
+        default: simt8_dense_fallback<<<grid, 128, 0, s>>>(p); break;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace nimble

@@ -1,0 +1,292 @@
+// tcgen05 / TMEM / TMA GEMM for the symbolic-shape dense and batch_matmul of
+// Nimble §3.5 on sm_100a.
+//
+// One CTA = one 128 x n output tile (n = UMMA N of this tile: full width, or the
+// residue-specialised tail width 16*ceil(r/16) chosen by the dispatch function)
+// over one K slice.  Warp roles (128 threads):
+//   warp 0 lane 0  TMA producer: A[128 x 64] and B[box_n x 64] bf16 tiles, 128-B
+//                  swizzle, into a `stages`-deep smem ring (full/empty mbarriers).
+//                  Rows beyond the symbolic extent are zero-filled by TMA bounds —
+//                  the dynamic dimension is never padded in memory.
+//   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (K = 16) per 64-wide k-block into an
+//                  fp32 accumulator in TMEM; tcgen05.commit frees each smem stage.
+//   warps 0-3      epilogue: tcgen05.ld (32 lanes x 16 columns per warp-load) ->
+//                  alpha / bias / GELU / residual -> bf16 (RNE) or fp32 -> global,
+//                  warp-uniform guards only on tiles that touch the extent.
+// split > 1: the K slices of one tile form a thread-block cluster along z; every
+// CTA parks its fp32 partial in its own smem, and CTA q reduces columns
+// [q*n/split, (q+1)*n/split) over ranks 0..split-1 in order through DSMEM
+// (deterministic; no atomics), then runs the epilogue on them.
+#include <cstdio>
+
+#include "launch.h"
+#include "ptx.cuh"
+
+namespace nimble {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kBlockK = 64;                   // one 128-B swizzle row of bf16
+constexpr int kABytes = 128 * kBlockK * 2;    // 16 KiB A stage
+constexpr int kSmemLimit = 232448;            // 227 KiB opt-in per CTA
+constexpr int kTailBytes = 1024;              // barriers + tmem slot
+
+__host__ __device__ inline int b_stage_bytes(int box_n, int b_mn) {
+    return b_mn ? ((box_n + 63) / 64) * (64 * kBlockK * 2) : box_n * kBlockK * 2;
+}
+
+__device__ __forceinline__ void store_out(const UmmaParams &p, int64_t off, float v) {
+    if (p.out_f32)
+        static_cast<float *>(p.out)[off] = v;
+    else
+        static_cast<__nv_bfloat16 *>(p.out)[off] = __float2bfloat16_rn(v);
+}
+
+// Epilogue for one (row i, column j) accumulator value.
+__device__ __forceinline__ float epi_value(const UmmaParams &p, float acc, float bias_i, int64_t res_off) {
+    float v = acc * p.alpha;
+    if (p.epi >= 1) v += bias_i;
+    if (p.epi == 2) v = ptx::gelu_erf(v);
+    if (p.epi == 3) v += __bfloat162float(static_cast<const __nv_bfloat16 *>(p.res)[res_off]);
+    return v;
+}
+
+template <int B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const UmmaParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment for the 128-B swizzle atoms
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int stage_bytes = kABytes + b_stage_bytes(p.box_n, B_MN);
+    const int ring_bytes = p.stages * stage_bytes;
+    const int red_bytes = p.split > 1 ? 128 * p.n_full * 4 : 0;
+    uint8_t *tail = smem + (ring_bytes > red_bytes ? ring_bytes : red_bytes);
+    uint64_t *full_bar = reinterpret_cast<uint64_t *>(tail);
+    uint64_t *empty_bar = full_bar + p.stages;
+    uint64_t *tmem_full = empty_bar + p.stages;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+
+    const uint32_t warp = ptx::warp_id();
+    const uint32_t lane = ptx::lane_id();
+    const int m_tile = blockIdx.x;
+    const int n_tile = blockIdx.y;
+    const int split_q = blockIdx.z % p.split;
+    const int batch = blockIdx.z / p.split;
+    const bool last_n = (n_tile == p.n_tiles - 1);
+    const int n_this = last_n ? p.n_tail : p.n_full;     // UMMA N of this tile (runtime idesc field)
+    const uint32_t tmem_cols = n_this <= 32 ? 32 : n_this <= 64 ? 64 : n_this <= 128 ? 128 : 256;
+    const int kb0 = (int)((int64_t)split_q * p.kb_total / p.split);
+    const int kb1 = (int)((int64_t)(split_q + 1) * p.kb_total / p.split);
+
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int s = 0; s < p.stages; ++s) {
+            ptx::mbar_init(&full_bar[s], 1);
+            ptx::mbar_init(&empty_bar[s], 1);
+        }
+        ptx::mbar_init(tmem_full, 1);
+        ptx::fence_mbar_init();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, tmem_cols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer
+        const int32_t a_row = m_tile * 128;
+        const int32_t b_row = n_tile * p.n_full;
+        const int32_t ab = p.a_bcast ? 0 : batch;
+        const int32_t bb = p.b_bcast ? 0 : batch;
+        const uint32_t tx = kABytes + b_stage_bytes(p.box_n, B_MN);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = kb0; kb < kb1; ++kb) {
+            ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t *sa = smem + stage * stage_bytes;
+            uint8_t *sb = sa + kABytes;
+            ptx::mbar_arrive_expect_tx(&full_bar[stage], tx);
+            const int32_t kc = kb * kBlockK;
+            if (p.a_batch_mid)
+                ptx::tma_load_3d(sa, &tmA, &full_bar[stage], kc, ab, a_row);
+            else
+                ptx::tma_load_3d(sa, &tmA, &full_bar[stage], kc, a_row, ab);
+            if (B_MN) {
+                const int chunks = (p.box_n + 63) / 64;
+                for (int c = 0; c < chunks; ++c) {
+                    if (p.b_batch_mid)
+                        ptx::tma_load_3d(sb + c * 8192, &tmB, &full_bar[stage], b_row + 64 * c, bb, kc);
+                    else
+                        ptx::tma_load_3d(sb + c * 8192, &tmB, &full_bar[stage], b_row + 64 * c, kc, bb);
+                }
+            } else {
+                if (p.b_batch_mid)
+                    ptx::tma_load_3d(sb, &tmB, &full_bar[stage], kc, bb, b_row);
+                else
+                    ptx::tma_load_3d(sb, &tmB, &full_bar[stage], kc, b_row, bb);
+            }
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer (single thread)
+        const uint32_t idesc = ptx::idesc_bf16(128, (uint32_t)n_this, B_MN);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = kb0; kb < kb1; ++kb) {
+            ptx::mbar_wait(&full_bar[stage], phase);
+            ptx::tc_fence_after();
+            const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
+            const uint32_t sb = sa + kABytes;
+            const uint64_t adesc = ptx::smem_desc_sw128(sa, 0, 1024);
+            // K-major B: 8-row groups 1024 B apart.  MN-major B: 64-column chunks
+            // 8 KiB apart (LBO), 8-row k groups 1024 B apart (SBO).
+            const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb, 8192, 1024) : ptx::smem_desc_sw128(sb, 0, 1024);
+#pragma unroll
+            for (int kk = 0; kk < kBlockK / 16; ++kk) {
+                const uint64_t a_k = adesc + (uint64_t)((kk * 32) >> 4);                // +32 B along K in the row
+                const uint64_t b_k = bdesc + (uint64_t)(B_MN ? ((kk * 2048) >> 4) : ((kk * 32) >> 4));
+                ptx::umma_bf16(tmem_base, a_k, b_k, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            }
+            ptx::umma_commit(&empty_bar[stage]);       // smem stage free once these MMAs retire
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+        ptx::umma_commit(tmem_full);                   // accumulator complete
+    }
+    __syncwarp();
+
+    // ---------------- epilogue (all 4 warps; warp w owns TMEM lanes 32w..32w+31)
+    ptx::mbar_wait(tmem_full, 0);
+    ptx::tc_fence_after();
+
+    const int row_local = (int)(warp * 32 + lane);
+    const int i = m_tile * 128 + row_local;                 // UMMA-M index
+    const int j0 = n_tile * p.n_full;                       // first UMMA-N index of the tile
+    const bool tile_guard = p.guard_all || last_n || (m_tile == (int)gridDim.x - 1);
+    const int n_valid = min(n_this, p.rows_b - j0);         // columns holding real data
+    const bool row_ok = i < p.rows_a;
+    const int64_t out_b = (int64_t)batch * p.stride_out;
+    const uint32_t tmem_row = tmem_base + ((warp * 32u) << 16);
+    float bias_i = 0.f;
+    if (p.epi >= 1 && row_ok) bias_i = p.bias[i];
+
+    if (p.split == 1) {
+        for (int c0 = 0; c0 < n_this; c0 += 16) {
+            float v[16];
+            ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
+            if (!row_ok) continue;
+            if (p.transposed) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int jl = c0 + q;
+                    if (tile_guard && jl >= n_valid) break;
+                    const int64_t j = j0 + jl;
+                    store_out(p, out_b + j * p.ld_out + i, epi_value(p, v[q], bias_i, j * p.ld_res + i));
+                }
+            } else {
+                const int64_t base = out_b + (int64_t)i * p.ld_out + j0 + c0;
+                if (!tile_guard || c0 + 16 <= n_valid) {
+                    if (p.out_f32) {
+                        float4 *dst = reinterpret_cast<float4 *>(static_cast<float *>(p.out) + base);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            dst[q] = make_float4(v[4 * q] * p.alpha, v[4 * q + 1] * p.alpha, v[4 * q + 2] * p.alpha,
+                                                 v[4 * q + 3] * p.alpha);
+                    } else {
+                        uint32_t w[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * q] * p.alpha, v[2 * q + 1] * p.alpha);
+                            w[q] = *reinterpret_cast<uint32_t *>(&h2);
+                        }
+                        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out) + base);
+                        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                    }
+                } else {
+                    for (int q = 0; q < 16 && c0 + q < n_valid; ++q) store_out(p, base + q, v[q] * p.alpha);
+                }
+            }
+        }
+    } else {
+        // ---------------- split-K: park partial in own smem as red[col][128] fp32
+        float *red = reinterpret_cast<float *>(smem);
+        for (int c0 = 0; c0 < n_this; c0 += 16) {
+            float v[16];
+            ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) red[(c0 + q) * 128 + row_local] = v[q];
+        }
+        ptx::cluster_sync();
+        const uint32_t rank = ptx::cluster_ctarank();
+        const int per = n_this / p.split;
+        const int cbeg = (int)rank * per;
+        const uint32_t red_s = ptx::smem_u32(red);
+        for (int jl = cbeg; jl < cbeg + per; ++jl) {
+            float acc = 0.f;
+            const uint32_t off = (uint32_t)((jl * 128 + row_local) * 4);
+            for (int r = 0; r < p.split; ++r)                      // fixed order: deterministic
+                acc += ptx::ld_shared_cluster_f32(ptx::map_shared_rank(red_s + off, (uint32_t)r));
+            if (!row_ok || (tile_guard && jl >= n_valid)) continue;
+            const int64_t j = j0 + jl;
+            if (p.transposed)
+                store_out(p, out_b + j * p.ld_out + i, epi_value(p, acc, bias_i, j * p.ld_res + i));
+            else
+                store_out(p, out_b + (int64_t)i * p.ld_out + j, acc * p.alpha);
+        }
+        ptx::cluster_sync();                                   // keep smem alive for peers
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, tmem_cols);
+    }
+}
+
+}  // namespace
+
+int umma_max_stages(int box_n, int b_mn_major) {
+    const int stage = kABytes + b_stage_bytes(box_n, b_mn_major);
+    return (kSmemLimit - 1024 - kTailBytes) / stage;
+}
+
+size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int n_full, int split) {
+    const size_t ring = (size_t)stages * (kABytes + b_stage_bytes(box_n, b_mn_major));
+    const size_t red = split > 1 ? (size_t)128 * n_full * 4 : 0;
+    return 1024 /* alignment slack */ + (ring > red ? ring : red) + kTailBytes;
+}
+
+cudaError_t launch_umma_gemm(const UmmaLaunch &L) {
+    static bool attr_set[2] = {false, false};
+    const void *fn = L.b_mn_major ? (const void *)umma_gemm_kernel<1> : (const void *)umma_gemm_kernel<0>;
+    if (!attr_set[L.b_mn_major]) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+        if (e != cudaSuccess) return e;
+        attr_set[L.b_mn_major] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = L.grid;
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = L.smem_bytes;
+    cfg.stream = L.stream;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = 0;
+    if (L.p.split > 1) {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = (unsigned)L.p.split;
+        cfg.numAttrs = 1;
+    }
+    if (L.b_mn_major) return cudaLaunchKernelEx(&cfg, umma_gemm_kernel<1>, L.tmA, L.tmB, L.p);
+    return cudaLaunchKernelEx(&cfg, umma_gemm_kernel<0>, L.tmA, L.tmB, L.p);
+}
+
+}  // namespace nimble

@@ -1,0 +1,117 @@
+"""LSTM language-model layers and Tree-LSTM forests composed from libnimble ops.
+
+LSTM (config 2): per layer one hoisted input GEMM
+G = X W_ih^T + b over all T steps (nimble_dense_dyn, fp32 SIMT8, M = T — the
+"dynamically batched" input matmul the paper calls orthogonal) and one
+persistent recurrent kernel (nimble_lstm_seq) that loops over the runtime T on
+the device.  Feature dims are padded to a multiple of 4 with zero columns for the
+fp32 vector loads; the padding contributes exact zeros.
+
+Tree-LSTM (config 4): the recursion over the tree ADT
+becomes a host schedule of levels (node height); each level is one
+nimble_treelstm_level launch over all nodes of that height in the forest, whose
+epilogue writes (h, c) straight into the parent's input row.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import nimble as nb
+
+
+def _pad4(n: int) -> int:
+    return 4 * ((n + 3) // 4)
+
+
+class LSTMStack:
+    def __init__(self, layers, max_T: int, device="cuda"):
+        """layers: [(W_ih [4H x I], W_hh [4H x H], b [4H])] fp32 (PyTorch gate order i, f, g, o)."""
+        self.H = layers[0][1].shape[1]
+        H = self.H
+        self.I = layers[0][0].shape[1]
+        self.Ip, self.Hp = _pad4(self.I), _pad4(H)
+        self.max_T = max_T
+        self.layers = []
+        for li, (W_ih, W_hh, b) in enumerate(layers):
+            inp = W_ih.shape[1]
+            Kp = _pad4(inp)
+            Wi = torch.zeros((4 * H, Kp), dtype=torch.float32, device=device)
+            Wi[:, :inp] = W_ih.to(device)
+            self.layers.append((Wi, W_hh.to(device).contiguous(), b.to(device).contiguous(), Kp))
+        self.G = torch.empty((max_T, 4 * H), dtype=torch.float32, device=device)
+        self.Hs = [torch.zeros((max_T, self.Hp), dtype=torch.float32, device=device) for _ in layers]
+        self.hT = torch.empty((len(layers), H), dtype=torch.float32, device=device)
+        self.cT = torch.empty((len(layers), H), dtype=torch.float32, device=device)
+        self.ws = torch.empty((nb.lstm_workspace_bytes(H),), dtype=torch.uint8, device=device)
+
+    def flops_per_token(self) -> int:
+        return sum(2 * 4 * self.H * (Kp + self.H) for (_, _, _, Kp) in self.layers)
+
+    def forward(self, x: torch.Tensor, T: int | None = None) -> torch.Tensor:
+        """x [>=T x Ip] fp32 (zero columns beyond I); returns the last layer's h sequence [T x H]."""
+        T = x.shape[0] if T is None else T
+        inp = x
+        for li, (Wi, Wh, b, Kp) in enumerate(self.layers):
+            nb.dense_dyn(inp, Wi, b, self.G, epi=nb.EPI_BIAS, M=T)        # hoisted input GEMM (M = T)
+            nb.lstm_seq(self.G, Wh, self.Hs[li], self.hT[li], self.cT[li], self.ws, T=T)
+            inp = self.Hs[li]
+        return self.Hs[-1][:T, :self.H]
+
+
+class TreeSchedule:
+    """Level schedule of a forest: node height, per-level node / input-row / parent-slot arrays."""
+
+    def __init__(self, trees, device="cuda"):
+        left, right, word, roots = [], [], [], []
+        for (root, l, r, w) in trees:
+            off = len(left)
+            left += [c + off if c >= 0 else -1 for c in l]
+            right += [c + off if c >= 0 else -1 for c in r]
+            word += list(w)
+            roots.append(root + off)
+        n = len(left)
+        height = [0] * n
+        parent_slot = [-1] * n
+        for i in range(n):                      # children precede parents (post-order ids)
+            if left[i] >= 0:
+                height[i] = 1 + max(height[left[i]], height[right[i]])
+                parent_slot[left[i]] = 2 * i
+                parent_slot[right[i]] = 2 * i + 1
+        self.n_nodes, self.roots = n, roots
+        self.left, self.right, self.word = left, right, word
+        self.levels = []
+        for h in range(max(height) + 1):
+            ids = [i for i in range(n) if height[i] == h]
+            rows = [word[i] if h == 0 else i for i in ids]
+            to = lambda a: torch.tensor(a, dtype=torch.int32, device=device)
+            self.levels.append((to(ids), to(rows), to([parent_slot[i] for i in ids]), len(ids)))
+        self.n_leaves = sum(1 for i in range(n) if left[i] < 0)
+
+
+class TreeLSTM:
+    def __init__(self, W_l, b_l, U, b_u, device="cuda"):
+        self.H = U.shape[1] // 2
+        self.I = W_l.shape[1]
+        assert self.I % 4 == 0 and (2 * self.H) % 4 == 0
+        self.W_l, self.b_l = W_l.to(device).contiguous(), b_l.to(device).contiguous()
+        self.U, self.b_u = U.to(device).contiguous(), b_u.to(device).contiguous()
+
+    def flops(self, sched: TreeSchedule) -> int:
+        n_int = sched.n_nodes - sched.n_leaves
+        return sched.n_leaves * 2 * 3 * self.H * self.I + n_int * 2 * 5 * self.H * 2 * self.H
+
+    def forward(self, X: torch.Tensor, sched: TreeSchedule):
+        """X [n_words x I] fp32 on device; returns (h [n_nodes x H], c [n_nodes x H])."""
+        H, n = self.H, sched.n_nodes
+        dev = X.device
+        hcat = torch.zeros((n, 2 * H), dtype=torch.float32, device=dev)
+        ccat = torch.zeros((n, 2 * H), dtype=torch.float32, device=dev)
+        h = torch.empty((n, H), dtype=torch.float32, device=dev)
+        c = torch.empty((n, H), dtype=torch.float32, device=dev)
+        for lvl, (ids, rows, pslot, M) in enumerate(sched.levels):
+            if lvl == 0:
+                nb.treelstm_level(ids, X, rows, self.W_l, self.b_l, pslot, hcat, ccat, h, c, M, self.I, H, 1)
+            else:
+                nb.treelstm_level(ids, hcat, rows, self.U, self.b_u, pslot, hcat, ccat, h, c, M, 2 * H, H, 0)
+        return h, c
