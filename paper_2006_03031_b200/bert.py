@@ -50,6 +50,18 @@ class BertEncoder:
         # pre-extracted raw pointers: the per-call marshalling is then just ints
         self._p = {k: getattr(self, k).data_ptr() for k in ("qkv", "S", "P", "ctx", "A", "H1", "F", "O")}
         self._lp = [{k: v.data_ptr() for k, v in w.items()} for w in self.layers]
+        self.trace = None     # list -> (M, N, K, epi, start_event, end_event) per dense launch
+
+    def _dense(self, x, ldx, W, ldw, bias, res, ldr, y, ldy, M, N, K, epi, stream):
+        if self.trace is None:
+            nb.dense_dyn_raw(x, ldx, W, ldw, bias, res, ldr, y, ldy, M, N, K, nb.BF16, epi, stream)
+            return
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        nb.dense_dyn_raw(x, ldx, W, ldw, bias, res, ldr, y, ldy, M, N, K, nb.BF16, epi, stream)
+        e1.record()
+        self.trace.append((M, N, K, epi, e0, e1))
 
     def flops(self, L: int) -> int:
         d, f = self.d, self.f
@@ -62,21 +74,17 @@ class BertEncoder:
         w = self._lp[li]
         p = self._p
         ldS = _pad8(L)
-        nb.dense_dyn_raw(x_ptr, d, w["Wqkv"], d, w["bqkv"], None, 0, p["qkv"], 3 * d, L, 3 * d, d,
-                         nb.BF16, nb.EPI_BIAS, stream)
+        self._dense(x_ptr, d, w["Wqkv"], d, w["bqkv"], None, 0, p["qkv"], 3 * d, L, 3 * d, d, nb.EPI_BIAS, stream)
         q, k, v = p["qkv"], p["qkv"] + 2 * d, p["qkv"] + 4 * d
         nb._check(nb._lib.nimble_bmm_dyn(q, 3 * d, dh, k, 3 * d, dh, 0, p["S"], ldS, L * ldS, H, L, L, dh,
                                          1.0 / float(dh) ** 0.5, nb.BF16, nb.F32, stream))
         nb._check(nb._lib.nimble_softmax_rows(p["S"], ldS, L * ldS, p["P"], ldS, L * ldS, H, L, L, stream))
         nb._check(nb._lib.nimble_bmm_dyn(p["P"], ldS, L * ldS, v, 3 * d, dh, 1, p["ctx"], d, dh, H, L, dh, L,
                                          1.0, nb.BF16, nb.BF16, stream))
-        nb.dense_dyn_raw(p["ctx"], d, w["Wo"], d, w["bo"], x_ptr, d, p["A"], d, L, d, d,
-                         nb.BF16, nb.EPI_BIAS_RESIDUAL, stream)
+        self._dense(p["ctx"], d, w["Wo"], d, w["bo"], x_ptr, d, p["A"], d, L, d, d, nb.EPI_BIAS_RESIDUAL, stream)
         nb._check(nb._lib.nimble_layernorm(p["A"], d, w["g1"], w["be1"], 1e-12, p["H1"], d, L, d, stream))
-        nb.dense_dyn_raw(p["H1"], d, w["W1"], d, w["b1"], None, 0, p["F"], f, L, f, d,
-                         nb.BF16, nb.EPI_BIAS_GELU, stream)
-        nb.dense_dyn_raw(p["F"], f, w["W2"], f, w["b2"], p["H1"], d, p["O"], d, L, d, f,
-                         nb.BF16, nb.EPI_BIAS_RESIDUAL, stream)
+        self._dense(p["H1"], d, w["W1"], d, w["b1"], None, 0, p["F"], f, L, f, d, nb.EPI_BIAS_GELU, stream)
+        self._dense(p["F"], f, w["W2"], f, w["b2"], p["H1"], d, p["O"], d, L, d, f, nb.EPI_BIAS_RESIDUAL, stream)
         nb._check(nb._lib.nimble_layernorm(p["O"], d, w["g2"], w["be2"], 1e-12, out_ptr, d, L, d, stream))
 
     def forward(self, x: torch.Tensor, L: int | None = None, stream: int | None = None) -> torch.Tensor:

@@ -1,0 +1,98 @@
+"""Request-stream serving across GPUs (config 5; BASELINE.json north_star: "a stream of
+variable-length inference requests is partitioned across the 8 GPUs of one box, each
+GPU running whole requests with no collectives beyond an NCCL gather of results").
+
+* shard():  deterministic LPT partition of the request list (nimble_partition_lpt,
+  native) — every rank computes the same partition, no communication.
+* GraphCache: one CUDA graph per distinct sequence length L, captured once (the
+  dynamic kernels + their dispatch decisions for that L; capture = Nimble's
+  "compile once, dispatch at run time", replay = the launch-overhead-free VM
+  InvokePacked stream).  Shape functions and dispatch still run at capture time
+  through the C ABI for each L.
+* gather_results(): the one collective — a padded torch.distributed gather of
+  (request id, [CLS] vector) to rank 0 (NCCL over NVLink on the GPU box; gloo in
+  the CPU tests).  Rank 0 reorders by request id.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import nimble as nb
+
+
+def shard(lens: np.ndarray, world: int, rank: int) -> np.ndarray:
+    """Request ids owned by `rank` (ascending), from the native LPT partition."""
+    owner = nb.partition_lpt(lens, world)
+    return np.nonzero(owner == rank)[0].astype(np.int64)
+
+
+class GraphCache:
+    """Per-L CUDA graphs of a full encoder forward reading a static input buffer and
+    writing the [CLS] row into a static output row."""
+
+    def __init__(self, encoder, device="cuda"):
+        self.enc = encoder
+        self.xin = torch.zeros((encoder.max_len, encoder.d), dtype=torch.bfloat16, device=device)
+        self.cls = torch.zeros((encoder.d,), dtype=torch.bfloat16, device=device)
+        self.graphs = {}
+        self.stream = torch.cuda.Stream(device=device)
+
+    def capture(self, L: int):
+        if L in self.graphs:
+            return
+        g = torch.cuda.CUDAGraph()
+        s = self.stream
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.enc.forward(self.xin, L)          # warm (lazy attribute setup) outside capture
+            with torch.cuda.graph(g, stream=s):
+                y = self.enc.forward(self.xin, L)
+                self.cls.copy_(y[0])
+        torch.cuda.current_stream().wait_stream(s)
+        self.graphs[L] = g
+
+    def capture_all(self, lengths):
+        for L in sorted(set(int(x) for x in lengths)):
+            self.capture(L)
+
+    def run(self, x: torch.Tensor, L: int, out_row: torch.Tensor):
+        """x [L x d] device; out_row [d] device receives the [CLS] vector (stream-ordered)."""
+        self.xin[:L].copy_(x, non_blocking=True)
+        self.graphs[L].replay()
+        out_row.copy_(self.cls, non_blocking=True)
+
+
+def run_requests(cache: GraphCache, ids, lens, X_all: torch.Tensor, offsets, out: torch.Tensor):
+    """Run whole requests (batch 1 each) in id order; out[i] = [CLS] of request ids[i]."""
+    for i, rid in enumerate(ids):
+        L = int(lens[rid])
+        o = int(offsets[rid])
+        cache.run(X_all[o:o + L], L, out[i])
+
+
+def gather_results(ids_local: torch.Tensor, cls_local: torch.Tensor, max_count: int, world: int, rank: int):
+    """Gather (ids, [CLS]) from every rank to rank 0; returns (ids, cls) sorted by id on rank 0,
+    (None, None) elsewhere.  Shards are padded to max_count (id -1 marks padding)."""
+    d = cls_local.shape[1]
+    n = ids_local.shape[0]
+    ids_pad = torch.full((max_count,), -1, dtype=torch.int64, device=cls_local.device)
+    cls_pad = torch.zeros((max_count, d), dtype=cls_local.dtype, device=cls_local.device)
+    ids_pad[:n] = ids_local
+    cls_pad[:n] = cls_local
+    if world == 1:
+        all_ids, all_cls = [ids_pad], [cls_pad]
+    else:
+        all_ids = [torch.empty_like(ids_pad) for _ in range(world)] if rank == 0 else None
+        all_cls = [torch.empty_like(cls_pad) for _ in range(world)] if rank == 0 else None
+        dist.gather(ids_pad, all_ids, dst=0)
+        dist.gather(cls_pad, all_cls, dst=0)
+    if rank != 0:
+        return None, None
+    ids = torch.cat(all_ids)
+    cls = torch.cat(all_cls)
+    keep = ids >= 0
+    ids, cls = ids[keep], cls[keep]
+    order = torch.argsort(ids)
+    return ids[order], cls[order]

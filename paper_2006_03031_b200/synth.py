@@ -145,3 +145,32 @@ def tree_weights(I: int, H: int, seed: int = 0):
     return (to_dtype(g.uniform(-k, k, (3 * H, I)), torch.float32), to_dtype(g.uniform(-k, k, 3 * H), torch.float32),
             to_dtype(g.uniform(-k, k, (5 * H, 2 * H)), torch.float32),
             to_dtype(g.uniform(-k, k, 5 * H), torch.float32))
+
+
+def bert_weights_device(cfg: dict, seed: int = 0, layers: int | None = None, device="cuda"):
+    """Same recipe as bert_weights (N(0, 0.02^2) weights/biases, gamma = 1 + N(0, 0.02^2)) drawn
+    with a seeded torch device generator — used by bench.py, where 604 MB of BERT-large
+    weights per GPU are too slow to draw on the host."""
+    d, f = cfg["d"], cfg["ffn"]
+    n = cfg["layers"] if layers is None else layers
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+
+    def rn(shape, dtype=torch.bfloat16, mean=0.0):
+        return (torch.randn(shape, generator=g, device=device, dtype=torch.float32) * 0.02 + mean).to(dtype)
+
+    out = []
+    for _ in range(n):
+        out.append({"Wqkv": rn((3 * d, d)), "bqkv": rn((3 * d,), torch.float32), "Wo": rn((d, d)),
+                    "bo": rn((d,), torch.float32), "g1": rn((d,), torch.float32, 1.0),
+                    "be1": rn((d,), torch.float32), "W1": rn((f, d)), "b1": rn((f,), torch.float32),
+                    "W2": rn((d, f)), "b2": rn((d,), torch.float32), "g2": rn((d,), torch.float32, 1.0),
+                    "be2": rn((d,), torch.float32)})
+    return out
+
+
+def device_normal(n_rows: int, d: int, seed: int, device="cuda") -> torch.Tensor:
+    """X ~ N(0, 1) [n_rows x d] bf16 drawn on the device (bench request inputs)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    return torch.randn((n_rows, d), generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)

@@ -138,7 +138,7 @@ def test_bert_large_layer_teacher_forced(nb, orc, L):
     assert np.max(np.abs(dd(enc.O) - ref) / D) <= 2e-2
     assert _abs_err(dd(y), orc.layernorm(dd(enc.O), W["g2"], W["be2"])) <= 2e-2
     # free-running (reported): whole layer from the same bf16 input
-    full = orc.bert_layer(dd(x), w[0], H)
+    full = orc.bert_layer(dd(x), W, H)
     drift = _abs_err(dd(y), full)
     print(f"BERT-large layer L={L}: free-running max abs err {drift:.3e}")
     assert drift <= 0.25
