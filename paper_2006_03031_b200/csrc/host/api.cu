@@ -82,6 +82,36 @@ int encode_operand(CUtensorMap *m, const void *base, int64_t inner, int64_t rows
     return NIMBLE_OK;
 }
 
+// Output tile map for the transposed epilogue: out[b*bstride + j*ld + i], i < rows_i (inner),
+// j < rows_j; box {128 i, box_j j, 1}, no swizzle.  TMA clips the box at the tensor bounds, so
+// rows beyond the symbolic extent are never written.
+int encode_out(CUtensorMap *m, void *base, bool f32, int64_t rows_i, int64_t rows_j, int64_t ld, int64_t batch,
+               int64_t bstride, int box_j, int *batch_mid) {
+    cudaError_t e = get_encoder();
+    if (e != cudaSuccess) return cuda_fail("cuTensorMapEncodeTiled lookup", e);
+    const int es = f32 ? 4 : 2;
+    cuuint64_t dims[3], strides[2];
+    cuuint32_t box[3], estr[3] = {1, 1, 1};
+    const bool mid = (batch > 1) && (bstride < ld);
+    dims[0] = (cuuint64_t)rows_i;
+    box[0] = 128;
+    if (mid) {
+        dims[1] = (cuuint64_t)batch;  strides[0] = (cuuint64_t)bstride * es; box[1] = 1;
+        dims[2] = (cuuint64_t)rows_j; strides[1] = (cuuint64_t)ld * es;      box[2] = (cuuint32_t)box_j;
+    } else {
+        dims[1] = (cuuint64_t)rows_j; strides[0] = (cuuint64_t)ld * es;      box[1] = (cuuint32_t)box_j;
+        dims[2] = (cuuint64_t)batch;
+        strides[1] = (cuuint64_t)(batch > 1 ? bstride : ld * rows_j) * es;
+        box[2] = 1;
+    }
+    CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(NIMBLE_E_CUDA, "cuTensorMapEncodeTiled(out) failed (code " + std::to_string((int)r) + ")");
+    *batch_mid = mid ? 1 : 0;
+    return NIMBLE_OK;
+}
+
 bool ext_ok(int64_t x) { return x >= 1 && x <= kMaxExtent; }
 
 // Fill the stage count / smem for a UMMA launch from the dispatch record.
@@ -91,7 +121,7 @@ void plan_pipeline(UmmaLaunch &L, int kb_per_split) {
     if (st > 8) st = 8;
     if (st < 1) st = 1;
     L.p.stages = st;
-    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.n_full, L.p.split);
+    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, L.p.out_f32 ? 4 : 2);
 }
 
 }  // namespace
@@ -142,8 +172,8 @@ extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64
         return NIMBLE_OK;
     }
     if (dt != NIMBLE_BF16) return fail(NIMBLE_E_DTYPE, "nimble_dense_dyn: unknown dtype");
-    if (!aligned16(x) || !aligned16(W) || ((ldx * 2) % 16) || ((ldw * 2) % 16))
-        return fail(NIMBLE_E_ALIGN, "nimble_dense_dyn(bf16): TMA needs 16-B aligned bases and ld*2 % 16 == 0");
+    if (!aligned16(x) || !aligned16(W) || !aligned16(y) || ((ldx * 2) % 16) || ((ldw * 2) % 16) || ((ldy * 2) % 16))
+        return fail(NIMBLE_E_ALIGN, "nimble_dense_dyn(bf16): TMA needs 16-B aligned x/W/y and ld*2 % 16 == 0");
     dispatch_umma_t(1, M, N, K, &d);
     UmmaLaunch L;
     std::memset(&L, 0, sizeof(L));
@@ -167,8 +197,11 @@ extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64
     L.p.bias = bias;
     L.p.res = residual;
     L.p.ld_res = ldr;
+    L.p.a_static = pdl_enabled() ? 1 : 0;   // weights: fetched before the PDL grid-dependency wait
+    L.p.tma_store = 1;
     if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
     if ((st = encode_operand(&L.tmB, x, K, M, ldx, 1, 0, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+    if ((st = encode_out(&L.tmOut, y, false, N, M, ldy, 1, 0, L.p.box_n, &L.p.out_batch_mid)) != NIMBLE_OK) return st;
     plan_pipeline(L, (L.p.kb_total + L.p.split - 1) / L.p.split);
     L.grid = dim3(d.grid[0], d.grid[1], d.grid[2]);
     L.stream = s;
@@ -223,8 +256,11 @@ extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const
         L.p.n_tail = d.r ? d.umma_n_tail : d.umma_n_full;
         L.p.box_n = (L.p.n_tiles == 1) ? L.p.n_tail : d.umma_n_full;
         L.p.transposed = 1;
+        L.p.tma_store = 1;
         if ((st = encode_operand(&L.tmA, B, K, N, ldb, batch, strideB, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
         if ((st = encode_operand(&L.tmB, A, K, M, lda, batch, strideA, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+        if ((st = encode_out(&L.tmOut, Cout, out_dt == NIMBLE_F32, N, M, ldc, batch, strideC, L.p.box_n,
+                             &L.p.out_batch_mid)) != NIMBLE_OK) return st;
     } else {
         // family 2: A rows (M) on the UMMA-M slot, columns of B (N) MN-major on the UMMA-N slot
         L.b_mn_major = 1;
@@ -233,9 +269,11 @@ extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const
         L.p.n_tail = d.umma_n_tail;
         L.p.box_n = d.umma_n_full;
         L.p.transposed = 0;
+        L.p.tma_store = 0;
         if ((st = encode_operand(&L.tmA, A, K, M, lda, batch, strideA, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
         // B is [K x N]: inner dim N (contiguous), K rows; box {64 cols, 64 k-rows}
         if ((st = encode_operand(&L.tmB, B, N, K, ldb, batch, strideB, 64, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+        L.tmOut = L.tmA;                      // unused by the direct epilogue
     }
     plan_pipeline(L, (L.p.kb_total + L.p.split - 1) / L.p.split);
     L.grid = dim3(d.grid[0], d.grid[1], d.grid[2]);

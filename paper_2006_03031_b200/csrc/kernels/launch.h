@@ -1,6 +1,7 @@
 // Host-side launch descriptors shared between api.cu and the kernel translation units.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -29,6 +30,9 @@ struct UmmaParams {
     int32_t b_batch_mid;
     int32_t a_bcast;     // 1: A batch is broadcast (coordinate 0)
     int32_t b_bcast;
+    int32_t a_static;    // 1: A (weights) is not written by in-flight kernels: TMA it before the PDL wait
+    int32_t tma_store;   // 1: transposed epilogue stages the tile in smem and TMA-stores it (tmOut)
+    int32_t out_batch_mid;
     float alpha;
     void *out;
     int64_t ld_out;
@@ -39,7 +43,7 @@ struct UmmaParams {
 };
 
 struct UmmaLaunch {
-    CUtensorMap tmA, tmB;
+    CUtensorMap tmA, tmB, tmOut;
     UmmaParams p;
     dim3 grid;
     int b_mn_major;
@@ -48,7 +52,27 @@ struct UmmaLaunch {
 };
 
 cudaError_t launch_umma_gemm(const UmmaLaunch &L);
-size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int n_full, int split);
+size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes);
+// Programmatic dependent launch (griddepcontrol) on every libnimble launch that supports it.
+bool pdl_enabled();
+
+// Launch `kern` on `s` with the PDL attribute (when enabled).  Every kernel launched this
+// way executes griddepcontrol.wait before touching memory written by earlier kernels.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 int umma_max_stages(int box_n, int b_mn_major);
 
 // fp32 SIMT8 dense (family 0)

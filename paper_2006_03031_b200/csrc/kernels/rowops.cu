@@ -25,6 +25,8 @@ constexpr int kMaxPerLane = 32;   // L <= 1024
 __global__ void __launch_bounds__(256) softmax_rows_kernel(const float *__restrict__ S, int64_t ldS, int64_t strideS,
                                                            __nv_bfloat16 *__restrict__ P, int64_t ldP,
                                                            int64_t strideP, int64_t batch, int64_t rows, int L) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (gw >= batch * rows) return;
     const int lane = threadIdx.x & 31;
@@ -63,6 +65,8 @@ __global__ void __launch_bounds__(128) layernorm_kernel(const __nv_bfloat16 *__r
                                                         float eps, __nv_bfloat16 *__restrict__ Y, int64_t ldy,
                                                         int d) {
     __shared__ float red[4];
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int64_t row = blockIdx.x;
     const __nv_bfloat16 *x = X + row * ldx;
     float v[32];
@@ -131,16 +135,14 @@ cudaError_t launch_softmax_rows(const float *S, int64_t ldS, int64_t strideS, __
                                 int64_t strideP, int64_t batch, int64_t rows, int64_t L, cudaStream_t s) {
     if (L > 32 * kMaxPerLane) return cudaErrorInvalidValue;
     const int64_t warps = batch * rows;
-    softmax_rows_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(S, ldS, strideS, P, ldP, strideP, batch, rows,
-                                                                     (int)L);
-    return cudaGetLastError();
+    return launch_pdl(softmax_rows_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, s, S, ldS, strideS, P, ldP,
+                      strideP, batch, rows, (int)L);
 }
 
 cudaError_t launch_layernorm(const __nv_bfloat16 *X, int64_t ldx, const float *g, const float *b, float eps,
                              __nv_bfloat16 *Y, int64_t ldy, int64_t rows, int64_t d, cudaStream_t s) {
     if (d > 4096 || d % 8) return cudaErrorInvalidValue;
-    layernorm_kernel<<<(unsigned)rows, 128, 0, s>>>(X, ldx, g, b, eps, Y, ldy, (int)d);
-    return cudaGetLastError();
+    return launch_pdl(layernorm_kernel, dim3((unsigned)rows), dim3(128), 0, s, X, ldx, g, b, eps, Y, ldy, (int)d);
 }
 
 }  // namespace nimble

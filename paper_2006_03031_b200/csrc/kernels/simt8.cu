@@ -73,6 +73,8 @@ __device__ __forceinline__ void simt8_tile(const Simt8Params &p, int row0, int r
 // Variant TAIL in 0..7: full tiles unguarded, tail compiled for exactly TAIL rows.
 template <int TAIL>
 __global__ void __launch_bounds__(128) simt8_dense_kernel(const Simt8Params p) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int row0 = blockIdx.y * 8;
     if ((int)blockIdx.y < p.k_tiles) simt8_tile<8>(p, row0, 8);
     else simt8_tile<TAIL>(p, row0, TAIL);
@@ -80,6 +82,8 @@ __global__ void __launch_bounds__(128) simt8_dense_kernel(const Simt8Params p) {
 
 // FALLBACK: every tile guarded at run time.
 __global__ void __launch_bounds__(128) simt8_dense_fallback(const Simt8Params p) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int row0 = blockIdx.y * 8;
     simt8_tile<-1>(p, row0, min(8, p.M - row0));
 }
@@ -88,17 +92,16 @@ __global__ void __launch_bounds__(128) simt8_dense_fallback(const Simt8Params p)
 
 cudaError_t launch_simt8(const Simt8Params &p, int variant, dim3 grid, cudaStream_t s) {
     switch (variant) {
-        case 0: simt8_dense_kernel<0><<<grid, 128, 0, s>>>(p); break;
-        case 1: simt8_dense_kernel<1><<<grid, 128, 0, s>>>(p); break;
-        case 2: simt8_dense_kernel<2><<<grid, 128, 0, s>>>(p); break;
-        case 3: simt8_dense_kernel<3><<<grid, 128, 0, s>>>(p); break;
-        case 4: simt8_dense_kernel<4><<<grid, 128, 0, s>>>(p); break;
-        case 5: simt8_dense_kernel<5><<<grid, 128, 0, s>>>(p); break;
-        case 6: simt8_dense_kernel<6><<<grid, 128, 0, s>>>(p); break;
-        case 7: simt8_dense_kernel<7><<<grid, 128, 0, s>>>(p); break;
-        default: simt8_dense_fallback<<<grid, 128, 0, s>>>(p); break;
+        case 0: return launch_pdl(simt8_dense_kernel<0>, grid, dim3(128), 0, s, p);
+        case 1: return launch_pdl(simt8_dense_kernel<1>, grid, dim3(128), 0, s, p);
+        case 2: return launch_pdl(simt8_dense_kernel<2>, grid, dim3(128), 0, s, p);
+        case 3: return launch_pdl(simt8_dense_kernel<3>, grid, dim3(128), 0, s, p);
+        case 4: return launch_pdl(simt8_dense_kernel<4>, grid, dim3(128), 0, s, p);
+        case 5: return launch_pdl(simt8_dense_kernel<5>, grid, dim3(128), 0, s, p);
+        case 6: return launch_pdl(simt8_dense_kernel<6>, grid, dim3(128), 0, s, p);
+        case 7: return launch_pdl(simt8_dense_kernel<7>, grid, dim3(128), 0, s, p);
+        default: return launch_pdl(simt8_dense_fallback, grid, dim3(128), 0, s, p);
     }
-    return cudaGetLastError();
 }
 
 }  // namespace nimble

@@ -20,6 +20,8 @@ template <int G>
 __global__ void __launch_bounds__(kNodes * kUnits) treelstm_level_kernel(const TreeParams p) {
     __shared__ float As[kNodes][kKc];
     __shared__ float Ws[G][kUnits][kKc + 1];
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int r = threadIdx.x >> 5;            // node within the tile (warp-uniform)
     const int u = threadIdx.x & 31;            // hidden unit within the tile
     const int m = blockIdx.y * kNodes + r;
@@ -80,11 +82,8 @@ __global__ void __launch_bounds__(kNodes * kUnits) treelstm_level_kernel(const T
 
 cudaError_t launch_treelstm_level(const TreeParams &p, cudaStream_t s) {
     dim3 grid((p.H + kUnits - 1) / kUnits, (p.M + kNodes - 1) / kNodes);
-    if (p.is_leaf)
-        treelstm_level_kernel<3><<<grid, kNodes * kUnits, 0, s>>>(p);
-    else
-        treelstm_level_kernel<5><<<grid, kNodes * kUnits, 0, s>>>(p);
-    return cudaGetLastError();
+    if (p.is_leaf) return launch_pdl(treelstm_level_kernel<3>, grid, dim3(kNodes * kUnits), 0, s, p);
+    return launch_pdl(treelstm_level_kernel<5>, grid, dim3(kNodes * kUnits), 0, s, p);
 }
 
 }  // namespace nimble
