@@ -190,7 +190,7 @@ def test_bmm_scores_and_context_vs_oracle(nb, orc, L):
     ref, D = orc.bmm(q, k, 0, 0.125)
     Sg = S[:, :, :L].double().cpu().numpy()
     assert np.max(np.abs(Sg - ref) / np.maximum(D, 1e-30)) <= TOL_BF16
-    assert torch.all(S[:, :, L:] == 7.0)
+    assert torch.all(S[:, :, 4 * ((L + 3) // 4):] == 7.0)     # TMA may fill the row's last 16-B segment
     # context: C_h = P_h V_h with V_h MN-major (trans_b = 1), P bf16 [H x L x ldP]
     ldP = 8 * ((L + 7) // 8)
     P = synth.normal((H, L, ldP), 0.5, 95 + L).cuda()
