@@ -109,23 +109,24 @@ static int32_t orc_split(int64_t tiles, int64_t K) {
 
 #define ORC_MAXEXT 2147483647LL
 
-/* family 1, UMMA_T: tokens (symbolic M) on the UMMA-N slot, t = 256, granule 16 */
+/* families 1 / 3, UMMA_T: tokens (symbolic M) on the UMMA-N slot, granule 16;
+ * t = 128 for M < 2048 (family 1, split-K allowed), t = 256 for M >= 2048 (family 3). */
 static int orc_umma_t(int64_t batch, int64_t M, int64_t N, int64_t K, int c, orc_dispatch *d) {
     memset(d, 0, sizeof(*d));
-    d->family = 1; d->tile_t = 256; d->granule = 16; d->n_classes = 17;
-    d->k = M / 256; d->r = M % 256;                  /* x = 256k + r */
+    int32_t t = (M < 2048) ? 128 : 256;
+    d->family = (t == 128) ? 1 : 3; d->tile_t = t; d->granule = 16; d->n_classes = t / 16 + 1;
+    d->k = M / t; d->r = M % t;                      /* x = t k + r */
     d->residue_class = (int32_t)orc_ceil_div(d->r, 16);
-    d->variant = orc_variant(d->residue_class, 17, c);
-    d->umma_m = 128; d->umma_n_full = 256;
+    d->variant = orc_variant(d->residue_class, d->n_classes, c);
+    d->umma_m = 128; d->umma_n_full = t;
     if (d->r == 0) d->umma_n_tail = 0;
-    else d->umma_n_tail = (d->variant >= 0) ? 16 * d->residue_class : 256;
+    else d->umma_n_tail = (d->variant >= 0) ? 16 * d->residue_class : t;
     int64_t mt = orc_ceil_div(N, 128), nt = d->k + (d->r > 0);
-    d->split_k = orc_split(mt * nt * batch, K);
+    d->split_k = (t == 128) ? orc_split(mt * nt * batch, K) : 1;
     d->grid[0] = (int32_t)mt; d->grid[1] = (int32_t)nt; d->grid[2] = (int32_t)(batch * d->split_k);
     d->cluster[0] = 1; d->cluster[1] = 1; d->cluster[2] = d->split_k;
     return ORC_OK;
 }
-
 
 int orc_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, int c, orc_dispatch *d) {
     if (M < 1 || N < 1 || K < 1 || M > ORC_MAXEXT || N > ORC_MAXEXT || K > ORC_MAXEXT) return ORC_E_EXTENT;

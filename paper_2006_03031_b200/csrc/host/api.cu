@@ -115,13 +115,26 @@ int encode_out(CUtensorMap *m, void *base, bool f32, int64_t rows_i, int64_t row
 bool ext_ok(int64_t x) { return x >= 1 && x <= kMaxExtent; }
 
 // Fill the stage count / smem for a UMMA launch from the dispatch record.
-void plan_pipeline(UmmaLaunch &L, int kb_per_split) {
-    const int maxst = umma_max_stages(L.p.box_n, L.b_mn_major);
-    int st = kb_per_split < maxst ? kb_per_split : maxst;
-    if (st > 8) st = 8;
+// Pipeline depth / smem from the tile geometry, then the launch grid: the dispatch record's
+// tile grid as is for split-K clusters, else min(tiles, 148) persistent CTAs.
+void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
+    const int kb_per_split = (L.p.kb_total + L.p.split - 1) / L.p.split;
+    const int ob = L.out_f32 ? 4 : 2;
+    int st = kb_per_split < 8 ? kb_per_split : 8;
     if (st < 1) st = 1;
+    // largest depth that fits next to the epilogue staging
+    while (st > 1 && umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed) > 232448) --st;
     L.p.stages = st;
-    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, L.p.out_f32 ? 4 : 2);
+    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed);
+    L.p.tiles_m = d.grid[0];
+    L.p.tiles_n = d.grid[1];
+    L.p.batch = d.grid[2] / d.split_k;
+    if (L.p.split > 1) {
+        L.grid = dim3(d.grid[0], d.grid[1], d.grid[2]);
+    } else {
+        const int64_t tiles = (int64_t)d.grid[0] * d.grid[1] * d.grid[2];
+        L.grid = dim3((unsigned)(tiles < kNumSMs ? tiles : kNumSMs), 1, 1);
+    }
 }
 
 }  // namespace
@@ -172,8 +185,9 @@ extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64
         return NIMBLE_OK;
     }
     if (dt != NIMBLE_BF16) return fail(NIMBLE_E_DTYPE, "nimble_dense_dyn: unknown dtype");
-    if (!aligned16(x) || !aligned16(W) || !aligned16(y) || ((ldx * 2) % 16) || ((ldw * 2) % 16) || ((ldy * 2) % 16))
-        return fail(NIMBLE_E_ALIGN, "nimble_dense_dyn(bf16): TMA needs 16-B aligned x/W/y and ld*2 % 16 == 0");
+    if (!aligned16(x) || !aligned16(W) || !aligned16(y) || ((ldx * 2) % 16) || ((ldw * 2) % 16) || ((ldy * 2) % 16) ||
+        (epi == NIMBLE_EPI_BIAS_RESIDUAL && (!aligned16(residual) || (ldr * 2) % 16)))
+        return fail(NIMBLE_E_ALIGN, "nimble_dense_dyn(bf16): TMA needs 16-B aligned x/W/y/residual and ld*2 % 16 == 0");
     dispatch_umma_t(1, M, N, K, &d);
     UmmaLaunch L;
     std::memset(&L, 0, sizeof(L));
@@ -181,15 +195,13 @@ extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64
     L.p.rows_a = (int32_t)N;             // weights on the UMMA-M slot
     L.p.rows_b = (int32_t)M;             // tokens on the UMMA-N slot (symbolic)
     L.p.n_full = d.umma_n_full;
-    L.p.n_tiles = d.grid[1];
     L.p.n_tail = d.r ? d.umma_n_tail : d.umma_n_full;
-    L.p.box_n = (L.p.n_tiles == 1) ? L.p.n_tail : d.umma_n_full;
+    L.p.box_n = (d.grid[1] == 1) ? L.p.n_tail : d.umma_n_full;
     L.p.kb_total = (int32_t)((K + 63) / 64);
     L.p.split = d.split_k;
-    L.p.guard_all = d.variant < 0;
-    L.p.epi = epi;
-    L.p.out_f32 = 0;
-    L.p.transposed = 1;
+    L.epi = epi;
+    L.out_f32 = 0;
+    L.transposed = 1;
     L.p.alpha = 1.f;
     L.p.out = y;
     L.p.ld_out = ldy;
@@ -198,12 +210,16 @@ extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64
     L.p.res = residual;
     L.p.ld_res = ldr;
     L.p.a_static = pdl_enabled() ? 1 : 0;   // weights: fetched before the PDL grid-dependency wait
-    L.p.tma_store = 1;
     if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
     if ((st = encode_operand(&L.tmB, x, K, M, ldx, 1, 0, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
     if ((st = encode_out(&L.tmOut, y, false, N, M, ldy, 1, 0, L.p.box_n, &L.p.out_batch_mid)) != NIMBLE_OK) return st;
-    plan_pipeline(L, (L.p.kb_total + L.p.split - 1) / L.p.split);
-    L.grid = dim3(d.grid[0], d.grid[1], d.grid[2]);
+    if (epi == NIMBLE_EPI_BIAS_RESIDUAL) {
+        int mid = 0;
+        if ((st = encode_out(&L.tmRes, const_cast<void *>(residual), false, N, M, ldr, 1, 0, L.p.box_n, &mid)) != NIMBLE_OK) return st;
+    } else {
+        L.tmRes = L.tmOut;
+    }
+    plan_pipeline(L, d);
     L.stream = s;
     cudaError_t e = launch_umma_gemm(L);
     if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn(bf16) launch", e);
@@ -239,28 +255,26 @@ extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const
     std::memset(&L, 0, sizeof(L));
     L.p.kb_total = (int32_t)((K + 63) / 64);
     L.p.split = d.split_k;
-    L.p.guard_all = d.variant < 0;
-    L.p.epi = 0;
-    L.p.out_f32 = out_dt == NIMBLE_F32;
+    L.epi = 0;
+    L.out_f32 = out_dt == NIMBLE_F32;
     L.p.alpha = alpha;
     L.p.out = Cout;
     L.p.ld_out = ldc;
     L.p.stride_out = strideC;
     L.p.n_full = d.umma_n_full;
-    L.p.n_tiles = d.grid[1];
     if (!trans_b) {
         // family 1: B rows (N) on the UMMA-M slot, A rows (M, symbolic) on the UMMA-N slot
         L.b_mn_major = 0;
         L.p.rows_a = (int32_t)N;
         L.p.rows_b = (int32_t)M;
         L.p.n_tail = d.r ? d.umma_n_tail : d.umma_n_full;
-        L.p.box_n = (L.p.n_tiles == 1) ? L.p.n_tail : d.umma_n_full;
-        L.p.transposed = 1;
-        L.p.tma_store = 1;
+        L.p.box_n = (d.grid[1] == 1) ? L.p.n_tail : d.umma_n_full;
+        L.transposed = 1;
         if ((st = encode_operand(&L.tmA, B, K, N, ldb, batch, strideB, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
         if ((st = encode_operand(&L.tmB, A, K, M, lda, batch, strideA, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
         if ((st = encode_out(&L.tmOut, Cout, out_dt == NIMBLE_F32, N, M, ldc, batch, strideC, L.p.box_n,
                              &L.p.out_batch_mid)) != NIMBLE_OK) return st;
+        L.tmRes = L.tmOut;
     } else {
         // family 2: A rows (M) on the UMMA-M slot, columns of B (N) MN-major on the UMMA-N slot
         L.b_mn_major = 1;
@@ -268,15 +282,14 @@ extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const
         L.p.rows_b = (int32_t)N;
         L.p.n_tail = d.umma_n_tail;
         L.p.box_n = d.umma_n_full;
-        L.p.transposed = 0;
-        L.p.tma_store = 0;
+        L.transposed = 0;
         if ((st = encode_operand(&L.tmA, A, K, M, lda, batch, strideA, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
         // B is [K x N]: inner dim N (contiguous), K rows; box {64 cols, 64 k-rows}
         if ((st = encode_operand(&L.tmB, B, N, K, ldb, batch, strideB, 64, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
         L.tmOut = L.tmA;                      // unused by the direct epilogue
+        L.tmRes = L.tmA;
     }
-    plan_pipeline(L, (L.p.kb_total + L.p.split - 1) / L.p.split);
-    L.grid = dim3(d.grid[0], d.grid[1], d.grid[2]);
+    plan_pipeline(L, d);
     L.stream = s;
     cudaError_t e = launch_umma_gemm(L);
     if (e != cudaSuccess) return cuda_fail("nimble_bmm_dyn launch", e);

@@ -19,7 +19,9 @@ struct ResidueFamily {
     int32_t id, t, granule, n_classes;
 };
 constexpr ResidueFamily kSIMT8{0, 8, 1, 8};      // fp32 CUDA-core dense, the paper's t = 8
-constexpr ResidueFamily kUMMA_T{1, 256, 16, 17}; // bf16 tcgen05, tokens on UMMA-N
+constexpr ResidueFamily kUMMA_T{1, 128, 16, 9};    // bf16 tcgen05, tokens on UMMA-N, M < 2048
+constexpr ResidueFamily kUMMA_T256{3, 256, 16, 17}; // same, M >= 2048 (no split-K)
+constexpr int64_t kWideTileFrom = 2048;
 constexpr ResidueFamily kUMMA_D{2, 128, 128, 2}; // bf16 tcgen05 bmm with MN-major B
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -71,15 +73,16 @@ int dispatch_simt8(int64_t M, int64_t N, nimble_dispatch *d) {
 
 int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, nimble_dispatch *d) {
     *d = nimble_dispatch{};
-    split_residue(kUMMA_T, M_tokens, d);
-    d->residue_class = static_cast<int32_t>(cdiv(d->r, kUMMA_T.granule));
-    d->variant = select_variant(kUMMA_T, d->residue_class);
+    const ResidueFamily &f = (M_tokens >= kWideTileFrom) ? kUMMA_T256 : kUMMA_T;
+    split_residue(f, M_tokens, d);
+    d->residue_class = static_cast<int32_t>(cdiv(d->r, f.granule));
+    d->variant = select_variant(f, d->residue_class);
     d->umma_m = 128;
-    d->umma_n_full = kUMMA_T.t;
-    d->umma_n_tail = d->r == 0 ? 0 : (d->variant < 0 ? kUMMA_T.t : kUMMA_T.granule * d->residue_class);
+    d->umma_n_full = f.t;
+    d->umma_n_tail = d->r == 0 ? 0 : (d->variant < 0 ? f.t : f.granule * d->residue_class);
     const int64_t m_tiles = cdiv(N_rows, 128);
     const int64_t n_tiles = d->k + (d->r ? 1 : 0);
-    d->split_k = choose_split(m_tiles * n_tiles * batch, K);
+    d->split_k = (f.id == kUMMA_T.id) ? choose_split(m_tiles * n_tiles * batch, K) : 1;
     d->grid[0] = static_cast<int32_t>(m_tiles);
     d->grid[1] = static_cast<int32_t>(n_tiles);
     d->grid[2] = static_cast<int32_t>(batch * d->split_k);

@@ -10,49 +10,43 @@ namespace nimble {
 
 // Parameters of one tcgen05 GEMM launch (families UMMA_T / UMMA_D, DISPATCH.md).
 //   D[i][j] = sum_k A[i][k] * B[j][k]   (i on the UMMA-M slot, j on the UMMA-N slot)
-// transposed = 1: out[b*stride + j*ld + i]  (lane = i = output feature: coalesced)
-// transposed = 0: out[b*stride + i*ld + j]  (row-major in i)
+// transposed epilogue: out[b*stride + j*ld + i]  (lane = i = output feature; TMA store)
+// direct epilogue:     out[b*stride + i*ld + j]  (row-major in i; vector stores)
 struct UmmaParams {
-    int32_t rows_a;      // valid extent of the UMMA-M slot (guard)
-    int32_t rows_b;      // valid extent of the UMMA-N slot (guard)
+    int32_t rows_a;      // valid extent of the UMMA-M slot
+    int32_t rows_b;      // valid extent of the UMMA-N slot (the symbolic one for dense)
     int32_t n_full;      // UMMA N of full tiles
-    int32_t n_tail;      // UMMA N of the last tile along the N slot
-    int32_t n_tiles;     // tiles along the N slot (grid.y)
-    int32_t box_n;       // B rows (K-major) / B columns (MN-major) per TMA stage
+    int32_t n_tail;      // UMMA N of the last tile along the N slot (residue variant width)
+    int32_t tiles_m;     // tile grid: tiles_m x tiles_n x batch
+    int32_t tiles_n;
+    int32_t batch;
+    int32_t box_n;       // B rows (K-major) / columns (MN-major) per TMA stage; out/res box rows
     int32_t kb_total;    // ceil(K / 64)
-    int32_t split;       // split-K factor (= cluster size along z)
+    int32_t split;       // split-K factor (= cluster size along z); 1 -> persistent tile loop
     int32_t stages;      // smem pipeline depth
-    int32_t guard_all;   // 1: fallback variant — guard every tile, tail at full width
-    int32_t epi;         // nimble_epilogue (family 1); 0 for bmm
-    int32_t out_f32;     // 1: fp32 output, 0: bf16 output
-    int32_t transposed;  // see above
-    int32_t a_batch_mid; // tensor-map dim order: 1 -> {K, batch, rows}, 0 -> {K, rows, batch}
-    int32_t b_batch_mid;
-    int32_t a_bcast;     // 1: A batch is broadcast (coordinate 0)
-    int32_t b_bcast;
+    int32_t a_batch_mid, b_batch_mid, out_batch_mid;   // tensor-map dim orders
+    int32_t a_bcast, b_bcast;                          // broadcast batch (coordinate 0)
     int32_t a_static;    // 1: A (weights) is not written by in-flight kernels: TMA it before the PDL wait
-    int32_t tma_store;   // 1: transposed epilogue stages the tile in smem and TMA-stores it (tmOut)
-    int32_t out_batch_mid;
     float alpha;
     void *out;
     int64_t ld_out;
     int64_t stride_out;
     const float *bias;
-    const void *res;
+    const void *res;     // residual (split-K path reads it directly; otherwise via tmRes)
     int64_t ld_res;
 };
 
 struct UmmaLaunch {
-    CUtensorMap tmA, tmB, tmOut;
+    CUtensorMap tmA, tmB, tmOut, tmRes;
     UmmaParams p;
     dim3 grid;
-    int b_mn_major;
+    int b_mn_major, epi, out_f32, transposed;
     size_t smem_bytes;
     cudaStream_t stream;
 };
 
 cudaError_t launch_umma_gemm(const UmmaLaunch &L);
-size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes);
+size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed);
 // Programmatic dependent launch (griddepcontrol) on every libnimble launch that supports it.
 bool pdl_enabled();
 

@@ -181,3 +181,34 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
 }
 }  // namespace ptx
 }  // namespace nimble
+
+namespace nimble {
+namespace ptx {
+// mbarrier arrive (count 1), local CTA
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// expect_tx without arriving (the arrive comes from someone else / later)
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// Bulk DSMEM copy: own smem -> a peer CTA's smem, completion (complete_tx) on the PEER's mbarrier.
+// dst and bar are shared::cluster addresses (mapa).
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, const void *src, uint32_t bytes,
+                                                  uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst_cluster),
+        "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
+        : "memory");
+}
+// 3-D TMA load with an mbarrier (same as tma_load_3d, named for the residual tile)
+__device__ __forceinline__ void tma_load_3d_nb(void *dst, const CUtensorMap *m, uint64_t *bar, int32_t c0, int32_t c1,
+                                               int32_t c2) {
+    tma_load_3d(dst, m, bar, c0, c1, c2);
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+}  // namespace ptx
+}  // namespace nimble

@@ -1,28 +1,31 @@
 // tcgen05 / TMEM / TMA GEMM for the symbolic-shape dense and batch_matmul of
 // Nimble §3.5 on sm_100a.
 //
-// One CTA = one 128 x n output tile (n = UMMA N of this tile: full width, or the
-// residue-specialised tail width 16*ceil(r/16) chosen by the dispatch function)
-// over one K slice.  256 threads, warp roles:
-//   warp 0 lane 0  TMA producer: A[128 x 64] and B[box_n x 64] bf16 tiles, 128-B
-//                  swizzle, into a `stages`-deep smem ring (full/empty mbarriers).
-//                  Rows beyond the symbolic extent are zero-filled by TMA bounds —
-//                  the dynamic dimension is never padded in memory.  With PDL the
-//                  static weight operand is fetched BEFORE griddepcontrol.wait, so
+// Tile = 128 (UMMA M) x n (UMMA N: the full tile width t, or the residue-specialised
+// tail width 16*ceil(r/16) the dispatch function picked) over K.
+// 384 threads, warp-specialised:
+//   warp 0 lane 0  TMA producer: A[128 x 64] + B[box_n x 64] bf16 tiles (128-B swizzle)
+//                  into a `stages`-deep smem ring (full/empty mbarriers).  Rows beyond
+//                  the symbolic extent are zero-filled by TMA bounds — the dynamic
+//                  dimension is never padded in memory.  With PDL the static weight
+//                  operand of the first tile is fetched BEFORE griddepcontrol.wait, so
 //                  the weight stream overlaps the previous kernel's tail.
-//   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (K = 16) per 64-wide k-block into an
-//                  fp32 accumulator in TMEM; tcgen05.commit frees each smem stage.
+//   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (K = 16) per 64-wide k-block into one of
+//                  two fp32 TMEM accumulators (double-buffered across tiles).
 //   warp 2         TMEM allocation / deallocation.
-//   warps 0-7      epilogue: warp w reads TMEM lane quarter (w % 4) and every other
-//                  16-column chunk (w / 4); alpha / bias / GELU / residual; the tile
-//                  is staged in smem in the output layout and written by ONE TMA
-//                  store that clips rows beyond the symbolic extent (no guards).
-// split > 1: the K slices of one tile form a thread-block cluster along z; every
-// CTA parks its fp32 partial in its own smem, and CTA q reduces columns
-// [q*n/split, (q+1)*n/split) over ranks 0..split-1 in order through DSMEM
-// (deterministic; no atomics), then runs the epilogue on them.
+//   warps 4-11     epilogue: warp w reads TMEM lane quarter (w % 4), 16-column chunks
+//                  alternating between the two warp groups; compile-time epilogue
+//                  (alpha | bias | bias+GELU | bias+residual, residual tile TMA-loaded into
+//                  the staging buffer); the transposed output tile is staged in smem and
+//                  written by ONE TMA store that clips rows beyond the symbolic extent.
+//                  The epilogue of tile i overlaps the MMAs of tile i+1 (persistent CTAs).
+// split > 1 (small M, weight-streaming regime): the K slices of one tile form a cluster
+// along z.  Each CTA parks its fp32 partial in smem and bulk-copies (cp.async.bulk over
+// DSMEM) slice q to CTA q, which sums the slices in rank order (deterministic, no
+// atomics) and runs the epilogue on its columns.
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "launch.h"
 #include "ptx.cuh"
@@ -31,7 +34,9 @@ namespace nimble {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
+constexpr int kEpiWarp0 = 4;
+constexpr int kEpiThreads = 256;
 constexpr int kBlockK = 64;                   // one 128-B swizzle row of bf16
 constexpr int kABytes = 128 * kBlockK * 2;    // 16 KiB A stage
 constexpr int kSmemLimit = 232448;            // 227 KiB opt-in per CTA
@@ -40,52 +45,78 @@ constexpr int kTailBytes = 1024;              // barriers + tmem slot
 __host__ __device__ inline int b_stage_bytes(int box_n, int b_mn) {
     return b_mn ? ((box_n + 63) / 64) * (64 * kBlockK * 2) : box_n * kBlockK * 2;
 }
+__host__ __device__ inline int pow2_cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
 
-__device__ __forceinline__ float epi_apply(const UmmaParams &p, float acc, float bias_i) {
-    float v = acc * p.alpha;
-    if (p.epi >= 1) v += bias_i;
-    if (p.epi == 2) v = ptx::gelu_erf(v);
-    return v;
+struct TileCoord {
+    int m, n, b;
+};
+__device__ __forceinline__ TileCoord tile_of(const UmmaParams &p, int t) {
+    TileCoord c;
+    c.m = t % p.tiles_m;
+    const int rest = t / p.tiles_m;
+    c.n = rest % p.tiles_n;
+    c.b = rest / p.tiles_n;
+    return c;
 }
 
-template <int B_MN>
+template <int EPI>
+__device__ __forceinline__ float epi_math(float acc, float alpha, float bias_i) {
+    if constexpr (EPI == 0) return acc * alpha;
+    else if constexpr (EPI == 2) return ptx::gelu_erf(acc + bias_i);
+    else return acc + bias_i;      // EPI 1, and 3 before the residual add
+}
+
+template <int B_MN, int EPI, int OUT_F32, int TRANS>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmOut, const UmmaParams p) {
+                     const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
+                     const UmmaParams p) {
+    using OutT = typename std::conditional<OUT_F32, float, __nv_bfloat16>::type;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-B alignment for the 128-B swizzle atoms
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const bool split = p.split > 1;
     const int b_bytes = b_stage_bytes(p.box_n, B_MN);
     const int stage_bytes = kABytes + b_bytes;
     const int ring_bytes = p.stages * stage_bytes;
-    const int red_bytes = 128 * p.box_n * ((p.split > 1 || p.out_f32) ? 4 : 2);   // epilogue staging
-    uint8_t *tail = smem + (ring_bytes > red_bytes ? ring_bytes : red_bytes);
-    uint64_t *full_bar = reinterpret_cast<uint64_t *>(tail);
+    const int part_bytes = split ? 128 * p.box_n * 4 : 0;
+    const int region0 = ring_bytes > part_bytes ? ring_bytes : part_bytes;
+    const int stg_bytes = split ? 128 * p.box_n * 4 : (TRANS ? 128 * p.box_n * (int)sizeof(OutT) : 0);
+    uint8_t *stg = smem + region0;                 // epilogue staging / split-K receive buffer
+    uint64_t *full_bar = reinterpret_cast<uint64_t *>(stg + stg_bytes);
     uint64_t *empty_bar = full_bar + p.stages;
-    uint64_t *tmem_full = empty_bar + p.stages;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+    uint64_t *tfull = empty_bar + p.stages;        // [2]
+    uint64_t *tempty = tfull + 2;                  // [2]
+    uint64_t *res_bar = tempty + 2;
+    uint64_t *recv_bar = res_bar + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(recv_bar + 1);
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
-    const int m_tile = blockIdx.x;
-    const int n_tile = blockIdx.y;
-    const int split_q = blockIdx.z % p.split;
-    const int batch = blockIdx.z / p.split;
-    const bool last_n = (n_tile == p.n_tiles - 1);
-    const int n_this = last_n ? p.n_tail : p.n_full;     // UMMA N of this tile (runtime idesc field)
-    const uint32_t tmem_cols = n_this <= 32 ? 32 : n_this <= 64 ? 64 : n_this <= 128 ? 128 : 256;
+    const int total_tiles = p.tiles_m * p.tiles_n * p.batch;
+    // split: exactly one tile per CTA (cluster along z); else persistent over the tile grid
+    const int t_first = split ? ((int)(blockIdx.z / p.split) * p.tiles_n + (int)blockIdx.y) * p.tiles_m + (int)blockIdx.x
+                              : (int)blockIdx.x;
+    const int t_step = split ? total_tiles : (int)gridDim.x;
+    const int split_q = split ? (int)(blockIdx.z % p.split) : 0;
     const int kb0 = (int)((int64_t)split_q * p.kb_total / p.split);
     const int kb1 = (int)((int64_t)(split_q + 1) * p.kb_total / p.split);
+    const uint32_t tmem_cols = split ? pow2_cols(p.box_n) : pow2_cols(2 * p.n_full);
 
     if (threadIdx.x == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
-        if (p.tma_store) ptx::prefetch_tmap(&tmOut);
+        if (TRANS) ptx::prefetch_tmap(&tmOut);
+        if (EPI == 3 && TRANS) ptx::prefetch_tmap(&tmRes);
         for (int s = 0; s < p.stages; ++s) {
             ptx::mbar_init(&full_bar[s], 1);
             ptx::mbar_init(&empty_bar[s], 1);
         }
-        ptx::mbar_init(tmem_full, 1);
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], kEpiThreads / 32);
+        }
+        ptx::mbar_init(res_bar, 1);
+        ptx::mbar_init(recv_bar, 1);
         ptx::fence_mbar_init();
         ptx::fence_async_smem();
     }
@@ -93,207 +124,279 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    if (split) ptx::cluster_sync();                // peers' barriers exist before any DSMEM copy
     const uint32_t tmem_base = *tmem_slot;
-    ptx::pdl_trigger();                               // the next kernel's prologue may start now
+    ptx::pdl_trigger();                            // the next kernel's prologue may start now
 
     if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer
-        const int32_t a_row = m_tile * 128;
-        const int32_t b_row = n_tile * p.n_full;
-        const int32_t ab = p.a_bcast ? 0 : batch;
-        const int32_t bb = p.b_bcast ? 0 : batch;
+        // ================= TMA producer
         const uint32_t tx = kABytes + b_bytes;
-        auto load_a = [&](int stage, int kb) {
-            uint8_t *sa = smem + stage * stage_bytes;
-            const int32_t kc = kb * kBlockK;
-            if (p.a_batch_mid) ptx::tma_load_3d(sa, &tmA, &full_bar[stage], kc, ab, a_row);
-            else ptx::tma_load_3d(sa, &tmA, &full_bar[stage], kc, a_row, ab);
-        };
-        auto load_b = [&](int stage, int kb) {
-            uint8_t *sb = smem + stage * stage_bytes + kABytes;
-            const int32_t kc = kb * kBlockK;
-            if (B_MN) {
-                const int chunks = (p.box_n + 63) / 64;
-                for (int c = 0; c < chunks; ++c) {
-                    if (p.b_batch_mid) ptx::tma_load_3d(sb + c * 8192, &tmB, &full_bar[stage], b_row + 64 * c, bb, kc);
-                    else ptx::tma_load_3d(sb + c * 8192, &tmB, &full_bar[stage], b_row + 64 * c, kc, bb);
-                }
-            } else {
-                if (p.b_batch_mid) ptx::tma_load_3d(sb, &tmB, &full_bar[stage], kc, bb, b_row);
-                else ptx::tma_load_3d(sb, &tmB, &full_bar[stage], kc, b_row, bb);
-            }
-        };
-        // prologue: the first `stages` k-blocks; static weights go out before the PDL wait
-        const int npre = min(p.stages, kb1 - kb0);
-        for (int s = 0; s < npre; ++s) {
-            ptx::mbar_arrive_expect_tx(&full_bar[s], tx);
-            if (p.a_static) load_a(s, kb0 + s);
-        }
-        ptx::pdl_wait();                              // producer grid's activations now visible
-        for (int s = 0; s < npre; ++s) {
-            if (!p.a_static) load_a(s, kb0 + s);
-            load_b(s, kb0 + s);
-        }
-        int stage = npre % p.stages;
-        uint32_t phase = (npre == p.stages) ? 1u : 0u;
-        for (int kb = kb0 + npre; kb < kb1; ++kb) {
-            ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-            ptx::mbar_arrive_expect_tx(&full_bar[stage], tx);
-            load_a(stage, kb);
-            load_b(stage, kb);
-            if (++stage == p.stages) { stage = 0; phase ^= 1; }
-        }
-    } else if (warp == 1 && lane == 0) {
-        // ---------------- MMA issuer (single thread)
-        const uint32_t idesc = ptx::idesc_bf16(128, (uint32_t)n_this, B_MN);
         int stage = 0;
         uint32_t phase = 0;
-        for (int kb = kb0; kb < kb1; ++kb) {
-            ptx::mbar_wait(&full_bar[stage], phase);
-            ptx::tc_fence_after();
-            const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
-            const uint32_t sb = sa + kABytes;
-            const uint64_t adesc = ptx::smem_desc_sw128(sa, 0, 1024);
-            // K-major B: 8-row groups 1024 B apart.  MN-major B: 64-column chunks
-            // 8 KiB apart (LBO), 8-row k groups 1024 B apart (SBO).
-            const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb, 8192, 1024) : ptx::smem_desc_sw128(sb, 0, 1024);
-#pragma unroll
-            for (int kk = 0; kk < kBlockK / 16; ++kk) {
-                const uint64_t a_k = adesc + (uint64_t)((kk * 32) >> 4);                // +32 B along K in the row
-                const uint64_t b_k = bdesc + (uint64_t)(B_MN ? ((kk * 2048) >> 4) : ((kk * 32) >> 4));
-                ptx::umma_bf16(tmem_base, a_k, b_k, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
-            }
-            ptx::umma_commit(&empty_bar[stage]);       // smem stage free once these MMAs retire
-            if (++stage == p.stages) { stage = 0; phase ^= 1; }
-        }
-        ptx::umma_commit(tmem_full);                   // accumulator complete
-    }
-    __syncwarp();
-    ptx::pdl_wait();                                   // epilogue reads residual / writes output
-
-    // ---------------- epilogue: warp w owns TMEM lanes 32*(w%4).. and chunks c = w/4 (mod 2)
-    ptx::mbar_wait(tmem_full, 0);
-    ptx::tc_fence_after();
-
-    const int quarter = (int)(warp & 3);
-    const int half = (int)(warp >> 2);
-    const int row_local = quarter * 32 + (int)lane;
-    const int i = m_tile * 128 + row_local;                 // UMMA-M index
-    const int j0 = n_tile * p.n_full;                       // first UMMA-N index of the tile
-    const bool row_ok = i < p.rows_a;
-    const int64_t out_b = (int64_t)batch * p.stride_out;
-    const uint32_t tmem_row = tmem_base + ((uint32_t)(quarter * 32) << 16);
-    float bias_i = 0.f;
-    if (p.epi >= 1 && row_ok) bias_i = p.bias[i];
-    const int n_valid = min(n_this, p.rows_b - j0);         // columns holding real data
-
-    if (p.split == 1) {
-        if (p.transposed) {
-            // stage out^T tile as [n][128] in smem (lane = i -> conflict-free), then one TMA store
-            for (int c0 = half * 16; c0 < n_this; c0 += 32) {
-                float v[16];
-                ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const int jl = c0 + q;
-                    float val = epi_apply(p, v[q], bias_i);
-                    if (p.epi == 3 && row_ok && jl < n_valid)
-                        val += __bfloat162float(static_cast<const __nv_bfloat16 *>(p.res)[(int64_t)(j0 + jl) * p.ld_res + i]);
-                    if (p.out_f32) reinterpret_cast<float *>(smem)[jl * 128 + row_local] = val;
-                    else reinterpret_cast<__nv_bfloat16 *>(smem)[jl * 128 + row_local] = __float2bfloat16_rn(val);
-                }
-            }
-            ptx::fence_async_smem();
-            ptx::named_bar_sync(1, kThreads);
-            if (threadIdx.x == 0) {
-                if (p.out_batch_mid) ptx::tma_store_3d(&tmOut, smem, m_tile * 128, batch, j0);
-                else ptx::tma_store_3d(&tmOut, smem, m_tile * 128, j0, batch);
-                ptx::tma_store_commit_wait();
-            }
-        } else {
-            // direct row-major store: thread owns row i, 16 consecutive columns per chunk
-            for (int c0 = half * 16; c0 < n_this; c0 += 32) {
-                float v[16];
-                ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
-                if (!row_ok || c0 >= n_valid) continue;
-                const int64_t base = out_b + (int64_t)i * p.ld_out + j0 + c0;
-                if (c0 + 16 <= n_valid) {
-                    if (p.out_f32) {
-                        float4 *dst = reinterpret_cast<float4 *>(static_cast<float *>(p.out) + base);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            dst[q] = make_float4(v[4 * q] * p.alpha, v[4 * q + 1] * p.alpha, v[4 * q + 2] * p.alpha,
-                                                 v[4 * q + 3] * p.alpha);
-                    } else {
-                        uint32_t w[8];
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * q] * p.alpha, v[2 * q + 1] * p.alpha);
-                            w[q] = *reinterpret_cast<uint32_t *>(&h2);
-                        }
-                        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out) + base);
-                        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-                        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        bool first = true;
+        for (int t = t_first; t < total_tiles; t += t_step) {
+            const TileCoord c = tile_of(p, t);
+            const int32_t a_row = c.m * 128;
+            const int32_t b_row = c.n * p.n_full;
+            const int32_t ab = p.a_bcast ? 0 : c.b;
+            const int32_t bb = p.b_bcast ? 0 : c.b;
+            auto load_a = [&](int st, int kb) {
+                uint8_t *sa = smem + st * stage_bytes;
+                const int32_t kc = kb * kBlockK;
+                if (p.a_batch_mid) ptx::tma_load_3d(sa, &tmA, &full_bar[st], kc, ab, a_row);
+                else ptx::tma_load_3d(sa, &tmA, &full_bar[st], kc, a_row, ab);
+            };
+            auto load_b = [&](int st, int kb) {
+                uint8_t *sb = smem + st * stage_bytes + kABytes;
+                const int32_t kc = kb * kBlockK;
+                if (B_MN) {
+                    const int chunks = (p.box_n + 63) / 64;
+                    for (int q = 0; q < chunks; ++q) {
+                        if (p.b_batch_mid) ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[st], b_row + 64 * q, bb, kc);
+                        else ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[st], b_row + 64 * q, kc, bb);
                     }
                 } else {
+                    if (p.b_batch_mid) ptx::tma_load_3d(sb, &tmB, &full_bar[st], kc, bb, b_row);
+                    else ptx::tma_load_3d(sb, &tmB, &full_bar[st], kc, b_row, bb);
+                }
+            };
+            int kb = kb0;
+            if (first) {
+                // ring is empty: the first `stages` blocks need no empty-wait; static weights
+                // are requested before the grid-dependency wait
+                const int npre = min(p.stages, kb1 - kb0);
+                for (int s = 0; s < npre; ++s) {
+                    ptx::mbar_arrive_expect_tx(&full_bar[s], tx);
+                    if (p.a_static) load_a(s, kb0 + s);
+                }
+                ptx::pdl_wait();
+                for (int s = 0; s < npre; ++s) {
+                    if (!p.a_static) load_a(s, kb0 + s);
+                    load_b(s, kb0 + s);
+                }
+                kb = kb0 + npre;
+                stage = npre % p.stages;
+                phase = (npre == p.stages) ? 1u : 0u;
+                first = false;
+            }
+            for (; kb < kb1; ++kb) {
+                ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+                ptx::mbar_arrive_expect_tx(&full_bar[stage], tx);
+                load_a(stage, kb);
+                load_b(stage, kb);
+                if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ================= MMA issuer (single thread)
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = t_first; t < total_tiles; t += t_step) {
+            const TileCoord c = tile_of(p, t);
+            const int n_this = (c.n == p.tiles_n - 1) ? p.n_tail : p.n_full;
+            const uint32_t idesc = ptx::idesc_bf16(128, (uint32_t)n_this, B_MN);
+            ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);     // epilogue drained this accumulator
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.n_full);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                ptx::mbar_wait(&full_bar[stage], phase);
+                ptx::tc_fence_after();
+                const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
+                const uint32_t sb = sa + kABytes;
+                const uint64_t adesc = ptx::smem_desc_sw128(sa, 0, 1024);
+                // K-major B: 8-row groups 1024 B apart.  MN-major B: 64-column chunks 8 KiB
+                // apart (LBO), 8-row k groups 1024 B apart (SBO).
+                const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb, 8192, 1024) : ptx::smem_desc_sw128(sb, 0, 1024);
 #pragma unroll
-                    for (int q = 0; q < 16; ++q) {
-                        if (c0 + q < n_valid) {
-                            if (p.out_f32) static_cast<float *>(p.out)[base + q] = v[q] * p.alpha;
-                            else static_cast<__nv_bfloat16 *>(p.out)[base + q] = __float2bfloat16_rn(v[q] * p.alpha);
+                for (int kk = 0; kk < kBlockK / 16; ++kk) {
+                    const uint64_t a_k = adesc + (uint64_t)((kk * 32) >> 4);            // +32 B along K
+                    const uint64_t b_k = bdesc + (uint64_t)(B_MN ? ((kk * 2048) >> 4) : ((kk * 32) >> 4));
+                    ptx::umma_bf16(d_tmem, a_k, b_k, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                }
+                ptx::umma_commit(&empty_bar[stage]);         // smem stage free once these MMAs retire
+                if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            }
+            ptx::umma_commit(&tfull[acc]);                   // accumulator complete
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    } else if (warp >= kEpiWarp0) {
+        // ================= epilogue warps
+        ptx::pdl_wait();                                     // residual / output dependencies
+        const int ew = (int)warp - kEpiWarp0;
+        const int quarter = (int)(warp & 3);
+        const int half = ew >> 2;
+        const int row_local = quarter * 32 + (int)lane;
+        const bool leader = (ew == 0 && lane == 0);
+        const int res_bytes = 128 * p.box_n * 2;
+        int acc = 0;
+        uint32_t acc_phase = 0, res_phase = 0;
+        if (EPI == 3 && TRANS && !split && leader && t_first < total_tiles) {
+            const TileCoord c = tile_of(p, t_first);
+            ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
+            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * 128, c.b, c.n * p.n_full);
+            else ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * 128, c.n * p.n_full, c.b);
+        }
+        for (int t = t_first; t < total_tiles; t += t_step) {
+            const TileCoord c = tile_of(p, t);
+            const int n_this = (c.n == p.tiles_n - 1) ? p.n_tail : p.n_full;
+            const int i = c.m * 128 + row_local;
+            const int j0 = c.n * p.n_full;
+            const bool row_ok = i < p.rows_a;
+            const int n_valid = min(n_this, p.rows_b - j0);
+            float bias_i = 0.f;
+            if (EPI >= 1 && row_ok) bias_i = __ldg(p.bias + i);
+            const int64_t out_b = (int64_t)c.b * p.stride_out;
+            if (split && leader) {
+                const int per = n_this / p.split;
+                ptx::mbar_arrive_expect_tx(recv_bar, (uint32_t)((p.split - 1) * per * 128 * 4));
+            }
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tmem_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.n_full);
+
+            if (!split) {
+                if (TRANS) {
+                    OutT *so = reinterpret_cast<OutT *>(stg);
+                    if (EPI == 3) {
+                        ptx::mbar_wait(res_bar, res_phase);
+                        res_phase ^= 1;
+                    }
+                    for (int c0 = half * 16; c0 < n_this; c0 += 32) {
+                        float v[16];
+                        ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            const int o = (c0 + q) * 128 + row_local;
+                            float val = epi_math<EPI>(v[q], p.alpha, bias_i);
+                            if constexpr (EPI == 3) val += __bfloat162float(reinterpret_cast<__nv_bfloat16 *>(stg)[o]);
+                            if constexpr (OUT_F32) so[o] = val;
+                            else so[o] = __float2bfloat16_rn(val);
                         }
                     }
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty[acc]);   // TMEM may be overwritten now
+                    ptx::fence_async_smem();
+                    ptx::named_bar_sync(1, kEpiThreads);
+                    if (leader) {
+                        if (p.out_batch_mid) ptx::tma_store_3d(&tmOut, stg, c.m * 128, c.b, j0);
+                        else ptx::tma_store_3d(&tmOut, stg, c.m * 128, j0, c.b);
+                        ptx::tma_store_commit_wait();                 // staging readable again
+                        const int tn = t + t_step;
+                        if (EPI == 3 && tn < total_tiles) {
+                            const TileCoord cn = tile_of(p, tn);
+                            ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
+                            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * 128, cn.b, cn.n * p.n_full);
+                            else ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * 128, cn.n * p.n_full, cn.b);
+                        }
+                    }
+                    ptx::named_bar_sync(2, kEpiThreads);
+                } else {
+                    // direct row-major store: thread owns row i, 16 consecutive columns per chunk
+                    for (int c0 = half * 16; c0 < n_this; c0 += 32) {
+                        float v[16];
+                        ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
+                        if (!row_ok || c0 >= n_valid) continue;
+                        OutT *dst = static_cast<OutT *>(p.out) + out_b + (int64_t)i * p.ld_out + j0 + c0;
+                        if (c0 + 16 <= n_valid) {
+                            if constexpr (OUT_F32) {
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    reinterpret_cast<float4 *>(dst)[q] =
+                                        make_float4(v[4 * q] * p.alpha, v[4 * q + 1] * p.alpha, v[4 * q + 2] * p.alpha,
+                                                    v[4 * q + 3] * p.alpha);
+                            } else {
+                                uint32_t w[8];
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) {
+                                    __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * q] * p.alpha, v[2 * q + 1] * p.alpha);
+                                    w[q] = *reinterpret_cast<uint32_t *>(&h2);
+                                }
+                                reinterpret_cast<uint4 *>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                                reinterpret_cast<uint4 *>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) {
+                                if (c0 + q < n_valid) {
+                                    if constexpr (OUT_F32) dst[q] = v[q] * p.alpha;
+                                    else dst[q] = __float2bfloat16_rn(v[q] * p.alpha);
+                                }
+                            }
+                        }
+                    }
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
                 }
-            }
-        }
-    } else {
-        // ---------------- split-K: park the fp32 partial in own smem as red[col][128]
-        float *red = reinterpret_cast<float *>(smem);
-        for (int c0 = half * 16; c0 < n_this; c0 += 32) {
-            float v[16];
-            ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
-#pragma unroll
-            for (int q = 0; q < 16; ++q) red[(c0 + q) * 128 + row_local] = v[q];
-        }
-        ptx::cluster_sync();
-        const uint32_t rank = ptx::cluster_ctarank();
-        const int per = n_this / p.split;
-        const int cbeg = (int)rank * per;
-        uint32_t rbase[8];
-        const uint32_t red_s = ptx::smem_u32(red);
-#pragma unroll
-        for (int r = 0; r < 8; ++r) rbase[r] = (r < p.split) ? ptx::map_shared_rank(red_s, (uint32_t)r) : 0u;
-        for (int jl = cbeg + half; jl < cbeg + per; jl += 2) {
-            const uint32_t off = (uint32_t)((jl * 128 + row_local) * 4);
-            float part[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) part[r] = (r < p.split) ? ptx::ld_dsmem_f32(rbase[r] + off) : 0.f;
-            float acc = 0.f;
-#pragma unroll
-            for (int r = 0; r < 8; ++r) acc += part[r];       // fixed rank order: deterministic
-            if (!row_ok || jl >= n_valid) continue;
-            const int64_t j = j0 + jl;
-            if (p.transposed) {
-                float val = epi_apply(p, acc, bias_i);
-                if (p.epi == 3) val += __bfloat162float(static_cast<const __nv_bfloat16 *>(p.res)[j * p.ld_res + i]);
-                const int64_t o = out_b + j * p.ld_out + i;
-                if (p.out_f32) static_cast<float *>(p.out)[o] = val;
-                else static_cast<__nv_bfloat16 *>(p.out)[o] = __float2bfloat16_rn(val);
             } else {
-                const int64_t o = out_b + (int64_t)i * p.ld_out + j;
-                if (p.out_f32) static_cast<float *>(p.out)[o] = acc * p.alpha;
-                else static_cast<__nv_bfloat16 *>(p.out)[o] = __float2bfloat16_rn(acc * p.alpha);
+                // ---- split-K reduce-scatter over DSMEM: partial[col][128] fp32 in the ring region
+                float *part = reinterpret_cast<float *>(smem);
+                for (int c0 = half * 16; c0 < n_this; c0 += 32) {
+                    float v[16];
+                    ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) part[(c0 + q) * 128 + row_local] = v[q];
+                }
+                ptx::fence_async_smem();                       // generic writes -> bulk-copy source
+                ptx::named_bar_sync(1, kEpiThreads);
+                const uint32_t rank = ptx::cluster_ctarank();
+                const int per = n_this / p.split;
+                const uint32_t slot = (uint32_t)(per * 128 * 4);
+                if (leader) {
+                    for (int r = 0; r < p.split; ++r) {
+                        if (r == (int)rank) continue;
+                        const uint32_t dst = ptx::map_shared_rank(ptx::smem_u32(stg) + rank * slot, (uint32_t)r);
+                        const uint32_t bar = ptx::map_shared_rank(ptx::smem_u32(recv_bar), (uint32_t)r);
+                        ptx::bulk_copy_to_peer(dst, part + (size_t)r * per * 128, slot, bar);
+                    }
+                }
+                ptx::mbar_wait(recv_bar, 0);
+                const float *recv = reinterpret_cast<const float *>(stg);
+                for (int jl = half; jl < per; jl += 2) {
+                    float a = 0.f;
+                    for (int r = 0; r < p.split; ++r) {            // fixed rank order: deterministic
+                        const float *src = (r == (int)rank) ? part + (size_t)(rank * per) * 128 : recv + (size_t)r * per * 128;
+                        a += src[jl * 128 + row_local];
+                    }
+                    const int jt = (int)rank * per + jl;          // column within the tile
+                    if (!row_ok || jt >= n_valid) continue;
+                    const int64_t j = j0 + jt;
+                    float val = epi_math<EPI>(a, p.alpha, bias_i);
+                    if constexpr (EPI == 3) val += __bfloat162float(static_cast<const __nv_bfloat16 *>(p.res)[j * p.ld_res + i]);
+                    const int64_t o = TRANS ? out_b + j * p.ld_out + i : out_b + (int64_t)i * p.ld_out + j;
+                    if constexpr (OUT_F32) static_cast<float *>(p.out)[o] = val;
+                    else static_cast<__nv_bfloat16 *>(p.out)[o] = __float2bfloat16_rn(val);
+                }
+                ptx::tc_fence_before();
             }
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
         }
-        ptx::cluster_sync();                                   // keep smem alive for peers
     }
 
     ptx::tc_fence_before();
     __syncthreads();
+    if (split) ptx::cluster_sync();      // every peer has received: our smem may go away
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, tmem_cols);
     }
+}
+
+template <int B_MN, int EPI, int OUT_F32, int TRANS>
+cudaError_t launch_t(const UmmaLaunch &L, cudaLaunchConfig_t &cfg) {
+    auto fn = umma_gemm_kernel<B_MN, EPI, OUT_F32, TRANS>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    return cudaLaunchKernelEx(&cfg, fn, L.tmA, L.tmB, L.tmOut, L.tmRes, L.p);
 }
 
 }  // namespace
@@ -311,20 +414,14 @@ int umma_max_stages(int box_n, int b_mn_major) {
     return (kSmemLimit - 1024 - kTailBytes) / stage;
 }
 
-size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes) {
+size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed) {
     const size_t ring = (size_t)stages * (kABytes + b_stage_bytes(box_n, b_mn_major));
-    const size_t red = (size_t)128 * box_n * (split > 1 ? 4 : out_bytes);
-    return 1024 /* alignment slack */ + (ring > red ? ring : red) + kTailBytes;
+    const size_t part = split > 1 ? (size_t)128 * box_n * 4 : 0;
+    const size_t stg = split > 1 ? (size_t)128 * box_n * 4 : (transposed ? (size_t)128 * box_n * out_bytes : 0);
+    return 1024 /* alignment slack */ + (ring > part ? ring : part) + stg + kTailBytes;
 }
 
 cudaError_t launch_umma_gemm(const UmmaLaunch &L) {
-    static bool attr_set[2] = {false, false};
-    const void *fn = L.b_mn_major ? (const void *)umma_gemm_kernel<1> : (const void *)umma_gemm_kernel<0>;
-    if (!attr_set[L.b_mn_major]) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-        if (e != cudaSuccess) return e;
-        attr_set[L.b_mn_major] = true;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = L.grid;
     cfg.blockDim = dim3(kThreads, 1, 1);
@@ -345,8 +442,17 @@ cudaError_t launch_umma_gemm(const UmmaLaunch &L) {
         attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
         cfg.numAttrs++;
     }
-    if (L.b_mn_major) return cudaLaunchKernelEx(&cfg, umma_gemm_kernel<1>, L.tmA, L.tmB, L.tmOut, L.p);
-    return cudaLaunchKernelEx(&cfg, umma_gemm_kernel<0>, L.tmA, L.tmB, L.tmOut, L.p);
+    if (L.b_mn_major) {   // bmm P.V: direct epilogue, alpha only
+        if (L.out_f32) return launch_t<1, 0, 1, 0>(L, cfg);
+        return launch_t<1, 0, 0, 0>(L, cfg);
+    }
+    if (L.out_f32) return launch_t<0, 0, 1, 1>(L, cfg);      // bmm Q.K^T scores
+    switch (L.epi) {
+        case 0: return launch_t<0, 0, 0, 1>(L, cfg);
+        case 1: return launch_t<0, 1, 0, 1>(L, cfg);
+        case 2: return launch_t<0, 2, 0, 1>(L, cfg);
+        default: return launch_t<0, 3, 0, 1>(L, cfg);
+    }
 }
 
 }  // namespace nimble

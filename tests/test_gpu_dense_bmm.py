@@ -149,7 +149,7 @@ def test_bf16_pad_then_slice_bitwise(nb):
     for M in (3, 129, 250, 259):
         x = synth.normal((M, K), 1.0, 73 + M)
         y = _dense_gpu(nb, x, W, b, nb.EPI_BIAS)
-        Mp = 256 * ((M + 255) // 256)
+        Mp = 128 * ((M + 127) // 128)
         xp = torch.zeros((Mp, K), dtype=torch.bfloat16)
         xp[:M] = x
         yp = _dense_gpu(nb, xp, W, b, nb.EPI_BIAS)

@@ -112,12 +112,13 @@ def test_dispatch_worked_examples(orc):
 
 @pytest.mark.parametrize("dt", [0, 1])
 def test_dispatch_invariants(orc, dt):
-    t = 8 if dt == 0 else 256
     for M in list(range(1, 2049)) + [4095, 4096, 4097, 65535, 65536]:
-        for c in (0, 1, 2, 5, 8, 17):
+        t = 8 if dt == 0 else (128 if M < 2048 else 256)
+        for c in (0, 1, 2, 5, 8, 9, 17):
             st, d = orc.dispatch_dense(M, 1024, 1024, dt, c)
             assert st == 0
             assert d["tile_t"] == t
+            assert d["n_classes"] == (8 if dt == 0 else t // 16 + 1)
             assert d["k"] * t + d["r"] == M and 0 <= d["r"] < t           # x = t k + r
             assert d["grid"][1] == d["k"] + (d["r"] > 0)                  # every row covered once
             n = d["n_classes"]
@@ -130,11 +131,14 @@ def test_dispatch_invariants(orc, dt):
                 if d["variant"] >= 0:
                     assert d["r"] <= d["umma_n_tail"] < d["r"] + 16 and d["umma_n_tail"] % 16 == 0
                 else:
-                    assert d["umma_n_tail"] == 256
+                    assert d["umma_n_tail"] == t
             if dt == 1:
                 s = d["split_k"]
                 assert s in (1, 2, 4, 8) and d["cluster"] == (1, 1, s)
                 assert (1024 // 64) // s >= 4 or s == 1
+                assert d["family"] == (1 if M < 2048 else 3)
+                if M >= 2048:
+                    assert s == 1
 
 
 def test_dispatch_errors(orc):
@@ -148,7 +152,7 @@ def test_dispatch_errors(orc):
 
 def test_dispatch_bmm_families(orc):
     st, d = orc.dispatch_bmm(16, 300, 300, 64, 0, 1)
-    assert st == 0 and d["family"] == 1 and d["grid"][0] == 3 and d["grid"][1] == 2
+    assert st == 0 and d["family"] == 1 and d["grid"][0] == 3 and d["grid"][1] == 3
     st, d = orc.dispatch_bmm(16, 300, 64, 300, 1, 1)
     assert st == 0 and d["family"] == 2 and d["k"] == 2 and d["r"] == 44
     assert d["umma_n_full"] == 64 and d["umma_n_tail"] == 64 and d["grid"][1] == 1
