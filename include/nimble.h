@@ -190,6 +190,12 @@ int nimble_treelstm_level(const int32_t *nodes, const float *A, int64_t lda, con
 int64_t nimble_request_cost(int64_t L);
 int nimble_partition_lpt(const int64_t *lens, int64_t R, int32_t G, int32_t *owner);
 
+/* Instrumentation (not on the hot path): when buf != NULL, every later tcgen05 GEMM launch
+ * writes 8 %globaltimer stamps (ns) per CTA into buf[cta*8 + slot] (device memory, caller-
+ * sized): 0 start, 1 setup done, 2 first operands landed, 3 accumulator ready, 4 split-K
+ * partial parked, 5 split-K slices received, 6 end.  NULL turns it off. */
+int nimble_debug_trace(unsigned long long *buf);
+
 /* Thread-local message for the last non-OK status ("" if none). */
 const char *nimble_last_error(void);
 /* Library version string. */

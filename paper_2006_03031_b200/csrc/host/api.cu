@@ -117,7 +117,10 @@ bool ext_ok(int64_t x) { return x >= 1 && x <= kMaxExtent; }
 // Fill the stage count / smem for a UMMA launch from the dispatch record.
 // Pipeline depth / smem from the tile geometry, then the launch grid: the dispatch record's
 // tile grid as is for split-K clusters, else min(tiles, 148) persistent CTAs.
+unsigned long long *g_trace = nullptr;     // debug: per-CTA phase timestamps (nimble_debug_trace)
+
 void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
+    L.p.trace = g_trace;
     const int kb_per_split = (L.p.kb_total + L.p.split - 1) / L.p.split;
     const int ob = L.out_f32 ? 4 : 2;
     int st = kb_per_split < 8 ? kb_per_split : 8;
@@ -143,6 +146,13 @@ void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
 using namespace nimble;
 
 extern "C" const char *nimble_last_error(void) { return t_err.c_str(); }
+
+// Debug hook (not part of the product contract): when non-NULL, every subsequent tcgen05 GEMM
+// launch writes 8 globaltimer stamps per CTA into buf[cta * 8 + slot].
+extern "C" int nimble_debug_trace(unsigned long long *buf) {
+    g_trace = buf;
+    return NIMBLE_OK;
+}
 extern "C" const char *nimble_version(void) { return "nimble-b200 0.1 (sm_100a)"; }
 
 extern "C" int nimble_last_dispatch(nimble_dispatch *out) {

@@ -34,6 +34,7 @@ struct UmmaParams {
     const float *bias;
     const void *res;     // residual (split-K path reads it directly; otherwise via tmRes)
     int64_t ld_res;
+    unsigned long long *trace;   // optional per-CTA phase timestamps (globaltimer ns), NULL = off
 };
 
 struct UmmaLaunch {

@@ -101,6 +101,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kb0 = (int)((int64_t)split_q * p.kb_total / p.split);
     const int kb1 = (int)((int64_t)(split_q + 1) * p.kb_total / p.split);
     const uint32_t tmem_cols = split ? pow2_cols(p.box_n) : pow2_cols(2 * p.n_full);
+    const int cta_lin = ((int)blockIdx.z * gridDim.y + (int)blockIdx.y) * gridDim.x + (int)blockIdx.x;
+    unsigned long long *trace = p.trace ? p.trace + (size_t)cta_lin * 8 : nullptr;
+#define NIMBLE_TRACE(slot) do { if (trace) trace[slot] = ptx::globaltimer(); } while (0)
+    if (threadIdx.x == 0) NIMBLE_TRACE(0);
 
     if (threadIdx.x == 0) {
         ptx::prefetch_tmap(&tmA);
@@ -127,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (split) ptx::cluster_sync();                // peers' barriers exist before any DSMEM copy
     const uint32_t tmem_base = *tmem_slot;
     ptx::pdl_trigger();                            // the next kernel's prologue may start now
+    if (threadIdx.x == 0) NIMBLE_TRACE(1);
 
     if (warp == 0 && lane == 0) {
         // ================= TMA producer
@@ -203,6 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kb = kb0; kb < kb1; ++kb) {
                 ptx::mbar_wait(&full_bar[stage], phase);
                 ptx::tc_fence_after();
+                if (kb == kb0 && t == t_first) NIMBLE_TRACE(2);
                 const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
                 const uint32_t sb = sa + kABytes;
                 const uint64_t adesc = ptx::smem_desc_sw128(sa, 0, 1024);
@@ -255,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
+            if (leader && t == t_first) NIMBLE_TRACE(3);
             const uint32_t tmem_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.n_full);
 
             if (!split) {
@@ -343,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::fence_async_smem();                       // generic writes -> bulk-copy source
                 ptx::named_bar_sync(1, kEpiThreads);
+                if (leader) NIMBLE_TRACE(4);
                 const uint32_t rank = ptx::cluster_ctarank();
                 const int per = n_this / p.split;
                 const uint32_t slot = (uint32_t)(per * 128 * 4);
@@ -355,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 ptx::mbar_wait(recv_bar, 0);
+                if (leader) NIMBLE_TRACE(5);
                 const float *recv = reinterpret_cast<const float *>(stg);
                 for (int jl = half; jl < per; jl += 2) {
                     float a = 0.f;
@@ -385,6 +394,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, tmem_cols);
     }
+    if (threadIdx.x == 0) NIMBLE_TRACE(6);
+#undef NIMBLE_TRACE
 }
 
 template <int B_MN, int EPI, int OUT_F32, int TRANS>

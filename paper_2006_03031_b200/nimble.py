@@ -71,6 +71,7 @@ _SIGS = {
     "nimble_treelstm_level": [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _i64,
                               _i64, C.c_int, _vp],
     "nimble_partition_lpt": [_i64p, _i64, C.c_int32, _i32p],
+    "nimble_debug_trace": [_vp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
