@@ -103,7 +103,7 @@ static int64_t orc_ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static int32_t orc_split(int64_t tiles, int64_t K) {
     int64_t kb = orc_ceil_div(K, 64);
     int32_t s = 1;
-    while (s < 8 && tiles * s < 148 && kb >= 8 * (int64_t)s) s *= 2;
+    while (s < 8 && tiles * 2 * s <= 148 && kb >= 8 * (int64_t)s) s *= 2;
     return s;
 }
 

@@ -34,14 +34,14 @@ int32_t select_variant(const ResidueFamily &f, int32_t cls) {
     return specialised ? cls : -1;
 }
 
-// split-K factor (cluster size along K): grow while the grid is below one wave
-// and every split keeps >= 4 k-blocks of 64.
+// split-K factor (cluster size along K): grow while the grown grid still fits one
+// wave of 148 CTAs and every split keeps >= 4 k-blocks of 64.
 int32_t choose_split(int64_t ctas, int64_t K) {
     const int64_t kblocks = cdiv(K, 64);
     int32_t s = 1;
     for (;;) {
         const int32_t next = s * 2;
-        if (next > 8 || ctas * s >= kNumSMs || kblocks / next < 4) break;
+        if (next > 8 || ctas * next > kNumSMs || kblocks / next < 4) break;
         s = next;
     }
     return s;

@@ -73,7 +73,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const UmmaParams p) {
     using OutT = typename std::conditional<OUT_F32, float, __nv_bfloat16>::type;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-B alignment for the 128-B swizzle atoms.  Offset the __shared__ array itself (no
+    // integer round trip) so every derived pointer stays in the shared address space (STS/LDS,
+    // not generic ST/LD through the LSU).
+    uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const bool split = p.split > 1;
     const int b_bytes = b_stage_bytes(p.box_n, B_MN);
     const int stage_bytes = kABytes + b_bytes;
