@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     else static_cast<__nv_bfloat16 *>(p.out)[o] = __float2bfloat16_rn(val);
                 }
                 ptx::tc_fence_before();
+                if (leader) NIMBLE_TRACE(7);
             }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
