@@ -4,6 +4,7 @@
 // encoding and asynchronous launches on the caller's stream.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -121,6 +122,8 @@ unsigned long long *g_trace = nullptr;     // debug: per-CTA phase timestamps (n
 
 void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
     L.p.trace = g_trace;
+    static const int dbg = [] { const char *e = std::getenv("NIMBLE_DBG"); return e ? std::atoi(e) : 0; }();
+    L.p.dbg = dbg;
     const int kb_per_split = (L.p.kb_total + L.p.split - 1) / L.p.split;
     const int ob = L.out_f32 ? 4 : 2;
     int st = kb_per_split < 8 ? kb_per_split : 8;

@@ -35,6 +35,7 @@ struct UmmaParams {
     const void *res;     // residual (split-K path reads it directly; otherwise via tmRes)
     int64_t ld_res;
     unsigned long long *trace;   // optional per-CTA phase timestamps (globaltimer ns), NULL = off
+    int32_t dbg;                 // experiment bits (NIMBLE_DBG env): 1 skip split stores, 2 skip recv reads
 };
 
 struct UmmaLaunch {
