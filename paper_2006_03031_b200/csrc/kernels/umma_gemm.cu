@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const float *src = (r == (int)rank) ? part + (size_t)(rank * per) * 128 : recv + (size_t)r * per * 128;
                         a += src[jl * 128 + row_local];
                     }
-                    if (p.dbg & 1) { if (a == 12345.f) p.bias = nullptr; continue; }
+                    if (p.dbg & 1) { if (a == 12345.f) asm volatile("trap;"); continue; }
                     const int jt = (int)rank * per + jl;          // column within the tile
                     if (!row_ok || jt >= n_valid) continue;
                     const int64_t j = j0 + jt;
