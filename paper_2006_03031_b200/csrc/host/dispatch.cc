@@ -4,6 +4,7 @@
 // (fig:sym-codegen PAPER.md:699) and the rest take the guarded
 // fallback.  The rule is DISPATCH.md; the oracle implements it independently.
 #include <atomic>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -83,6 +84,8 @@ int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, 
     const int64_t m_tiles = cdiv(N_rows, 128);
     const int64_t n_tiles = d->k + (d->r ? 1 : 0);
     d->split_k = (f.id == kUMMA_T.id) ? choose_split(m_tiles * n_tiles * batch, K) : 1;
+    static const int force = [] { const char *e = std::getenv("NIMBLE_FORCE_SPLIT"); return e ? std::atoi(e) : 0; }();
+    if (force > 0) d->split_k = force;      // experiment-only override (breaks oracle parity)
     d->grid[0] = static_cast<int32_t>(m_tiles);
     d->grid[1] = static_cast<int32_t>(n_tiles);
     d->grid[2] = static_cast<int32_t>(batch * d->split_k);
