@@ -136,6 +136,22 @@ int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const void *B, i
                    int out_dt, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * nimble_attention_varlen — fused attention over token-packed variable-length
+ * requests: for request i = 0..R-1 (tokens
+ * [seq_off[i], seq_off[i+1]) of the packed qkv), every head h:
+ *     C_h = softmax( Q_h K_h^T * scale ) V_h,     L_i = seq_off[i+1] - seq_off[i]
+ * qkv [T x ld_qkv] bf16 with row blocks Q | K | V of width heads*head_dim (BERT's
+ * fused QKV projection output); out [T x ld_out] bf16, head h in columns
+ * [h*head_dim, (h+1)*head_dim).  seq_off: DEVICE int32 [R+1], seq_off[0] = 0,
+ * nondecreasing, seq_off[R] = T.  max_len >= every L_i.  One launch; S and P stay
+ * on chip (TMEM / smem).  head_dim must be 64 and max_len <= 512 (E_UNSUPPORTED
+ * otherwise); qkv/out 16-byte aligned with ld*2 % 16 == 0 (E_ALIGN).
+ * ------------------------------------------------------------------------- */
+int nimble_attention_varlen(const void *qkv, int64_t ld_qkv, int64_t T, const int32_t *seq_off, int32_t R,
+                            int32_t max_len, int32_t heads, int32_t head_dim, float scale, void *out,
+                            int64_t ld_out, void *stream);
+
+/* ---------------------------------------------------------------------------
  * Row ops used around bmm_dyn in BERT (the paper is silent: DESIGN.md readings 8-10).
  * nimble_softmax_rows: P[b][i][j] = softmax_j(S[b][i][j]) over j < L, for i < rows;
  *   S fp32, P bf16; columns L..ldP-1 of P are written with 0 (so a following

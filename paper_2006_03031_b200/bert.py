@@ -101,3 +101,75 @@ class BertEncoder:
 
     def launches_per_forward(self) -> int:
         return 9 * len(self.layers)
+
+
+class BertPacked:
+    """Token-packed BERT encoder over a batch of variable-length requests (SURVEY §8(f)
+    NEXT-1).  The R requests' tokens are concatenated into X [T x d], T = sum L_i; every
+    dense runs once with the symbolic M = T (residue dispatch on T), attention runs once
+    per layer over all (request, head) pairs with each request's own L_i
+    (nimble_attention_varlen: no S / P round trip through HBM).  Per layer 7 launches:
+
+        QKV = X Wqkv^T + bqkv            dense_dyn  (M = T)
+        C   = attention_varlen(QKV)      one launch, per-request L_i
+        A   = C Wo^T + bo + X            dense_dyn  (fused residual)
+        H1  = LN1(A)
+        F   = GELU(H1 W1^T + b1)         dense_dyn  (fused GELU)
+        O   = F W2^T + b2 + H1           dense_dyn  (fused residual)
+        Y   = LN2(O)
+    """
+
+    def __init__(self, cfg: dict, weights: list, max_tokens: int, device="cuda"):
+        self.d, self.H, self.f = cfg["d"], cfg["heads"], cfg["ffn"]
+        self.dh = self.d // self.H
+        self.max_tokens = max_tokens
+        self.layers = [{k: v.to(device).contiguous() for k, v in w.items()} for w in weights]
+        d, f, Tm = self.d, self.f, max_tokens
+        bf = dict(dtype=torch.bfloat16, device=device)
+        self.qkv = torch.empty((Tm, 3 * d), **bf)
+        self.ctx = torch.empty((Tm, d), **bf)
+        self.A = torch.empty((Tm, d), **bf)
+        self.H1 = torch.empty((Tm, d), **bf)
+        self.F = torch.empty((Tm, f), **bf)
+        self.O = torch.empty((Tm, d), **bf)
+        self.X = [torch.empty((Tm, d), **bf), torch.empty((Tm, d), **bf)]
+        self._p = {k: getattr(self, k).data_ptr() for k in ("qkv", "ctx", "A", "H1", "F", "O")}
+        self._lp = [{k: v.data_ptr() for k, v in w.items()} for w in self.layers]
+
+    @staticmethod
+    def flops(lens, d=1024, f=4096, layers=24) -> int:
+        return int(sum((2 * L * d * (3 * d + d + 2 * f) + 4 * L * L * d) * layers for L in lens))
+
+    def launches_per_forward(self) -> int:
+        return 7 * len(self.layers)
+
+    def layer(self, x_ptr, out_ptr, T, seq_off_ptr, R, max_len, li, stream):
+        d, f, H = self.d, self.f, self.H
+        w, p = self._lp[li], self._p
+        nb.dense_dyn_raw(x_ptr, d, w["Wqkv"], d, w["bqkv"], None, 0, p["qkv"], 3 * d, T, 3 * d, d,
+                         nb.BF16, nb.EPI_BIAS, stream)
+        nb._check(nb._lib.nimble_attention_varlen(p["qkv"], 3 * d, T, seq_off_ptr, R, max_len, H, self.dh,
+                                                  1.0 / float(self.dh) ** 0.5, p["ctx"], d, stream))
+        nb.dense_dyn_raw(p["ctx"], d, w["Wo"], d, w["bo"], x_ptr, d, p["A"], d, T, d, d,
+                         nb.BF16, nb.EPI_BIAS_RESIDUAL, stream)
+        nb._check(nb._lib.nimble_layernorm(p["A"], d, w["g1"], w["be1"], 1e-12, p["H1"], d, T, d, stream))
+        nb.dense_dyn_raw(p["H1"], d, w["W1"], d, w["b1"], None, 0, p["F"], f, T, f, d,
+                         nb.BF16, nb.EPI_BIAS_GELU, stream)
+        nb.dense_dyn_raw(p["F"], f, w["W2"], f, w["b2"], p["H1"], d, p["O"], d, T, d, f,
+                         nb.BF16, nb.EPI_BIAS_RESIDUAL, stream)
+        nb._check(nb._lib.nimble_layernorm(p["O"], d, w["g2"], w["be2"], 1e-12, out_ptr, d, T, d, stream))
+
+    def forward(self, x: torch.Tensor, seq_off: torch.Tensor, max_len: int, T: int | None = None,
+                stream: int | None = None) -> torch.Tensor:
+        """x [>=T x d] bf16 (packed requests), seq_off device int32 [R+1]; returns [T x d] view."""
+        R = seq_off.shape[0] - 1
+        T = x.shape[0] if T is None else T
+        assert 1 <= T <= self.max_tokens
+        s = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        src = x.data_ptr()
+        so = seq_off.data_ptr()
+        for li in range(len(self.layers)):
+            dst = self.X[li & 1].data_ptr()
+            self.layer(src, dst, T, so, R, max_len, li, s)
+            src = dst
+        return self.X[(len(self.layers) - 1) & 1][:T]

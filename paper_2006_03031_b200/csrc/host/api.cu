@@ -311,6 +311,42 @@ extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const
     return NIMBLE_OK;
 }
 
+// ------------------------------------------------------------------ varlen attention
+extern "C" int nimble_attention_varlen(const void *qkv, int64_t ld_qkv, int64_t T, const int32_t *seq_off, int32_t R,
+                                       int32_t max_len, int32_t heads, int32_t head_dim, float scale, void *out,
+                                       int64_t ld_out, void *stream) {
+    if (!qkv || !seq_off || !out) return fail(NIMBLE_E_NULL, "nimble_attention_varlen: NULL pointer");
+    if (!ext_ok(T) || R < 1 || max_len < 1 || heads < 1 || head_dim < 1)
+        return fail(NIMBLE_E_EXTENT, "nimble_attention_varlen: extents must be >= 1");
+    if (head_dim != 64) return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen: head_dim must be 64");
+    if (max_len > 512) return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen: max_len > 512 not built");
+    if (ld_qkv < 3LL * heads * head_dim || ld_out < (int64_t)heads * head_dim)
+        return fail(NIMBLE_E_SHAPE, "nimble_attention_varlen: leading dimension too small");
+    if (!aligned16(qkv) || !aligned16(out) || (ld_qkv * 2) % 16 || (ld_out * 2) % 16)
+        return fail(NIMBLE_E_ALIGN, "nimble_attention_varlen: 16-B aligned qkv/out and ld*2 % 16 == 0 required");
+    cudaError_t e = get_encoder();
+    if (e != cudaSuccess) return cuda_fail("cuTensorMapEncodeTiled lookup", e);
+    // packed QKV viewed as {64 (e), 3*heads (Q heads | K heads | V heads), T (tokens)}
+    CUtensorMap tmQK, tmV;
+    cuuint64_t dims[3] = {64, (cuuint64_t)(3 * heads), (cuuint64_t)T};
+    cuuint64_t strides[2] = {(cuuint64_t)head_dim * 2, (cuuint64_t)ld_qkv * 2};
+    cuuint32_t estr[3] = {1, 1, 1};
+    cuuint32_t box_qk[3] = {64, 1, 128}, box_v[3] = {64, 1, 64};
+    CUresult r = g_encode(&tmQK, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(qkv), dims, strides, box_qk,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS)
+        r = g_encode(&tmV, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(qkv), dims, strides, box_v, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(NIMBLE_E_CUDA, "cuTensorMapEncodeTiled(attention) failed (code " + std::to_string((int)r) + ")");
+    e = launch_attention_varlen(tmQK, tmV, seq_off, R, max_len, heads, scale, static_cast<__nv_bfloat16 *>(out), ld_out,
+                                static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen launch", e);
+    clear_error();
+    return NIMBLE_OK;
+}
+
 // ------------------------------------------------------------------ row ops
 extern "C" int nimble_softmax_rows(const float *S, int64_t ldS, int64_t strideS, void *P, int64_t ldP, int64_t strideP,
                                    int64_t batch, int64_t rows, int64_t L, void *stream) {

@@ -83,6 +83,11 @@ struct Simt8Params {
 };
 cudaError_t launch_simt8(const Simt8Params &p, int variant, dim3 grid, cudaStream_t s);
 
+size_t attention_smem_bytes(int max_len);
+cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const int32_t *seq_off,
+                                    int R, int max_len, int heads, float scale, __nv_bfloat16 *out, int64_t ld_out,
+                                    cudaStream_t s);
+
 cudaError_t launch_softmax_rows(const float *S, int64_t ldS, int64_t strideS, __nv_bfloat16 *P, int64_t ldP,
                                 int64_t strideP, int64_t batch, int64_t rows, int64_t L, cudaStream_t s);
 cudaError_t launch_layernorm(const __nv_bfloat16 *X, int64_t ldx, const float *g, const float *b, float eps,

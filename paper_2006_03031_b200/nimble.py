@@ -72,6 +72,8 @@ _SIGS = {
                               _i64, C.c_int, _vp],
     "nimble_partition_lpt": [_i64p, _i64, C.c_int32, _i32p],
     "nimble_debug_trace": [_vp],
+    "nimble_attention_varlen": [_vp, _i64, _i64, _vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, _vp,
+                                _i64, _vp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -214,6 +216,19 @@ def bmm_dyn(A, lda, strideA, B, ldb, strideB, trans_b, Cout, ldc, strideC, batch
     _check(_lib.nimble_bmm_dyn(a, lda, strideA, b, ldb, strideB, int(trans_b), c, ldc, strideC, batch, M, N, K,
                                float(alpha), BF16, out_dt, _stream(stream)))
     return Cout
+
+
+def attention_varlen(qkv, seq_off, R, max_len, heads, out, T=None, scale=None, head_dim=64, stream=None):
+    """Fused softmax(Q K^T * scale) V over token-packed requests; seq_off: device int32 [R+1]."""
+    T = qkv.shape[0] if T is None else T
+    scale = head_dim ** -0.5 if scale is None else scale
+    q = qkv if isinstance(qkv, int) else _ptr(qkv)
+    o = out if isinstance(out, int) else _ptr(out)
+    ldq = 3 * heads * head_dim if isinstance(qkv, int) else qkv.stride(0)
+    ldo = heads * head_dim if isinstance(out, int) else out.stride(0)
+    _check(_lib.nimble_attention_varlen(q, ldq, T, _ptr(seq_off), R, max_len, heads, head_dim, float(scale), o, ldo,
+                                        _stream(stream)))
+    return out
 
 
 def softmax_rows(S, ldS, strideS, P, ldP, strideP, batch, rows, L, stream=None):
