@@ -7,10 +7,12 @@ libnimble's dynamic-shape sm_100a kernels, 1..8 GPUs of one box.
 
 A step = one pass of the whole hot path over one batch of synthetic requests:
 R_PER_GPU x N requests with L ~ U{1..512} (seeded), LPT-partitioned over the N ranks
-(native nimble_partition_lpt), each rank running its whole requests at batch 1
-through 24 BERT-large layers (shape fns -> residue dispatch -> dense_dyn / bmm_dyn /
-softmax / LN, replayed from per-L CUDA graphs), then one NCCL gather of the [CLS]
-vectors to rank 0.  value = requests/s of the whole job (weak scaling).
+(native nimble_partition_lpt).  Each rank runs its whole requests through 24
+BERT-large layers — by default token-packed (--mode packed: every dense_dyn has the
+symbolic M = sum of its requests' L_i, attention_varlen handles each request's own
+L_i), or one request at a time (--mode batch1: per-L CUDA graphs of the batch-1
+kernels) — then one NCCL gather of the [CLS] vectors to rank 0.
+value = requests/s of the whole job (weak scaling).
 
 --impl reference times the fp64 CPU oracle (oracle/, the reference arm for this
 tier) on a bounded sample of the same workload.  See DESIGN.md §Measurement.
@@ -173,6 +175,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nimble", choices=["nimble", "reference"])
+    ap.add_argument("--mode", default="packed", choices=["packed", "batch1"],
+                    help="packed: a rank's whole shard as one token-packed forward (M = sum L_i); "
+                         "batch1: one request at a time from per-L CUDA graphs")
     ap.add_argument("--requests-per-gpu", type=int, default=64)
     ap.add_argument("--layers", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -196,37 +201,53 @@ def main():
 
     from paper_2006_03031_b200 import nimble as nb
     from paper_2006_03031_b200 import synth
-    from paper_2006_03031_b200.bert import BertEncoder
+    from paper_2006_03031_b200.bert import BertEncoder, BertPacked
     from paper_2006_03031_b200.serve import GraphCache, gather_results, shard
 
     peaks = load_peaks()
     cfg = dict(synth.BERT_LARGE)
     cfg["layers"] = args.layers
     d = cfg["d"]
-    enc = BertEncoder(cfg, synth.bert_weights_device(cfg, seed=0), max_len=512)
+    weights = synth.bert_weights_device(cfg, seed=0)
 
     R = args.requests_per_gpu * world
     lens = synth.request_lengths(R, seed=2)
     ids = shard(lens, world, rank)
-    offsets = np.concatenate([[0], np.cumsum(lens)[:-1]])
-    my_tokens = int(sum(lens[i] for i in ids))
-    # request inputs resident in HBM (only this rank's requests), packed in id order
+    my_lens = np.array([lens[i] for i in ids], dtype=np.int64)
+    my_tokens = int(my_lens.sum())
+    my_off = np.concatenate([[0], np.cumsum(my_lens)]).astype(np.int64)
+    # this rank's request inputs, resident in HBM, packed in id order
     X_mine = synth.device_normal(max(my_tokens, 1), d, seed=1 + rank)
-    my_off = np.concatenate([[0], np.cumsum([lens[i] for i in ids])[:-1]]).astype(np.int64)
     max_count = int(max(np.bincount(nb.partition_lpt(lens, world), minlength=world)))
     out = torch.zeros((len(ids), d), dtype=torch.bfloat16, device="cuda")
     ids_t = torch.tensor(ids, dtype=torch.int64, device="cuda")
+    seq_off = torch.tensor(my_off, dtype=torch.int32, device="cuda")
+    cls_idx = torch.tensor(my_off[:-1], dtype=torch.int64, device="cuda")
+    max_len = int(my_lens.max()) if len(my_lens) else 1
 
-    cache = GraphCache(enc)
-    t_cap = time.perf_counter()
-    cache.capture_all([lens[i] for i in ids])
-    t_cap = time.perf_counter() - t_cap
+    t_setup = time.perf_counter()
+    if args.mode == "packed":
+        enc = BertPacked(cfg, weights, max_tokens=max(my_tokens, 1))
+        launches_per_step = enc.launches_per_forward()
+
+        def run_local(X):
+            if len(ids):
+                y = enc.forward(X, seq_off, max_len, T=my_tokens)
+                torch.index_select(y, 0, cls_idx, out=out)
+    else:
+        enc = BertEncoder(cfg, weights, max_len=512)
+        cache = GraphCache(enc)
+        cache.capture_all(my_lens)
+        launches_per_step = len(ids) * enc.launches_per_forward()
+
+        def run_local(X):
+            for j in range(len(ids)):
+                L, o = int(my_lens[j]), int(my_off[j])
+                cache.run(X[o:o + L], L, out[j])
+    t_setup = time.perf_counter() - t_setup
 
     def step():
-        for j, rid in enumerate(ids):
-            L = int(lens[rid])
-            o = int(my_off[j])
-            cache.run(X_mine[o:o + L], L, out[j])
+        run_local(X_mine)
         return gather_results(ids_t, out, max_count, world, rank)
 
     stream = torch.cuda.current_stream()
@@ -257,29 +278,36 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     value = R * args.steps / t_max
-    flops_step = sum(enc.flops(int(L)) for L in lens)
+    flops_step = BertPacked.flops(lens, d, cfg["ffn"], args.layers)
     tflops = flops_step * args.steps / t_max / 1e12
-    gpu_launches = args.steps * len(ids) * enc.launches_per_forward()
+    gpu_launches = args.steps * launches_per_step
 
-    # ---------------- dominant-kernel roofline: dense_dyn (tcgen05 GEMM) timed live with CUDA events
+    # ---------------- dominant-kernel roofline: dense_dyn (tcgen05 GEMM), CUDA events per launch
     roof = None
-    if not args.profile:
-        sample_ids = ids[: min(len(ids), 16)]
-        enc.trace = []
-        xin = cache.xin
-        # keep the GPU busy while the host enqueues, so each event pair brackets device time only
-        torch.cuda._sleep(int(4e8))
-        for rid in sample_ids:
-            L = int(lens[rid])
-            enc.forward(xin, L)
-        torch.cuda.synchronize()
+    if not args.profile and args.mode == "packed" and len(ids):
+        trace = []
+        orig = nb.dense_dyn_raw
+
+        def timed(*a):
+            e_a = torch.cuda.Event(enable_timing=True)
+            e_b = torch.cuda.Event(enable_timing=True)
+            e_a.record()
+            orig(*a)
+            e_b.record()
+            trace.append((a[9], a[10], a[11], a[13], e_a, e_b))
+        nb.dense_dyn_raw = timed
+        try:
+            torch.cuda._sleep(int(2e8))            # keep the GPU busy while the host enqueues
+            run_local(X_mine)
+            torch.cuda.synchronize()
+        finally:
+            nb.dense_dyn_raw = orig
         fl = by = tm = 0.0
-        for (M, N, K, epi, a, b) in enc.trace:
+        for (M, N, K, epi, a, b) in trace:
             fl += 2.0 * M * N * K
             by += 2.0 * (M * K + N * K) + 4.0 * N + 2.0 * M * N + (2.0 * M * N if epi == 3 else 0.0)
             tm += a.elapsed_time(b) / 1e3
-        enc.trace = None
-        n_launch = len([1 for _ in range(len(sample_ids) * 4 * args.layers)])
+        n = len(trace)
         t_tc, t_hbm = fl / (peaks["tc_sus"] * 1e12), by / (peaks["hbm"] * 1e9)
         bound = "tensor" if t_tc >= t_hbm else "hbm"
         if bound == "tensor":
@@ -287,12 +315,12 @@ def main():
         else:
             ach, pk, unit = by / tm / 1e9, peaks["hbm"], "GB/s"
         roof = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit, "frac": ach / pk, "traffic": None,
-                "kernel": "nimble::umma_gemm_kernel<0> (dense_dyn bf16, all 4 BERT-large GEMMs)",
-                "launches_sampled": n_launch, "avg_launch_us": 1e6 * tm / max(n_launch, 1),
-                "algorithmic_flops_per_launch": fl / max(n_launch, 1),
-                "algorithmic_bytes_per_launch": by / max(n_launch, 1),
-                "roofline_time_frac": max(t_tc, t_hbm) / tm,
-                "peak_note": f"{peaks['src']} sustained bf16 {peaks['tc_sus']} TFLOP/s / HBM {peaks['hbm']} GB/s"}
+                "kernel": "nimble::umma_gemm_kernel (dense_dyn bf16: QKV, O, FFN1, FFN2 at M = packed tokens)",
+                "launches": n, "avg_launch_us": 1e6 * tm / max(n, 1),
+                "algorithmic_flops_per_launch": fl / max(n, 1), "algorithmic_bytes_per_launch": by / max(n, 1),
+                "frac_of_burst_peak": fl / tm / 1e12 / peaks["tc"],
+                "peak_note": f"{peaks['src']}: sustained bf16 {peaks['tc_sus']} TFLOP/s (burst {peaks['tc']}), "
+                             f"HBM {peaks['hbm']} GB/s"}
 
     # ---------------- e2e: host buffers, H2D of inputs + D2H of results inside the timed region
     e2e = None
@@ -304,10 +332,7 @@ def main():
 
         def e2e_step():
             X_dev.copy_(host_in, non_blocking=True)
-            for j, rid in enumerate(ids):
-                L = int(lens[rid])
-                o = int(my_off[j])
-                cache.run(X_dev[o:o + L], L, out[j])
+            run_local(X_dev)
             host_out.copy_(out, non_blocking=True)
             r = gather_results(ids_t, out, max_count, world, rank)
             torch.cuda.current_stream().synchronize()
@@ -318,7 +343,6 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
         a0 = torch.cuda.Event(enable_timing=True)
         a1 = torch.cuda.Event(enable_timing=True)
         a0.record()
@@ -340,12 +364,15 @@ def main():
         res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-               "config": {"workload": WORKLOAD, "requests_per_gpu_per_step": args.requests_per_gpu,
+               "config": {"workload": WORKLOAD, "mode": args.mode,
+                          "requests_per_gpu_per_step": args.requests_per_gpu,
                           "requests_per_step": R, "tokens_per_step": int(lens.sum()), "layers": args.layers,
-                          "l2": "weights 604 MB/GPU > 126 MB L2: every request streams weights from HBM; no flush",
+                          "l2": "inputs 35 MB + weights 604 MB/GPU > 126 MB L2 per step; no flush",
                           "parallelism": f"dp-requests{world} (LPT shards, NCCL gather)",
-                          "execution": "per-L CUDA graphs of the dynamic kernels (captured once, "
-                                       f"{len(cache.graphs)} graphs in {t_cap:.1f} s)"},
+                          "execution": ("token-packed forward: 7 launches/layer (dense_dyn M=sum L_i x4, "
+                                        "attention_varlen, layernorm x2)" if args.mode == "packed" else
+                                        "per-L CUDA graphs of the batch-1 dynamic kernels"),
+                          "setup_s": round(t_setup, 2)},
                "tflops": tflops, "pct_tc_peak": tflops / peaks["tc_sus"],
                "gpu_launches": gpu_launches, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk}
         print(json.dumps(res))
