@@ -366,8 +366,8 @@ extern "C" int nimble_layernorm(const void *X, int64_t ldx, const float *gamma, 
     if (!X || !gamma || !beta || !Y) return fail(NIMBLE_E_NULL, "nimble_layernorm: NULL pointer");
     if (!ext_ok(rows) || !ext_ok(d)) return fail(NIMBLE_E_EXTENT, "nimble_layernorm: extents must be >= 1");
     if (d > 4096) return fail(NIMBLE_E_UNSUPPORTED, "nimble_layernorm: d > 4096 not built");
-    if (d % 8 || ldx % 8 || ldy % 8 || !aligned16(X) || !aligned16(Y))
-        return fail(NIMBLE_E_ALIGN, "nimble_layernorm: d, ldx, ldy must be multiples of 8 and bases 16-B aligned");
+    if (d % 8 || ldx % 8 || ldy % 8 || !aligned16(X) || !aligned16(Y) || !aligned16(gamma) || !aligned16(beta))
+        return fail(NIMBLE_E_ALIGN, "nimble_layernorm: d, ldx, ldy multiples of 8; X, Y, gamma, beta 16-B aligned");
     cudaError_t e = launch_layernorm(static_cast<const __nv_bfloat16 *>(X), ldx, gamma, beta, eps,
                                      static_cast<__nv_bfloat16 *>(Y), ldy, rows, d, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail("nimble_layernorm launch", e);

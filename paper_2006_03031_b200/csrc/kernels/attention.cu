@@ -5,15 +5,17 @@
 // equal dynamic dims; P:575 BERT's dynamic sequence length).  It replaces the
 // bmm_dyn -> softmax_rows -> bmm_dyn triple and never writes S or P to HBM.
 //
-// CTA = (query tile of 128, head, request).  128 threads.
+// CTA = (query tile of 128, head, request).  256 threads.
 //   warp 0 lane 0  TMA producer: Q tile [128 x 64] and all key tiles K[128 x 64] of the
 //                  request (128-B swizzle); after S is computed, the V blocks [64 x 64]
 //                  (MN-major operand) into the same smem.
 //   warp 1 lane 0  MMA issuer: S_kt = Q K_kt^T into TMEM columns [128 kt, 128 kt + 128),
 //                  then O = P V into TMEM columns [0, 64) (after S has been read).
-//   warps 0-3      softmax: thread = query row (TMEM lane); two passes over the row in
-//                  TMEM (max, then exp2 / sum), unnormalised P written as bf16 straight into
-//                  the UMMA K-major swizzled smem layout; epilogue O / rowsum -> bf16.
+//   warps 0-7      softmax: warp w owns TMEM lanes 32*(w%4).. (query rows) and every other
+//                  16-column chunk (w/4); two passes over the row in TMEM (max, then exp2 /
+//                  sum, combined across the two warpgroups through smem), unnormalised P
+//                  written as bf16 straight into the UMMA K-major swizzled smem layout;
+//                  epilogue O / rowsum -> bf16.
 // Keys >= L_i (the next request's rows, or TMA zero-fill past T) get P = 0; query rows
 // >= L_i are computed but never stored.
 #include <cstdint>
@@ -25,7 +27,7 @@ namespace nimble {
 
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;    // 8 warps: two warpgroups split every row's columns
 constexpr int kQBytes = 128 * 64 * 2;     // Q tile / one K tile: 16 KiB
 constexpr int kVBytes = 64 * 64 * 2;      // one V block (64 keys): 8 KiB
 constexpr int kPBlock = 128 * 64 * 2;     // one P k-block (64 keys): 16 KiB
@@ -106,22 +108,27 @@ __global__ void __launch_bounds__(kThreads)
     }
     __syncwarp();
 
-    // ---------------- softmax: thread = query row q (TMEM lane 32*warp + lane)
-    const int q = (int)(warp * 32 + lane);
-    const uint32_t trow = tmem + ((warp * 32u) << 16);
+    // ---------------- softmax: row q = TMEM lane 32*(warp%4) + lane, column chunks alternate by warp/4
+    const int quarter = (int)(warp & 3), half = (int)(warp >> 2);
+    const int q = quarter * 32 + (int)lane;
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    float *red = reinterpret_cast<float *>(tmem_slot + 4);      // [2][128] partial max, then sum
     ptx::mbar_wait(bar_s, 0);
     ptx::tc_fence_after();
     float mx = -INFINITY;
-    for (int c0 = 0; c0 < nk * 128; c0 += 16) {
+    for (int c0 = half * 16; c0 < nk * 128; c0 += 32) {
         float v[16];
         ptx::tmem_ld16(trow + (uint32_t)c0, v);
 #pragma unroll
         for (int e = 0; e < 16; ++e)
             if (c0 + e < L) mx = fmaxf(mx, v[e]);
     }
+    red[half * 128 + q] = mx;
+    __syncthreads();
+    mx = fmaxf(red[q], red[128 + q]);
     const float mx_s = mx * p.scale_log2;
     float sum = 0.f;
-    for (int c0 = 0; c0 < nkb * 64; c0 += 16) {
+    for (int c0 = half * 16; c0 < nkb * 64; c0 += 32) {
         float v[16];
         ptx::tmem_ld16(trow + (uint32_t)c0, v);
         uint32_t w[8];
@@ -139,6 +146,8 @@ __global__ void __launch_bounds__(kThreads)
         *reinterpret_cast<uint4 *>(rowp + (((c) ^ (q & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         *reinterpret_cast<uint4 *>(rowp + (((c + 1) ^ (q & 7)) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
     }
+    __syncthreads();                              // everyone has read red[] (max) before reuse
+    red[half * 128 + q] = sum;
     ptx::fence_async_smem();                      // P (generic stores) -> tensor-core reads
     ptx::tc_fence_before();                       // all S reads done before O overwrites cols 0..63
     __syncthreads();
@@ -160,11 +169,11 @@ __global__ void __launch_bounds__(kThreads)
     __syncwarp();
     ptx::mbar_wait(bar_o, 0);
     ptx::tc_fence_after();
-    const float inv = 1.f / sum;
+    const float inv = 1.f / (red[q] + red[128 + q]);
     const bool live = q0 + q < L;
     __nv_bfloat16 *dst = p.out + (int64_t)(o + q0 + q) * p.ld_out + h * 64;
 #pragma unroll
-    for (int c0 = 0; c0 < 64; c0 += 16) {
+    for (int c0 = half * 16; c0 < 64; c0 += 32) {
         float v[16];
         ptx::tmem_ld16(trow + (uint32_t)c0, v);
         if (live) {
@@ -190,7 +199,7 @@ __global__ void __launch_bounds__(kThreads)
 
 size_t attention_smem_bytes(int max_len) {
     const int mt = (max_len + 127) / 128;
-    return 1024 + (size_t)kQBytes * (1 + mt) + (size_t)mt * 2 * kPBlock + 256;
+    return 1024 + (size_t)kQBytes * (1 + mt) + (size_t)mt * 2 * kPBlock + 64 + 2 * 128 * 4;
 }
 
 cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const int32_t *seq_off,

@@ -59,27 +59,31 @@ __global__ void __launch_bounds__(256) softmax_rows_kernel(const float *__restri
     for (int64_t j = L + lane; j < ldP; j += 32) pr[j] = __float2bfloat16_rn(0.f);
 }
 
-// One 128-thread CTA per row; each thread keeps <= 32 values (d <= 4096, d % 8 == 0).
-__global__ void __launch_bounds__(128) layernorm_kernel(const __nv_bfloat16 *__restrict__ X, int64_t ldx,
-                                                        const float *__restrict__ g, const float *__restrict__ be,
-                                                        float eps, __nv_bfloat16 *__restrict__ Y, int64_t ldy,
-                                                        int d) {
-    __shared__ float red[4];
+// One warp per row, 8 rows per 256-thread CTA; lane l holds the 8-element chunks
+// l, l+32, l+64, ... of its row in registers (d <= 256 * CH, d % 8 == 0), so the two
+// statistics passes are register-only with warp-shuffle reductions (no __syncthreads).
+template <int CH>
+__global__ void __launch_bounds__(256) layernorm_warp_kernel(const __nv_bfloat16 *__restrict__ X, int64_t ldx,
+                                                             const float *__restrict__ g, const float *__restrict__ be,
+                                                             float eps, __nv_bfloat16 *__restrict__ Y, int64_t ldy,
+                                                             int64_t rows, int d) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
-    const int64_t row = blockIdx.x;
+    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const int lane = threadIdx.x & 31;
     const __nv_bfloat16 *x = X + row * ldx;
-    float v[32];
+    float v[CH * 8];
     float s = 0.f;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int j = (threadIdx.x + 128 * q) * 8;
+    for (int q = 0; q < CH; ++q) {
+        const int j = (lane + 32 * q) * 8;
         if (j < d) {
-            uint4 u = *reinterpret_cast<const uint4 *>(x + j);
+            const uint4 u = *reinterpret_cast<const uint4 *>(x + j);
             const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                float2 f = __bfloat1622float2(h[e]);
+                const float2 f = __bfloat1622float2(h[e]);
                 v[8 * q + 2 * e] = f.x;
                 v[8 * q + 2 * e + 1] = f.y;
             }
@@ -90,15 +94,11 @@ __global__ void __launch_bounds__(128) layernorm_kernel(const __nv_bfloat16 *__r
 #pragma unroll
         for (int e = 0; e < 8; ++e) s += v[8 * q + e];
     }
-    s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    const float mean = (red[0] + red[1] + red[2] + red[3]) / (float)d;
-    __syncthreads();
+    const float mean = warp_sum(s) / (float)d;
     float ss = 0.f;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int j = (threadIdx.x + 128 * q) * 8;
+    for (int q = 0; q < CH; ++q) {
+        const int j = (lane + 32 * q) * 8;
         if (j < d) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
@@ -107,21 +107,20 @@ __global__ void __launch_bounds__(128) layernorm_kernel(const __nv_bfloat16 *__r
             }
         }
     }
-    ss = warp_sum(ss);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-    __syncthreads();
-    const float var = (red[0] + red[1] + red[2] + red[3]) / (float)d;
-    const float inv = rsqrtf(var + eps);
+    const float inv = rsqrtf(warp_sum(ss) / (float)d + eps);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int j = (threadIdx.x + 128 * q) * 8;
+    for (int q = 0; q < CH; ++q) {
+        const int j = (lane + 32 * q) * 8;
         if (j < d) {
+            const float4 g0 = *reinterpret_cast<const float4 *>(g + j), g1 = *reinterpret_cast<const float4 *>(g + j + 4);
+            const float4 b0 = *reinterpret_cast<const float4 *>(be + j), b1 = *reinterpret_cast<const float4 *>(be + j + 4);
+            const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
             uint32_t w[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const int jj = j + 2 * e;
-                __nv_bfloat162 h2 = __floats2bfloat162_rn((v[8 * q + 2 * e] - mean) * inv * g[jj] + be[jj],
-                                                          (v[8 * q + 2 * e + 1] - mean) * inv * g[jj + 1] + be[jj + 1]);
+                __nv_bfloat162 h2 = __floats2bfloat162_rn((v[8 * q + 2 * e] - mean) * inv * gg[2 * e] + bb[2 * e],
+                                                          (v[8 * q + 2 * e + 1] - mean) * inv * gg[2 * e + 1] + bb[2 * e + 1]);
                 w[e] = *reinterpret_cast<uint32_t *>(&h2);
             }
             *reinterpret_cast<uint4 *>(Y + row * ldy + j) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -142,7 +141,10 @@ cudaError_t launch_softmax_rows(const float *S, int64_t ldS, int64_t strideS, __
 cudaError_t launch_layernorm(const __nv_bfloat16 *X, int64_t ldx, const float *g, const float *b, float eps,
                              __nv_bfloat16 *Y, int64_t ldy, int64_t rows, int64_t d, cudaStream_t s) {
     if (d > 4096 || d % 8) return cudaErrorInvalidValue;
-    return launch_pdl(layernorm_kernel, dim3((unsigned)rows), dim3(128), 0, s, X, ldx, g, b, eps, Y, ldy, (int)d);
+    const dim3 grid((unsigned)((rows + 7) / 8)), block(256);
+    if (d <= 1024) return launch_pdl(layernorm_warp_kernel<4>, grid, block, 0, s, X, ldx, g, b, eps, Y, ldy, rows, (int)d);
+    if (d <= 2048) return launch_pdl(layernorm_warp_kernel<8>, grid, block, 0, s, X, ldx, g, b, eps, Y, ldy, rows, (int)d);
+    return launch_pdl(layernorm_warp_kernel<16>, grid, block, 0, s, X, ldx, g, b, eps, Y, ldy, rows, (int)d);
 }
 
 }  // namespace nimble
