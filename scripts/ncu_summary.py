@@ -12,6 +12,7 @@ def run(args):
 def main(rep, top=12):
     raw = list(csv.reader(io.StringIO(run([rep, "--page", "raw", "--csv"]))))
     hdr = raw[0]
+    units = dict(zip(hdr, raw[1]))
     keys = ["Kernel Name", "Grid Size", "Block Size", "gpu__time_duration.sum", "dram__bytes_read.sum",
             "dram__bytes_write.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
@@ -21,7 +22,7 @@ def main(rep, top=12):
         d = dict(zip(hdr, row))
         for k in keys:
             if k in d:
-                print(f"  {k}: {d[k][:90]}")
+                print(f"  {k}: {d[k][:90]} {units.get(k, '')}")
     src = list(csv.reader(io.StringIO(run([rep, "--page", "source", "--csv", "--print-source", "sass"]))))
     i = [j for j, x in enumerate(src) if x and x[0] == "Address"][0]
     h = src[i]
@@ -29,8 +30,11 @@ def main(rep, top=12):
     S = h.index("Warp Stall Sampling (All Samples)")
     tot = sum(int(x[S] or 0) for x in rows if len(x) > S)
     print(f"  stall samples: {tot}")
-    for x in sorted(rows, key=lambda x: -int(x[S] or 0))[:top]:
-        print(f"    {x[S]:>6} {x[1][:100]}")
+    try:
+        for x in sorted(rows, key=lambda x: -int(x[S] or 0))[:top]:
+            print(f"    {x[S]:>6} {x[1][:100]}")
+    except BrokenPipeError:
+        pass
 
 
 if __name__ == "__main__":
