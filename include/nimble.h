@@ -120,6 +120,17 @@ int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, con
                      const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
                      int64_t K, int dt, int epi, void *stream);
 
+/* nimble_dense_static — measurement baseline: the SAME kernel source as nimble_dense_dyn
+ * instantiated with the extents as compile-time constants (the paper's static-shape
+ * codegen, fig:sym-codegen P:696-703; "kernels compiled with a single static shape",
+ * P:387).  Same arguments and dispatch record as nimble_dense_dyn.  Only compiled shapes
+ * are available: fp32 with M in 1..64 (any N, K), bf16 with EPI_BIAS and (M, N, K) in the
+ * table of umma_gemm.cu (BERT-large QKV/FFN2 shapes at M in {128, 384, 512, 513, 527,
+ * 2048, 2049, 8192}, BERT-base shapes at M = 128); else NIMBLE_E_UNSUPPORTED. */
+int nimble_dense_static(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+                        const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
+                        int64_t K, int dt, int epi, void *stream);
+
 /* ---------------------------------------------------------------------------
  * nimble_bmm_dyn — C[b] = alpha . A[b] . Bhat[b] over a strided batch (attention
  * heads), bf16 inputs, fp32 accumulation; out_dt = NIMBLE_F32 or NIMBLE_BF16.

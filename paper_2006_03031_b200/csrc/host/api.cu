@@ -166,9 +166,9 @@ extern "C" int nimble_last_dispatch(nimble_dispatch *out) {
 }
 
 // ------------------------------------------------------------------ dense_dyn
-extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
-                                const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
-                                int64_t K, int dt, int epi, void *stream) {
+static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+                      const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
+                      int64_t K, int dt, int epi, void *stream, bool static_twin) {
     // 1. shape function (runtime type-relation check)
     const int64_t xs[2] = {M, K}, ws[2] = {N, K};
     int64_t os[2];
@@ -191,7 +191,9 @@ extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64
         Simt8Params p{static_cast<const float *>(x), ldx, static_cast<const float *>(W), ldw, bias,
                       static_cast<const float *>(residual), ldr, static_cast<float *>(y), ldy,
                       (int32_t)M, (int32_t)N, (int32_t)K, epi, (int32_t)d.k};
-        cudaError_t e = launch_simt8(p, d.variant, dim3(d.grid[0], d.grid[1], d.grid[2]), s);
+        if (static_twin && M > 64) return fail(NIMBLE_E_UNSUPPORTED, "nimble_dense_static(f32): M must be in 1..64");
+        cudaError_t e = static_twin ? launch_simt8_static(p, dim3(d.grid[0], d.grid[1], d.grid[2]), s)
+                                    : launch_simt8(p, d.variant, dim3(d.grid[0], d.grid[1], d.grid[2]), s);
         if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn(f32) launch", e);
         record_dispatch(d);
         clear_error();
@@ -234,11 +236,25 @@ extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64
     }
     plan_pipeline(L, d);
     L.stream = s;
-    cudaError_t e = launch_umma_gemm(L);
+    if (static_twin && (epi != NIMBLE_EPI_BIAS || !umma_static_available(M, N, K)))
+        return fail(NIMBLE_E_UNSUPPORTED, "nimble_dense_static(bf16): (M, N, K) not compiled in, or epilogue != BIAS");
+    cudaError_t e = static_twin ? launch_umma_gemm_static(L, M, N, K) : launch_umma_gemm(L);
     if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn(bf16) launch", e);
     record_dispatch(d);
     clear_error();
     return NIMBLE_OK;
+}
+
+extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+                                const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
+                                int64_t K, int dt, int epi, void *stream) {
+    return dense_impl(x, ldx, W, ldw, bias, residual, ldr, y, ldy, M, N, K, dt, epi, stream, false);
+}
+
+extern "C" int nimble_dense_static(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+                                   const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
+                                   int64_t K, int dt, int epi, void *stream) {
+    return dense_impl(x, ldx, W, ldw, bias, residual, ldr, y, ldy, M, N, K, dt, epi, stream, true);
 }
 
 // ------------------------------------------------------------------ bmm_dyn

@@ -48,6 +48,8 @@ struct UmmaLaunch {
 };
 
 cudaError_t launch_umma_gemm(const UmmaLaunch &L);
+bool umma_static_available(int64_t M, int64_t N, int64_t K);
+cudaError_t launch_umma_gemm_static(const UmmaLaunch &L, int64_t M, int64_t N, int64_t K);
 size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed);
 // Programmatic dependent launch (griddepcontrol) on every libnimble launch that supports it.
 bool pdl_enabled();
@@ -82,6 +84,7 @@ struct Simt8Params {
     int32_t k_tiles;      // k = floor(M / 8)
 };
 cudaError_t launch_simt8(const Simt8Params &p, int variant, dim3 grid, cudaStream_t s);
+cudaError_t launch_simt8_static(const Simt8Params &p, dim3 grid, cudaStream_t s);   // M in 1..64
 
 size_t attention_smem_bytes(int max_len);
 cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const int32_t *seq_off,

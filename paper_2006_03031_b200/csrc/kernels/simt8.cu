@@ -88,7 +88,30 @@ __global__ void __launch_bounds__(128) simt8_dense_fallback(const Simt8Params p)
     simt8_tile<-1>(p, row0, min(8, p.M - row0));
 }
 
+// Static twin: M compile-time (k = M / 8 full tiles, tail of M % 8 rows).
+template <int SM>
+__global__ void __launch_bounds__(128) simt8_static_kernel(const Simt8Params p) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    constexpr int k = SM / 8, r = SM % 8;
+    const int row0 = blockIdx.y * 8;
+    if ((int)blockIdx.y < k) simt8_tile<8>(p, row0, 8);
+    else simt8_tile<r>(p, row0, r);
+}
+
+template <int SM>
+cudaError_t launch_static_rec(const Simt8Params &p, dim3 grid, cudaStream_t s) {
+    if constexpr (SM > 64) {
+        return cudaErrorInvalidValue;
+    } else {
+        if (p.M == SM) return launch_pdl(simt8_static_kernel<SM>, grid, dim3(128), 0, s, p);
+        return launch_static_rec<SM + 1>(p, grid, s);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_simt8_static(const Simt8Params &p, dim3 grid, cudaStream_t s) { return launch_static_rec<1>(p, grid, s); }
 
 cudaError_t launch_simt8(const Simt8Params &p, int variant, dim3 grid, cudaStream_t s) {
     switch (variant) {

@@ -47,15 +47,34 @@ __host__ __device__ inline int b_stage_bytes(int box_n, int b_mn) {
 }
 __host__ __device__ inline int pow2_cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
 
+// Tile geometry.  Dynamic kernels read it from the launch parameters; the static twin
+// (SM, SN, SK > 0: the paper's static-shape codegen baseline, fig:sym-codegen P:696-703)
+// derives it at compile time with the same DISPATCH.md rule.
+struct Geo {
+    int rows_a, rows_b, n_full, n_tail, tiles_m, tiles_n, box_n, kb_total;
+};
+template <int SM, int SN, int SK>
+__device__ __forceinline__ Geo make_geo(const UmmaParams &p) {
+    if constexpr (SM > 0) {
+        constexpr int t = SM < 2048 ? 128 : 256;
+        constexpr int r = SM % t;
+        constexpr int tiles_n = SM / t + (r ? 1 : 0);
+        constexpr int n_tail = r ? 16 * ((r + 15) / 16) : t;
+        return Geo{SN, SM, t, n_tail, (SN + 127) / 128, tiles_n, tiles_n == 1 ? n_tail : t, (SK + 63) / 64};
+    } else {
+        return Geo{p.rows_a, p.rows_b, p.n_full, p.n_tail, p.tiles_m, p.tiles_n, p.box_n, p.kb_total};
+    }
+}
+
 struct TileCoord {
     int m, n, b;
 };
-__device__ __forceinline__ TileCoord tile_of(const UmmaParams &p, int t) {
+__device__ __forceinline__ TileCoord tile_of(const Geo &g, int t) {
     TileCoord c;
-    c.m = t % p.tiles_m;
-    const int rest = t / p.tiles_m;
-    c.n = rest % p.tiles_n;
-    c.b = rest / p.tiles_n;
+    c.m = t % g.tiles_m;
+    const int rest = t / g.tiles_m;
+    c.n = rest % g.tiles_n;
+    c.b = rest / g.tiles_n;
     return c;
 }
 
@@ -66,24 +85,25 @@ __device__ __forceinline__ float epi_math(float acc, float alpha, float bias_i) 
     else return acc + bias_i;      // EPI 1, and 3 before the residual add
 }
 
-template <int B_MN, int EPI, int OUT_F32, int TRANS>
+template <int B_MN, int EPI, int OUT_F32, int TRANS, int SM = 0, int SN = 0, int SK = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
                      const UmmaParams p) {
     using OutT = typename std::conditional<OUT_F32, float, __nv_bfloat16>::type;
+    const Geo g = make_geo<SM, SN, SK>(p);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the 128-B swizzle atoms.  Offset the __shared__ array itself (no
     // integer round trip) so every derived pointer stays in the shared address space (STS/LDS,
     // not generic ST/LD through the LSU).
     uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const bool split = p.split > 1;
-    const int b_bytes = b_stage_bytes(p.box_n, B_MN);
+    const int b_bytes = b_stage_bytes(g.box_n, B_MN);
     const int stage_bytes = kABytes + b_bytes;
     const int ring_bytes = p.stages * stage_bytes;
-    const int part_bytes = split ? 128 * p.box_n * 4 : 0;
+    const int part_bytes = split ? 128 * g.box_n * 4 : 0;
     const int region0 = ring_bytes > part_bytes ? ring_bytes : part_bytes;
-    const int stg_bytes = split ? 128 * p.box_n * 4 : (TRANS ? 128 * p.box_n * (int)sizeof(OutT) : 0);
+    const int stg_bytes = split ? 128 * g.box_n * 4 : (TRANS ? 128 * g.box_n * (int)sizeof(OutT) : 0);
     uint8_t *stg = smem + region0;                 // epilogue staging / split-K receive buffer
     uint64_t *full_bar = reinterpret_cast<uint64_t *>(stg + stg_bytes);
     uint64_t *empty_bar = full_bar + p.stages;
@@ -95,15 +115,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
-    const int total_tiles = p.tiles_m * p.tiles_n * p.batch;
+    const int total_tiles = g.tiles_m * g.tiles_n * p.batch;
     // split: exactly one tile per CTA (cluster along z); else persistent over the tile grid
-    const int t_first = split ? ((int)(blockIdx.z / p.split) * p.tiles_n + (int)blockIdx.y) * p.tiles_m + (int)blockIdx.x
+    const int t_first = split ? ((int)(blockIdx.z / p.split) * g.tiles_n + (int)blockIdx.y) * g.tiles_m + (int)blockIdx.x
                               : (int)blockIdx.x;
     const int t_step = split ? total_tiles : (int)gridDim.x;
     const int split_q = split ? (int)(blockIdx.z % p.split) : 0;
-    const int kb0 = (int)((int64_t)split_q * p.kb_total / p.split);
-    const int kb1 = (int)((int64_t)(split_q + 1) * p.kb_total / p.split);
-    const uint32_t tmem_cols = split ? pow2_cols(p.box_n) : pow2_cols(2 * p.n_full);
+    const int kb0 = (int)((int64_t)split_q * g.kb_total / p.split);
+    const int kb1 = (int)((int64_t)(split_q + 1) * g.kb_total / p.split);
+    const uint32_t tmem_cols = split ? pow2_cols(g.box_n) : pow2_cols(2 * g.n_full);
     const int cta_lin = ((int)blockIdx.z * gridDim.y + (int)blockIdx.y) * gridDim.x + (int)blockIdx.x;
     unsigned long long *trace = p.trace ? p.trace + (size_t)cta_lin * 8 : nullptr;
 #define NIMBLE_TRACE(slot) do { if (trace) trace[slot] = ptx::globaltimer(); } while (0)
@@ -143,9 +163,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         bool first = true;
         for (int t = t_first; t < total_tiles; t += t_step) {
-            const TileCoord c = tile_of(p, t);
+            const TileCoord c = tile_of(g, t);
             const int32_t a_row = c.m * 128;
-            const int32_t b_row = c.n * p.n_full;
+            const int32_t b_row = c.n * g.n_full;
             const int32_t ab = p.a_bcast ? 0 : c.b;
             const int32_t bb = p.b_bcast ? 0 : c.b;
             auto load_a = [&](int st, int kb) {
@@ -158,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t *sb = smem + st * stage_bytes + kABytes;
                 const int32_t kc = kb * kBlockK;
                 if (B_MN) {
-                    const int chunks = (p.box_n + 63) / 64;
+                    const int chunks = (g.box_n + 63) / 64;
                     for (int q = 0; q < chunks; ++q) {
                         if (p.b_batch_mid) ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[st], b_row + 64 * q, bb, kc);
                         else ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[st], b_row + 64 * q, kc, bb);
@@ -202,12 +222,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = t_first; t < total_tiles; t += t_step) {
-            const TileCoord c = tile_of(p, t);
-            const int n_this = (c.n == p.tiles_n - 1) ? p.n_tail : p.n_full;
+            const TileCoord c = tile_of(g, t);
+            const int n_this = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
             const uint32_t idesc = ptx::idesc_bf16(128, (uint32_t)n_this, B_MN);
             ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);     // epilogue drained this accumulator
             ptx::tc_fence_after();
-            const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.n_full);
+            const uint32_t d_tmem = tmem_base + (uint32_t)(acc * g.n_full);
             for (int kb = kb0; kb < kb1; ++kb) {
                 ptx::mbar_wait(&full_bar[stage], phase);
                 ptx::tc_fence_after();
@@ -239,22 +259,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int half = ew >> 2;
         const int row_local = quarter * 32 + (int)lane;
         const bool leader = (ew == 0 && lane == 0);
-        const int res_bytes = 128 * p.box_n * 2;
+        const int res_bytes = 128 * g.box_n * 2;
         int acc = 0;
         uint32_t acc_phase = 0, res_phase = 0;
         if (EPI == 3 && TRANS && !split && leader && t_first < total_tiles) {
-            const TileCoord c = tile_of(p, t_first);
+            const TileCoord c = tile_of(g, t_first);
             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
-            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * 128, c.b, c.n * p.n_full);
-            else ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * 128, c.n * p.n_full, c.b);
+            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * 128, c.b, c.n * g.n_full);
+            else ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * 128, c.n * g.n_full, c.b);
         }
         for (int t = t_first; t < total_tiles; t += t_step) {
-            const TileCoord c = tile_of(p, t);
-            const int n_this = (c.n == p.tiles_n - 1) ? p.n_tail : p.n_full;
+            const TileCoord c = tile_of(g, t);
+            const int n_this = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
             const int i = c.m * 128 + row_local;
-            const int j0 = c.n * p.n_full;
-            const bool row_ok = i < p.rows_a;
-            const int n_valid = min(n_this, p.rows_b - j0);
+            const int j0 = c.n * g.n_full;
+            const bool row_ok = i < g.rows_a;
+            const int n_valid = min(n_this, g.rows_b - j0);
             float bias_i = 0.f;
             if (EPI >= 1 && row_ok) bias_i = __ldg(p.bias + i);
             const int64_t out_b = (int64_t)c.b * p.stride_out;
@@ -265,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             if (leader && t == t_first) NIMBLE_TRACE(3);
-            const uint32_t tmem_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.n_full);
+            const uint32_t tmem_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * g.n_full);
 
             if (!split) {
                 if (TRANS) {
@@ -297,10 +317,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::tma_store_commit_wait();                 // staging readable again
                         const int tn = t + t_step;
                         if (EPI == 3 && tn < total_tiles) {
-                            const TileCoord cn = tile_of(p, tn);
+                            const TileCoord cn = tile_of(g, tn);
                             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
-                            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * 128, cn.b, cn.n * p.n_full);
-                            else ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * 128, cn.n * p.n_full, cn.b);
+                            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * 128, cn.b, cn.n * g.n_full);
+                            else ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * 128, cn.n * g.n_full, cn.b);
                         }
                     }
                     ptx::named_bar_sync(2, kEpiThreads);
@@ -404,9 +424,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #undef NIMBLE_TRACE
 }
 
-template <int B_MN, int EPI, int OUT_F32, int TRANS>
+template <int B_MN, int EPI, int OUT_F32, int TRANS, int SM = 0, int SN = 0, int SK = 0>
 cudaError_t launch_t(const UmmaLaunch &L, cudaLaunchConfig_t &cfg) {
-    auto fn = umma_gemm_kernel<B_MN, EPI, OUT_F32, TRANS>;
+    auto fn = umma_gemm_kernel<B_MN, EPI, OUT_F32, TRANS, SM, SN, SK>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
@@ -417,6 +437,13 @@ cudaError_t launch_t(const UmmaLaunch &L, cudaLaunchConfig_t &cfg) {
 }
 
 }  // namespace
+
+// Static-shape twins (measurement only): (M, N, K) compiled in.
+#define NIMBLE_STATIC_GEMM_SHAPES(X)                                                                   \
+    X(128, 3072, 1024) X(384, 3072, 1024) X(512, 3072, 1024) X(513, 3072, 1024) X(527, 3072, 1024)     \
+    X(2048, 3072, 1024) X(2049, 3072, 1024) X(8192, 3072, 1024) X(128, 1024, 4096) X(384, 1024, 4096)  \
+    X(512, 1024, 4096) X(513, 1024, 4096) X(527, 1024, 4096) X(2048, 1024, 4096) X(2049, 1024, 4096)   \
+    X(8192, 1024, 4096) X(128, 2304, 768) X(128, 768, 768) X(128, 3072, 768) X(128, 768, 3072)
 
 bool pdl_enabled() {
     static const bool on = [] {
@@ -436,6 +463,47 @@ size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out
     const size_t part = split > 1 ? (size_t)128 * box_n * 4 : 0;
     const size_t stg = split > 1 ? (size_t)128 * box_n * 4 : (transposed ? (size_t)128 * box_n * out_bytes : 0);
     return 1024 /* alignment slack */ + (ring > part ? ring : part) + stg + kTailBytes;
+}
+
+bool umma_static_available(int64_t M, int64_t N, int64_t K) {
+#define NIMBLE_X(m, n, k) if (M == m && N == n && K == k) return true;
+    NIMBLE_STATIC_GEMM_SHAPES(NIMBLE_X)
+#undef NIMBLE_X
+    return false;
+}
+
+static void fill_cfg(const UmmaLaunch &L, cudaLaunchConfig_t &cfg, cudaLaunchAttribute *attr) {
+    cfg = {};
+    cfg.gridDim = L.grid;
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = L.smem_bytes;
+    cfg.stream = L.stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 0;
+    if (L.p.split > 1) {
+        attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+        attr[cfg.numAttrs].val.clusterDim.x = 1;
+        attr[cfg.numAttrs].val.clusterDim.y = 1;
+        attr[cfg.numAttrs].val.clusterDim.z = (unsigned)L.p.split;
+        cfg.numAttrs++;
+    }
+    if (pdl_enabled()) {
+        attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+        cfg.numAttrs++;
+    }
+}
+
+// Static twin of the bias-epilogue dense kernel: identical source, M/N/K compile-time.
+cudaError_t launch_umma_gemm_static(const UmmaLaunch &L, int64_t M, int64_t N, int64_t K) {
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr[2];
+    fill_cfg(L, cfg, attr);
+#define NIMBLE_X(m, n, k) \
+    if (M == m && N == n && K == k) return launch_t<0, 1, 0, 1, m, n, k>(L, cfg);
+    NIMBLE_STATIC_GEMM_SHAPES(NIMBLE_X)
+#undef NIMBLE_X
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_umma_gemm(const UmmaLaunch &L) {

@@ -63,6 +63,7 @@ _SIGS = {
     "nimble_get_variant_limit": [],
     "nimble_last_dispatch": [C.POINTER(Dispatch)],
     "nimble_dense_dyn": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, C.c_int, C.c_int, _vp],
+    "nimble_dense_static": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, C.c_int, C.c_int, _vp],
     "nimble_bmm_dyn": [_vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
                        C.c_float, C.c_int, C.c_int, _vp],
     "nimble_softmax_rows": [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
@@ -197,6 +198,16 @@ def dense_dyn(x, W, bias, y, epi=EPI_BIAS, residual=None, M=None, stream=None):
     _check(_lib.nimble_dense_dyn(_ptr(x), x.stride(0), _ptr(W), W.stride(0), _ptr(bias), _ptr(residual),
                                  residual.stride(0) if residual is not None else 0, _ptr(y), y.stride(0),
                                  M, N, K, _dt(x), epi, _stream(stream)))
+    return y
+
+
+def dense_static(x, W, bias, y, epi=EPI_BIAS, residual=None, M=None, stream=None):
+    """The static-shape twin of dense_dyn (measurement baseline; compiled shapes only)."""
+    M = x.shape[0] if M is None else M
+    N, K = W.shape
+    _check(_lib.nimble_dense_static(_ptr(x), x.stride(0), _ptr(W), W.stride(0), _ptr(bias), _ptr(residual),
+                                    residual.stride(0) if residual is not None else 0, _ptr(y), y.stride(0),
+                                    M, N, K, _dt(x), epi, _stream(stream)))
     return y
 
 

@@ -221,3 +221,30 @@ def test_bmm_integer_exact(nb, orc):
     nb.bmm_dyn(P, ldP, L * ldP, Bt, dh, L * dh, 1, C2, dh, L * dh, H, L, dh, L)
     ref2, _ = orc.bmm(P[:, :, :L].double().cpu().numpy(), Bt.double().cpu().numpy(), 1)
     assert np.array_equal(C2.double().cpu().numpy(), ref2)
+
+
+# ------------------------------------------------------------------ static twins
+def test_static_twin_bitwise_equal(nb, orc):
+    # the static-shape instantiation computes exactly what the symbolic kernel computes
+    for (M, N, K) in ((128, 3072, 1024), (527, 3072, 1024), (513, 1024, 4096), (128, 768, 3072)):
+        W = synth.normal((N, K), 0.05, 3 + M)
+        b = synth.normal((N,), 0.1, 4 + M, torch.float32)
+        x = synth.normal((M, K), 1.0, 5 + M)
+        y1 = _dense_gpu(nb, x, W, b, nb.EPI_BIAS)
+        Wd, bd, xd = W.cuda(), b.cuda(), x.cuda()
+        y2 = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        nb.dense_static(xd, Wd, bd, y2)
+        torch.cuda.synchronize()
+        assert torch.equal(y1, y2), (M, N, K)
+    for M in (1, 8, 13, 64):
+        x, W, b = synth.config1_dense(M)
+        y1 = _dense_gpu(nb, x, W, b, nb.EPI_BIAS)
+        y2 = torch.empty((M, 128), dtype=torch.float32, device="cuda")
+        nb.dense_static(x.cuda(), W.cuda(), b.cuda(), y2)
+        torch.cuda.synchronize()
+        assert torch.equal(y1, y2), M
+    with pytest.raises(nb.NimbleError):
+        nb.dense_static(torch.zeros((77, 1024), dtype=torch.bfloat16, device="cuda"),
+                        torch.zeros((3072, 1024), dtype=torch.bfloat16, device="cuda"),
+                        torch.zeros((3072,), device="cuda"),
+                        torch.zeros((77, 3072), dtype=torch.bfloat16, device="cuda"))
