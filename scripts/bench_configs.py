@@ -1,0 +1,99 @@
+"""Latency measurements for BASELINE configs 2, 3, 4 (BJ:8-10) on one B200.
+
+config 2: 2-layer LSTM LM, I = H = 650, batch 1, T in {35, 128, 512}: us/token (hoisted input
+          GEMM via dense_dyn + persistent recurrence, all on one stream, CUDA events).
+config 3: BERT-base, batch 1, every L in 1..128: per-request latency (per-L CUDA graph of the
+          12-layer batch-1 path) -> us/token; plus the packed equivalent.
+config 4: Tree-LSTM (300/150) forests of 1 and 32 random trees: us/tree, us/leaf.
+Paper context (other hardware): LSTM 2L Nimble T4 107.4 us/token (300/512); BERT-base
+Nimble T4 95.2 us/token; Tree-LSTM Nimble Intel 40.3 us/token.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2006_03031_b200 import synth  # noqa: E402
+from paper_2006_03031_b200.bert import BertEncoder, BertPacked  # noqa: E402
+from paper_2006_03031_b200.rnn import LSTMStack, TreeLSTM, TreeSchedule  # noqa: E402
+from paper_2006_03031_b200.serve import GraphCache  # noqa: E402
+
+
+def ev_time(fn, reps=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / 1e3 / reps
+
+
+def main():
+    rep = {}
+    # ---- config 2
+    I = H = 650
+    st = LSTMStack(synth.lstm_weights(I, H, 2, seed=0), max_T=512)
+    c2 = []
+    for T in (1, 35, 128, 512):
+        x = torch.zeros((T, st.Ip), dtype=torch.float32, device="cuda")
+        x[:, :I] = synth.lstm_input(T, I, seed=1).cuda()
+        t = ev_time(lambda: st.forward(x, T))
+        c2.append({"T": T, "us_per_seq": t * 1e6, "us_per_token": t * 1e6 / T,
+                   "gflops": st.flops_per_token() * T / t / 1e9})
+        print(json.dumps(c2[-1]), flush=True)
+    rep["config2_lstm_650x2"] = c2
+    # ---- config 3 (batch-1 graphs, every L in 1..128)
+    cfg = dict(synth.BERT_BASE)
+    w = synth.bert_weights_device(cfg, seed=0)
+    enc = BertEncoder(cfg, w, max_len=128)
+    cache = GraphCache(enc)
+    c3 = []
+    out = torch.empty((cfg["d"],), dtype=torch.bfloat16, device="cuda")
+    for L in range(1, 129):
+        cache.capture(L)
+        x = synth.device_normal(L, cfg["d"], seed=L)
+        t = ev_time(lambda: cache.run(x, L, out), reps=5, warm=2)
+        fl = enc.flops(L)
+        c3.append({"L": L, "us": t * 1e6, "us_per_token": t * 1e6 / L, "tflops": fl / t / 1e12})
+    rep["config3_bert_base_batch1"] = c3
+    print(json.dumps({k: c3[i] for k, i in (("L1", 0), ("L64", 63), ("L128", 127))}), flush=True)
+    # packed BERT-base: 64 requests with L ~ U{1..128}
+    lens = synth.request_lengths(64, seed=2, hi=128)
+    Tt = int(lens.sum())
+    pk = BertPacked(cfg, w, max_tokens=Tt)
+    off = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
+    X = synth.device_normal(Tt, cfg["d"], seed=3)
+    t = ev_time(lambda: pk.forward(X, off, int(lens.max())))
+    rep["config3_bert_base_packed64"] = {"requests": 64, "tokens": Tt, "ms": t * 1e3, "req_per_s": 64 / t,
+                                        "us_per_token": t * 1e6 / Tt,
+                                        "tflops": BertPacked.flops(lens, cfg["d"], cfg["ffn"], cfg["layers"]) / t / 1e12}
+    print(json.dumps(rep["config3_bert_base_packed64"]), flush=True)
+    # ---- config 4
+    I, Hh = 300, 150
+    W_l, b_l, U, b_u = synth.tree_weights(I, Hh)
+    model = TreeLSTM(W_l, b_l, U, b_u)
+    c4 = []
+    for n in (1, 32):
+        trees, nw = synth.random_forest(n, seed=2)
+        sched = TreeSchedule(trees)
+        X = synth.normal((nw, I), 1.0, 4, torch.float32).cuda()
+        t = ev_time(lambda: model.forward(X, sched))
+        c4.append({"trees": n, "leaves": sched.n_leaves, "levels": len(sched.levels), "us_per_forest": t * 1e6,
+                   "us_per_tree": t * 1e6 / n, "us_per_leaf": t * 1e6 / sched.n_leaves})
+        print(json.dumps(c4[-1]), flush=True)
+    rep["config4_treelstm_300_150"] = c4
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/configs_report.json", "w") as f:
+        json.dump(rep, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
