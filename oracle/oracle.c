@@ -124,7 +124,9 @@ static int orc_umma_t(int64_t batch, int64_t M, int64_t N, int64_t K, int c, orc
     int64_t mt = orc_ceil_div(N, 128), nt = d->k + (d->r > 0);
     d->split_k = (t == 128) ? orc_split(mt * nt * batch, K) : 1;
     d->grid[0] = (int32_t)mt; d->grid[1] = (int32_t)nt; d->grid[2] = (int32_t)(batch * d->split_k);
-    d->cluster[0] = 1; d->cluster[1] = 1; d->cluster[2] = d->split_k;
+    /* family 3 runs CTA pairs (tcgen05 cta_group::2): one 256-row MMA per pair */
+    d->cluster[0] = (t == 128) ? 1 : 2; d->cluster[1] = 1; d->cluster[2] = d->split_k;
+    if (t == 256) d->umma_m = 256;
     return ORC_OK;
 }
 

@@ -129,17 +129,18 @@ void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
     int st = kb_per_split < 8 ? kb_per_split : 8;
     if (st < 1) st = 1;
     // largest depth that fits next to the epilogue staging
-    while (st > 1 && umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed) > 232448) --st;
+    while (st > 1 && umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair) > 232448) --st;
     L.p.stages = st;
-    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed);
-    L.p.tiles_m = d.grid[0];
+    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair);
+    L.p.tiles_m = L.pair ? (L.p.rows_a + 255) / 256 : d.grid[0];   // pairs own 256-row tiles
     L.p.tiles_n = d.grid[1];
     L.p.batch = d.grid[2] / d.split_k;
     if (L.p.split > 1) {
         L.grid = dim3(d.grid[0], d.grid[1], d.grid[2]);
     } else {
-        const int64_t tiles = (int64_t)d.grid[0] * d.grid[1] * d.grid[2];
-        L.grid = dim3((unsigned)(tiles < kNumSMs ? tiles : kNumSMs), 1, 1);
+        const int64_t tiles = (int64_t)L.p.tiles_m * L.p.tiles_n * L.p.batch;
+        const int64_t slots = L.pair ? kNumSMs / 2 : kNumSMs;
+        L.grid = dim3((unsigned)((tiles < slots ? tiles : slots) * (L.pair ? 2 : 1)), 1, 1);
     }
 }
 
@@ -225,8 +226,10 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     L.p.res = residual;
     L.p.ld_res = ldr;
     L.p.a_static = pdl_enabled() ? 1 : 0;   // weights: fetched before the PDL grid-dependency wait
+    L.pair = (d.family == 3) ? 1 : 0;       // large M: 2-CTA pairs, each CTA loads half of B
+    const int box_b = L.pair ? L.p.box_n / 2 : L.p.box_n;
     if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
-    if ((st = encode_operand(&L.tmB, x, K, M, ldx, 1, 0, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+    if ((st = encode_operand(&L.tmB, x, K, M, ldx, 1, 0, box_b, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
     if ((st = encode_out(&L.tmOut, y, false, N, M, ldy, 1, 0, L.p.box_n, &L.p.out_batch_mid)) != NIMBLE_OK) return st;
     if (epi == NIMBLE_EPI_BIAS_RESIDUAL) {
         int mid = 0;
@@ -234,6 +237,8 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     } else {
         L.tmRes = L.tmOut;
     }
+    L.p.box_n = box_b;
+    if (L.pair && (L.p.a_batch_mid || L.p.b_batch_mid)) return fail(NIMBLE_E_UNSUPPORTED, "pair mode needs row-major batches");
     plan_pipeline(L, d);
     L.stream = s;
     if (static_twin && (epi != NIMBLE_EPI_BIAS || !umma_static_available(M, N, K)))
@@ -299,11 +304,14 @@ extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const
         L.p.n_tail = d.r ? d.umma_n_tail : d.umma_n_full;
         L.p.box_n = (d.grid[1] == 1) ? L.p.n_tail : d.umma_n_full;
         L.transposed = 1;
+        L.pair = (d.family == 3) ? 1 : 0;
+        const int box_b = L.pair ? L.p.box_n / 2 : L.p.box_n;
         if ((st = encode_operand(&L.tmA, B, K, N, ldb, batch, strideB, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
-        if ((st = encode_operand(&L.tmB, A, K, M, lda, batch, strideA, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+        if ((st = encode_operand(&L.tmB, A, K, M, lda, batch, strideA, box_b, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
         if ((st = encode_out(&L.tmOut, Cout, out_dt == NIMBLE_F32, N, M, ldc, batch, strideC, L.p.box_n,
                              &L.p.out_batch_mid)) != NIMBLE_OK) return st;
         L.tmRes = L.tmOut;
+        L.p.box_n = box_b;
     } else {
         // family 2: A rows (M) on the UMMA-M slot, columns of B (N) MN-major on the UMMA-N slot
         L.b_mn_major = 1;

@@ -89,7 +89,9 @@ int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, 
     d->grid[0] = static_cast<int32_t>(m_tiles);
     d->grid[1] = static_cast<int32_t>(n_tiles);
     d->grid[2] = static_cast<int32_t>(batch * d->split_k);
-    d->cluster[0] = 1;
+    const bool pair = (f.id == kUMMA_T256.id);             // family 3: CTA pairs, cta_group::2
+    d->umma_m = pair ? 256 : 128;
+    d->cluster[0] = pair ? 2 : 1;
     d->cluster[1] = 1;
     d->cluster[2] = d->split_k;
     return NIMBLE_OK;

@@ -43,6 +43,7 @@ struct UmmaLaunch {
     UmmaParams p;
     dim3 grid;
     int b_mn_major, epi, out_f32, transposed;
+    int pair;              // 1: 2-CTA clusters (tcgen05 cta_group::2, 256-row tiles)
     size_t smem_bytes;
     cudaStream_t stream;
 };
@@ -50,7 +51,7 @@ struct UmmaLaunch {
 cudaError_t launch_umma_gemm(const UmmaLaunch &L);
 bool umma_static_available(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_umma_gemm_static(const UmmaLaunch &L, int64_t M, int64_t N, int64_t K);
-size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed);
+size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed, int pair);
 // Programmatic dependent launch (griddepcontrol) on every libnimble launch that supports it.
 bool pdl_enabled();
 

@@ -85,7 +85,7 @@ __device__ __forceinline__ float epi_math(float acc, float alpha, float bias_i) 
     else return acc + bias_i;      // EPI 1, and 3 before the residual add
 }
 
-template <int B_MN, int EPI, int OUT_F32, int TRANS, int SM = 0, int SN = 0, int SK = 0>
+template <int B_MN, int EPI, int OUT_F32, int TRANS, int PAIR = 0, int SM = 0, int SN = 0, int SK = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
@@ -101,9 +101,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int b_bytes = b_stage_bytes(g.box_n, B_MN);
     const int stage_bytes = kABytes + b_bytes;
     const int ring_bytes = p.stages * stage_bytes;
-    const int part_bytes = split ? 128 * g.box_n * 4 : 0;
+    // PAIR: each CTA of the pair holds half of the B rows (box_n); output tiles are 2x box_n wide
+    const int n_stage = PAIR ? 2 * g.box_n : g.box_n;
+    const int part_bytes = split ? 128 * n_stage * 4 : 0;
     const int region0 = ring_bytes > part_bytes ? ring_bytes : part_bytes;
-    const int stg_bytes = split ? 128 * g.box_n * 4 : (TRANS ? 128 * g.box_n * (int)sizeof(OutT) : 0);
+    const int stg_bytes = split ? 128 * n_stage * 4 : (TRANS ? 128 * n_stage * (int)sizeof(OutT) : 0);
     uint8_t *stg = smem + region0;                 // epilogue staging / split-K receive buffer
     uint64_t *full_bar = reinterpret_cast<uint64_t *>(stg + stg_bytes);
     uint64_t *empty_bar = full_bar + p.stages;
@@ -116,10 +118,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
     const int total_tiles = g.tiles_m * g.tiles_n * p.batch;
+    // PAIR: a cluster of 2 CTAs shares every 256-row tile (cta_group::2), rank r owns rows 128r..
+    const uint32_t prank = PAIR ? ptx::cluster_ctarank() : 0u;
+    constexpr int kRowsPerTile = PAIR ? 256 : 128;
     // split: exactly one tile per CTA (cluster along z); else persistent over the tile grid
     const int t_first = split ? ((int)(blockIdx.z / p.split) * g.tiles_n + (int)blockIdx.y) * g.tiles_m + (int)blockIdx.x
-                              : (int)blockIdx.x;
-    const int t_step = split ? total_tiles : (int)gridDim.x;
+                              : (int)blockIdx.x / (PAIR ? 2 : 1);
+    const int t_step = split ? total_tiles : (int)gridDim.x / (PAIR ? 2 : 1);
     const int split_q = split ? (int)(blockIdx.z % p.split) : 0;
     const int kb0 = (int)((int64_t)split_q * g.kb_total / p.split);
     const int kb1 = (int)((int64_t)(split_q + 1) * g.kb_total / p.split);
@@ -140,38 +145,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], kEpiThreads / 32);
+            ptx::mbar_init(&tempty[a], (PAIR ? 2 : 1) * kEpiThreads / 32);
         }
         ptx::mbar_init(res_bar, 1);
         ptx::mbar_init(recv_bar, 1);
         ptx::fence_mbar_init();
         ptx::fence_async_smem();
     }
-    if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
+    if (warp == 2) {
+        if (PAIR) ptx::tmem_alloc_pair(tmem_slot, tmem_cols);
+        else ptx::tmem_alloc(tmem_slot, tmem_cols);
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    if (split) ptx::cluster_sync();                // peers' barriers exist before any DSMEM copy
+    if (split || PAIR) ptx::cluster_sync();        // peers' barriers exist before any remote arrive / copy
     const uint32_t tmem_base = *tmem_slot;
     ptx::pdl_trigger();                            // the next kernel's prologue may start now
     if (threadIdx.x == 0) NIMBLE_TRACE(1);
 
     if (warp == 0 && lane == 0) {
         // ================= TMA producer
-        const uint32_t tx = kABytes + b_bytes;
+        const uint32_t tx = (PAIR ? 2u : 1u) * (kABytes + b_bytes);    // PAIR: rank 0 expects both halves
+        const bool arms = !PAIR || prank == 0;                          // who arms the full barriers
         int stage = 0;
         uint32_t phase = 0;
         bool first = true;
         for (int t = t_first; t < total_tiles; t += t_step) {
             const TileCoord c = tile_of(g, t);
-            const int32_t a_row = c.m * 128;
-            const int32_t b_row = c.n * g.n_full;
+            const int n_this_p = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
+            const int32_t a_row = c.m * kRowsPerTile + (int)prank * 128;
+            const int32_t b_row = c.n * g.n_full + (PAIR ? (int)prank * (n_this_p / 2) : 0);
             const int32_t ab = p.a_bcast ? 0 : c.b;
             const int32_t bb = p.b_bcast ? 0 : c.b;
             auto load_a = [&](int st, int kb) {
                 uint8_t *sa = smem + st * stage_bytes;
                 const int32_t kc = kb * kBlockK;
-                if (p.a_batch_mid) ptx::tma_load_3d(sa, &tmA, &full_bar[st], kc, ab, a_row);
+                if (PAIR) ptx::tma_load_3d_pair(sa, &tmA, &full_bar[st], kc, a_row, ab);
+                else if (p.a_batch_mid) ptx::tma_load_3d(sa, &tmA, &full_bar[st], kc, ab, a_row);
                 else ptx::tma_load_3d(sa, &tmA, &full_bar[st], kc, a_row, ab);
             };
             auto load_b = [&](int st, int kb) {
@@ -184,7 +195,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[st], b_row + 64 * q, kc, bb);
                     }
                 } else {
-                    if (p.b_batch_mid) ptx::tma_load_3d(sb, &tmB, &full_bar[st], kc, bb, b_row);
+                    if (PAIR) ptx::tma_load_3d_pair(sb, &tmB, &full_bar[st], kc, b_row, bb);
+                    else if (p.b_batch_mid) ptx::tma_load_3d(sb, &tmB, &full_bar[st], kc, bb, b_row);
                     else ptx::tma_load_3d(sb, &tmB, &full_bar[st], kc, b_row, bb);
                 }
             };
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // are requested before the grid-dependency wait
                 const int npre = min(p.stages, kb1 - kb0);
                 for (int s = 0; s < npre; ++s) {
-                    ptx::mbar_arrive_expect_tx(&full_bar[s], tx);
+                    if (arms) ptx::mbar_arrive_expect_tx(&full_bar[s], tx);
                     if (p.a_static) load_a(s, kb0 + s);
                 }
                 ptx::pdl_wait();
@@ -209,14 +221,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             for (; kb < kb1; ++kb) {
                 ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-                ptx::mbar_arrive_expect_tx(&full_bar[stage], tx);
+                if (arms) ptx::mbar_arrive_expect_tx(&full_bar[stage], tx);
                 load_a(stage, kb);
                 load_b(stage, kb);
                 if (++stage == p.stages) { stage = 0; phase ^= 1; }
             }
         }
-    } else if (warp == 1 && lane == 0) {
-        // ================= MMA issuer (single thread)
+    } else if (warp == 1 && lane == 0 && (!PAIR || prank == 0)) {
+        // ================= MMA issuer (single thread; the even CTA of a pair issues for both)
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
@@ -224,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = t_first; t < total_tiles; t += t_step) {
             const TileCoord c = tile_of(g, t);
             const int n_this = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
-            const uint32_t idesc = ptx::idesc_bf16(128, (uint32_t)n_this, B_MN);
+            const uint32_t idesc = ptx::idesc_bf16(PAIR ? 256u : 128u, (uint32_t)n_this, B_MN);
             ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);     // epilogue drained this accumulator
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)(acc * g.n_full);
@@ -242,12 +254,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < kBlockK / 16; ++kk) {
                     const uint64_t a_k = adesc + (uint64_t)((kk * 32) >> 4);            // +32 B along K
                     const uint64_t b_k = bdesc + (uint64_t)(B_MN ? ((kk * 2048) >> 4) : ((kk * 32) >> 4));
-                    ptx::umma_bf16(d_tmem, a_k, b_k, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                    if (PAIR) ptx::umma_bf16_pair(d_tmem, a_k, b_k, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                    else ptx::umma_bf16(d_tmem, a_k, b_k, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
                 }
-                ptx::umma_commit(&empty_bar[stage]);         // smem stage free once these MMAs retire
+                if (PAIR) ptx::umma_commit_pair(&empty_bar[stage], 0x3);   // frees the stage in both CTAs
+                else ptx::umma_commit(&empty_bar[stage]);    // smem stage free once these MMAs retire
                 if (++stage == p.stages) { stage = 0; phase ^= 1; }
             }
-            ptx::umma_commit(&tfull[acc]);                   // accumulator complete
+            if (PAIR) ptx::umma_commit_pair(&tfull[acc], 0x3);
+            else ptx::umma_commit(&tfull[acc]);              // accumulator complete
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
@@ -259,19 +274,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int half = ew >> 2;
         const int row_local = quarter * 32 + (int)lane;
         const bool leader = (ew == 0 && lane == 0);
-        const int res_bytes = 128 * g.box_n * 2;
+        const int res_bytes = 128 * n_stage * 2;
+        const int row_base = (int)prank * 128;
         int acc = 0;
         uint32_t acc_phase = 0, res_phase = 0;
         if (EPI == 3 && TRANS && !split && leader && t_first < total_tiles) {
             const TileCoord c = tile_of(g, t_first);
             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
-            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * 128, c.b, c.n * g.n_full);
-            else ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * 128, c.n * g.n_full, c.b);
+            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * kRowsPerTile + row_base, c.b, c.n * g.n_full);
+            else ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * kRowsPerTile + row_base, c.n * g.n_full, c.b);
         }
         for (int t = t_first; t < total_tiles; t += t_step) {
             const TileCoord c = tile_of(g, t);
             const int n_this = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
-            const int i = c.m * 128 + row_local;
+            const int i = c.m * kRowsPerTile + row_base + row_local;
             const int j0 = c.n * g.n_full;
             const bool row_ok = i < g.rows_a;
             const int n_valid = min(n_this, g.rows_b - j0);
@@ -308,19 +324,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&tempty[acc]);   // TMEM may be overwritten now
+                    if (lane == 0) {                                 // TMEM may be overwritten now
+                        if (PAIR) ptx::mbar_arrive_cluster(ptx::map_shared_rank(ptx::smem_u32(&tempty[acc]), 0));
+                        else ptx::mbar_arrive(&tempty[acc]);
+                    }
                     ptx::fence_async_smem();
                     ptx::named_bar_sync(1, kEpiThreads);
                     if (leader) {
-                        if (p.out_batch_mid) ptx::tma_store_3d(&tmOut, stg, c.m * 128, c.b, j0);
-                        else ptx::tma_store_3d(&tmOut, stg, c.m * 128, j0, c.b);
+                        if (p.out_batch_mid) ptx::tma_store_3d(&tmOut, stg, c.m * kRowsPerTile + row_base, c.b, j0);
+                        else ptx::tma_store_3d(&tmOut, stg, c.m * kRowsPerTile + row_base, j0, c.b);
                         ptx::tma_store_commit_wait();                 // staging readable again
                         const int tn = t + t_step;
                         if (EPI == 3 && tn < total_tiles) {
                             const TileCoord cn = tile_of(g, tn);
                             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
-                            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * 128, cn.b, cn.n * g.n_full);
-                            else ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * 128, cn.n * g.n_full, cn.b);
+                            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * kRowsPerTile + row_base, cn.b, cn.n * g.n_full);
+                            else ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * kRowsPerTile + row_base, cn.n * g.n_full, cn.b);
                         }
                     }
                     ptx::named_bar_sync(2, kEpiThreads);
@@ -415,18 +434,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     ptx::tc_fence_before();
     __syncthreads();
-    if (split) ptx::cluster_sync();      // every peer has received: our smem may go away
+    if (split || PAIR) ptx::cluster_sync();   // peers are done with our smem / barriers / TMEM
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, tmem_cols);
+        if (PAIR) ptx::tmem_dealloc_pair(tmem_base, tmem_cols);
+        else ptx::tmem_dealloc(tmem_base, tmem_cols);
     }
     if (threadIdx.x == 0) NIMBLE_TRACE(6);
 #undef NIMBLE_TRACE
 }
 
-template <int B_MN, int EPI, int OUT_F32, int TRANS, int SM = 0, int SN = 0, int SK = 0>
+template <int B_MN, int EPI, int OUT_F32, int TRANS, int PAIR = 0, int SM = 0, int SN = 0, int SK = 0>
 cudaError_t launch_t(const UmmaLaunch &L, cudaLaunchConfig_t &cfg) {
-    auto fn = umma_gemm_kernel<B_MN, EPI, OUT_F32, TRANS, SM, SN, SK>;
+    auto fn = umma_gemm_kernel<B_MN, EPI, OUT_F32, TRANS, PAIR, SM, SN, SK>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
@@ -458,10 +478,11 @@ int umma_max_stages(int box_n, int b_mn_major) {
     return (kSmemLimit - 1024 - kTailBytes) / stage;
 }
 
-size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed) {
+size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed, int pair) {
     const size_t ring = (size_t)stages * (kABytes + b_stage_bytes(box_n, b_mn_major));
-    const size_t part = split > 1 ? (size_t)128 * box_n * 4 : 0;
-    const size_t stg = split > 1 ? (size_t)128 * box_n * 4 : (transposed ? (size_t)128 * box_n * out_bytes : 0);
+    const int n_stage = pair ? 2 * box_n : box_n;
+    const size_t part = split > 1 ? (size_t)128 * n_stage * 4 : 0;
+    const size_t stg = split > 1 ? (size_t)128 * n_stage * 4 : (transposed ? (size_t)128 * n_stage * out_bytes : 0);
     return 1024 /* alignment slack */ + (ring > part ? ring : part) + stg + kTailBytes;
 }
 
@@ -480,11 +501,11 @@ static void fill_cfg(const UmmaLaunch &L, cudaLaunchConfig_t &cfg, cudaLaunchAtt
     cfg.stream = L.stream;
     cfg.attrs = attr;
     cfg.numAttrs = 0;
-    if (L.p.split > 1) {
+    if (L.p.split > 1 || L.pair) {
         attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
-        attr[cfg.numAttrs].val.clusterDim.x = 1;
+        attr[cfg.numAttrs].val.clusterDim.x = L.pair ? 2 : 1;
         attr[cfg.numAttrs].val.clusterDim.y = 1;
-        attr[cfg.numAttrs].val.clusterDim.z = (unsigned)L.p.split;
+        attr[cfg.numAttrs].val.clusterDim.z = L.pair ? 1 : (unsigned)L.p.split;
         cfg.numAttrs++;
     }
     if (pdl_enabled()) {
@@ -500,7 +521,10 @@ cudaError_t launch_umma_gemm_static(const UmmaLaunch &L, int64_t M, int64_t N, i
     cudaLaunchAttribute attr[2];
     fill_cfg(L, cfg, attr);
 #define NIMBLE_X(m, n, k) \
-    if (M == m && N == n && K == k) return launch_t<0, 1, 0, 1, m, n, k>(L, cfg);
+    if (M == m && N == n && K == k) {                                                  \
+        if (L.pair) return launch_t<0, 1, 0, 1, 1, m, n, k>(L, cfg);                     \
+        return launch_t<0, 1, 0, 1, 0, m, n, k>(L, cfg);                                 \
+    }
     NIMBLE_STATIC_GEMM_SHAPES(NIMBLE_X)
 #undef NIMBLE_X
     return cudaErrorInvalidValue;
@@ -515,11 +539,11 @@ cudaError_t launch_umma_gemm(const UmmaLaunch &L) {
     cudaLaunchAttribute attr[2];
     cfg.attrs = attr;
     cfg.numAttrs = 0;
-    if (L.p.split > 1) {
+    if (L.p.split > 1 || L.pair) {
         attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
-        attr[cfg.numAttrs].val.clusterDim.x = 1;
+        attr[cfg.numAttrs].val.clusterDim.x = L.pair ? 2 : 1;
         attr[cfg.numAttrs].val.clusterDim.y = 1;
-        attr[cfg.numAttrs].val.clusterDim.z = (unsigned)L.p.split;
+        attr[cfg.numAttrs].val.clusterDim.z = L.pair ? 1 : (unsigned)L.p.split;
         cfg.numAttrs++;
     }
     if (pdl_enabled()) {
@@ -530,6 +554,15 @@ cudaError_t launch_umma_gemm(const UmmaLaunch &L) {
     if (L.b_mn_major) {   // bmm P.V: direct epilogue, alpha only
         if (L.out_f32) return launch_t<1, 0, 1, 0>(L, cfg);
         return launch_t<1, 0, 0, 0>(L, cfg);
+    }
+    if (L.pair) {                                            // 2-CTA large-M family
+        if (L.out_f32) return launch_t<0, 0, 1, 1, 1>(L, cfg);
+        switch (L.epi) {
+            case 0: return launch_t<0, 0, 0, 1, 1>(L, cfg);
+            case 1: return launch_t<0, 1, 0, 1, 1>(L, cfg);
+            case 2: return launch_t<0, 2, 0, 1, 1>(L, cfg);
+            default: return launch_t<0, 3, 0, 1, 1>(L, cfg);
+        }
     }
     if (L.out_f32) return launch_t<0, 0, 1, 1>(L, cfg);      // bmm Q.K^T scores
     switch (L.epi) {

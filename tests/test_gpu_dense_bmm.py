@@ -248,3 +248,26 @@ def test_static_twin_bitwise_equal(nb, orc):
                         torch.zeros((3072, 1024), dtype=torch.bfloat16, device="cuda"),
                         torch.zeros((3072,), device="cuda"),
                         torch.zeros((77, 3072), dtype=torch.bfloat16, device="cuda"))
+
+
+@pytest.mark.parametrize("M", [2048, 2049, 2300, 4111])
+def test_bf16_large_m_cta_pairs(nb, orc, M):
+    # family 3: 2-CTA pairs (tcgen05 cta_group::2), each CTA loads half of the token tile
+    N, K = 640, 256
+    W = synth.normal((N, K), 0.05, 91)
+    b = synth.normal((N,), 0.1, 92, torch.float32)
+    x = synth.normal((M, K), 1.0, 93 + M)
+    for epi in (nb.EPI_BIAS, nb.EPI_BIAS_GELU, nb.EPI_BIAS_RESIDUAL):
+        res = synth.normal((M, N), 1.0, 94 + M) if epi == nb.EPI_BIAS_RESIDUAL else None
+        y = _dense_gpu(nb, x, W, b, epi, res)
+        d = nb.last_dispatch()
+        assert d == orc.dispatch_dense(M, N, K, 1)[1] and d["cluster"] == (2, 1, 1)
+        ref, D = orc.dense(x.double().numpy(), W.double().numpy(), b.numpy(),
+                           None if res is None else res.double().numpy(), epi)
+        assert _err(y, ref, D) <= TOL_BF16, (M, epi)
+    xi = synth.ternary((M, K), 95 + M, torch.bfloat16, max_nonzero_per_row=200)
+    Wi = synth.ternary((N, K), 96, torch.bfloat16)
+    bi = synth.ternary((N,), 97, torch.float32)
+    y = _dense_gpu(nb, xi, Wi, bi, nb.EPI_BIAS)
+    ref, _ = orc.dense(xi.double().numpy(), Wi.double().numpy(), bi.numpy(), None, 1)
+    assert np.array_equal(y.double().cpu().numpy(), ref)

@@ -134,7 +134,8 @@ def test_dispatch_invariants(orc, dt):
                     assert d["umma_n_tail"] == t
             if dt == 1:
                 s = d["split_k"]
-                assert s in (1, 2, 4, 8) and d["cluster"] == (1, 1, s)
+                assert s in (1, 2, 4, 8) and d["cluster"] == ((1 if M < 2048 else 2), 1, s)
+                assert d["umma_m"] == (128 if M < 2048 else 256)
                 assert (1024 // 64) // s >= 4 or s == 1
                 assert d["family"] == (1 if M < 2048 else 3)
                 if M >= 2048:
