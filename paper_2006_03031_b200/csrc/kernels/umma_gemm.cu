@@ -3,7 +3,7 @@
 //
 // Tile = 128 (UMMA M) x n (UMMA N: the full tile width t, or the residue-specialised
 // tail width 16*ceil(r/16) the dispatch function picked) over K.
-// 384 threads, warp-specialised:
+// 512 threads, warp-specialised:
 //   warp 0 lane 0  TMA producer: A[128 x 64] + B[box_n x 64] bf16 tiles (128-B swizzle)
 //                  into a `stages`-deep smem ring (full/empty mbarriers).  Rows beyond
 //                  the symbolic extent are zero-filled by TMA bounds — the dynamic
@@ -13,8 +13,8 @@
 //   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (K = 16) per 64-wide k-block into one of
 //                  two fp32 TMEM accumulators (double-buffered across tiles).
 //   warp 2         TMEM allocation / deallocation.
-//   warps 4-11     epilogue: warp w reads TMEM lane quarter (w % 4), 16-column chunks
-//                  alternating between the two warp groups; compile-time epilogue
+//   warps 4-15     epilogue: warp w reads TMEM lane quarter (w % 4), 16-column chunks
+//                  round-robin over three warp groups; compile-time epilogue
 //                  (alpha | bias | bias+GELU | bias+residual, residual tile TMA-loaded into
 //                  the staging buffer); the transposed output tile is staged in smem and
 //                  written by ONE TMA store that clips rows beyond the symbolic extent.
@@ -34,9 +34,10 @@ namespace nimble {
 
 namespace {
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int kEpiWarp0 = 4;
-constexpr int kEpiThreads = 256;
+constexpr int kEpiThreads = 384;            // 12 epilogue warps = 3 column groups x 4 lane quarters
+constexpr int kEpiGroups = kEpiThreads / 128;
 constexpr int kBlockK = 64;                   // one 128-B swizzle row of bf16
 constexpr int kABytes = 128 * kBlockK * 2;    // 16 KiB A stage
 constexpr int kSmemLimit = 232448;            // 227 KiB opt-in per CTA
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::pdl_wait();                                     // residual / output dependencies
         const int ew = (int)warp - kEpiWarp0;
         const int quarter = (int)(warp & 3);
-        const int half = ew >> 2;
+        const int half = ew >> 2;                            // column group 0..kEpiGroups-1
         const int row_local = quarter * 32 + (int)lane;
         const bool leader = (ew == 0 && lane == 0);
         const int res_bytes = 128 * n_stage * 2;
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mbar_wait(res_bar, res_phase);
                         res_phase ^= 1;
                     }
-                    for (int c0 = half * 16; c0 < n_this; c0 += 32) {
+                    for (int c0 = half * 16; c0 < n_this; c0 += 16 * kEpiGroups) {
                         float v[16];
                         ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
 #pragma unroll
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::named_bar_sync(2, kEpiThreads);
                 } else {
                     // direct row-major store: thread owns row i, 16 consecutive columns per chunk
-                    for (int c0 = half * 16; c0 < n_this; c0 += 32) {
+                    for (int c0 = half * 16; c0 < n_this; c0 += 16 * kEpiGroups) {
                         float v[16];
                         ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
                         if (!row_ok || c0 >= n_valid) continue;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
                 // ---- split-K reduce-scatter over DSMEM: partial[col][128] fp32 in the ring region
                 float *part = reinterpret_cast<float *>(smem);
-                for (int c0 = half * 16; c0 < n_this; c0 += 32) {
+                for (int c0 = half * 16; c0 < n_this; c0 += 16 * kEpiGroups) {
                     float v[16];
                     ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
 #pragma unroll
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(recv_bar, 0);
                 if (leader) NIMBLE_TRACE(5);
                 const float *recv = reinterpret_cast<const float *>(stg);
-                for (int jl = half; jl < per; jl += 2) {
+                for (int jl = half; jl < per; jl += kEpiGroups) {
                     float a = 0.f;
                     for (int r = 0; r < p.split; ++r) {            // fixed rank order: deterministic
                         if ((p.dbg & 2) && r != (int)rank) continue;
