@@ -13,13 +13,16 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(HERE, "libnimble.so")
+# Experiment builds: NIMBLE_VARIANT=tag adds -D flags from NIMBLE_DEFINES and writes
+# libnimble_<tag>.so (loaded with NIMBLE_LIB=...); the default build is libnimble.so.
+_TAG = os.environ.get("NIMBLE_VARIANT", "")
+OBJ = os.path.join(ROOT, "build", "obj" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(HERE, f"libnimble_{_TAG}.so" if _TAG else "libnimble.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include")]
+         "-I", os.path.join(ROOT, "include")] + (os.environ.get("NIMBLE_DEFINES", "").split() if _TAG else [])
 
 
 def sources():

@@ -147,7 +147,8 @@ __device__ __forceinline__ float ld_shared_cluster_f32(uint32_t addr) {
 // 1.5e-7, far below the bf16 output rounding of 2^-9), one exp2 + one rcp + 5 FMAs.
 __device__ __forceinline__ float erf_as(float x) {
     const float ax = fabsf(x);
-    const float t = __frcp_rn(fmaf(0.3275911f, ax, 1.0f));
+    float t;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, ax, 1.0f)));
     float poly = fmaf(1.061405429f, t, -1.453152027f);
     poly = fmaf(poly, t, 1.421413741f);
     poly = fmaf(poly, t, -0.284496736f);
@@ -156,7 +157,11 @@ __device__ __forceinline__ float erf_as(float x) {
     const float e = exp2f(-ax * ax * 1.4426950408889634f);
     return copysignf(fmaf(-poly, e, 1.0f), x);
 }
+#ifdef NIMBLE_GELU_ERFF
+__device__ __forceinline__ float gelu_erf(float z) { return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f)); }
+#else
 __device__ __forceinline__ float gelu_erf(float z) { return 0.5f * z * (1.0f + erf_as(z * 0.70710678118654752f)); }
+#endif
 __device__ __forceinline__ float sigmoidf_(float z) { return 1.0f / (1.0f + expf(-z)); }
 
 }  // namespace ptx

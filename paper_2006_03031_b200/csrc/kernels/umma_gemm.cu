@@ -34,9 +34,12 @@ namespace nimble {
 
 namespace {
 
-constexpr int kThreads = 512;
+#ifndef NIMBLE_EPI_WARPS
+#define NIMBLE_EPI_WARPS 12
+#endif
+constexpr int kThreads = 128 + 32 * NIMBLE_EPI_WARPS;
 constexpr int kEpiWarp0 = 4;
-constexpr int kEpiThreads = 384;            // 12 epilogue warps = 3 column groups x 4 lane quarters
+constexpr int kEpiThreads = 32 * NIMBLE_EPI_WARPS;   // 12 epilogue warps = 3 column groups x 4 lane quarters
 constexpr int kEpiGroups = kEpiThreads / 128;
 constexpr int kBlockK = 64;                   // one 128-B swizzle row of bf16
 constexpr int kABytes = 128 * kBlockK * 2;    // 16 KiB A stage

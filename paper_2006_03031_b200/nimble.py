@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnimble.so")
+LIB_PATH = os.environ.get("NIMBLE_LIB") or os.path.join(HERE, "libnimble.so")
 
 ANY = -1
 F32, BF16 = 0, 1
