@@ -3,7 +3,7 @@
 //
 // Tile = 128 (UMMA M) x n (UMMA N: the full tile width t, or the residue-specialised
 // tail width 16*ceil(r/16) the dispatch function picked) over K.
-// 512 threads, warp-specialised:
+// 384 threads, warp-specialised:
 //   warp 0 lane 0  TMA producer: A[128 x 64] + B[box_n x 64] bf16 tiles (128-B swizzle)
 //                  into a `stages`-deep smem ring (full/empty mbarriers).  Rows beyond
 //                  the symbolic extent are zero-filled by TMA bounds — the dynamic
@@ -13,8 +13,8 @@
 //   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (K = 16) per 64-wide k-block into one of
 //                  two fp32 TMEM accumulators (double-buffered across tiles).
 //   warp 2         TMEM allocation / deallocation.
-//   warps 4-15     epilogue: warp w reads TMEM lane quarter (w % 4), 16-column chunks
-//                  round-robin over three warp groups; compile-time epilogue
+//   warps 4..      epilogue: warp w reads TMEM lane quarter (w % 4), 16-column chunks
+//                  round-robin over the column groups; compile-time epilogue
 //                  (alpha | bias | bias+GELU | bias+residual, residual tile TMA-loaded into
 //                  the staging buffer); the transposed output tile is staged in smem and
 //                  written by ONE TMA store that clips rows beyond the symbolic extent.
@@ -35,11 +35,11 @@ namespace nimble {
 namespace {
 
 #ifndef NIMBLE_EPI_WARPS
-#define NIMBLE_EPI_WARPS 12
+#define NIMBLE_EPI_WARPS 8
 #endif
 constexpr int kThreads = 128 + 32 * NIMBLE_EPI_WARPS;
 constexpr int kEpiWarp0 = 4;
-constexpr int kEpiThreads = 32 * NIMBLE_EPI_WARPS;   // 12 epilogue warps = 3 column groups x 4 lane quarters
+constexpr int kEpiThreads = 32 * NIMBLE_EPI_WARPS;   // epilogue warps: column groups x 4 lane quarters
 constexpr int kEpiGroups = kEpiThreads / 128;
 constexpr int kBlockK = 64;                   // one 128-B swizzle row of bf16
 constexpr int kABytes = 128 * kBlockK * 2;    // 16 KiB A stage
