@@ -115,30 +115,48 @@ __global__ void __launch_bounds__(kThreads)
     float *red = reinterpret_cast<float *>(tmem_slot + 4);      // [2][128] partial max, then sum
     ptx::mbar_wait(bar_s, 0);
     ptx::tc_fence_after();
+    // pass 1: row max.  Interior chunks (all 16 keys < L) take an unmasked path.
     float mx = -INFINITY;
     for (int c0 = half * 16; c0 < nk * 128; c0 += 32) {
         float v[16];
         ptx::tmem_ld16(trow + (uint32_t)c0, v);
+        if (c0 + 16 <= L) {
+            float m0 = fmaxf(v[0], v[1]), m1 = fmaxf(v[2], v[3]), m2 = fmaxf(v[4], v[5]), m3 = fmaxf(v[6], v[7]);
+            m0 = fmaxf(m0, fmaxf(v[8], v[9])); m1 = fmaxf(m1, fmaxf(v[10], v[11]));
+            m2 = fmaxf(m2, fmaxf(v[12], v[13])); m3 = fmaxf(m3, fmaxf(v[14], v[15]));
+            mx = fmaxf(mx, fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)));
+        } else {
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-            if (c0 + e < L) mx = fmaxf(mx, v[e]);
+            for (int e = 0; e < 16; ++e)
+                if (c0 + e < L) mx = fmaxf(mx, v[e]);
+        }
     }
     red[half * 128 + q] = mx;
     __syncthreads();
     mx = fmaxf(red[q], red[128 + q]);
     const float mx_s = mx * p.scale_log2;
-    float sum = 0.f;
+    // pass 2: p = 2^(s*scale*log2e - max*scale*log2e) (one FFMA + one MUFU.EX2 per key),
+    // four independent partial sums, bf16 pairs packed straight into the swizzled P layout.
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
     for (int c0 = half * 16; c0 < nkb * 64; c0 += 32) {
         float v[16];
         ptx::tmem_ld16(trow + (uint32_t)c0, v);
+        if (c0 + 16 <= L) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = ptx::ex2_approx(fmaf(v[e], p.scale_log2, -mx_s));
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = (c0 + e < L) ? ptx::ex2_approx(fmaf(v[e], p.scale_log2, -mx_s)) : 0.f;
+        }
         uint32_t w[8];
 #pragma unroll
-        for (int e = 0; e < 16; e += 2) {
-            const float a = (c0 + e < L) ? exp2f(fmaf(v[e], p.scale_log2, -mx_s)) : 0.f;
-            const float b = (c0 + e + 1 < L) ? exp2f(fmaf(v[e + 1], p.scale_log2, -mx_s)) : 0.f;
-            sum += a + b;
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-            w[e / 2] = *reinterpret_cast<uint32_t *>(&h2);
+        for (int e = 0; e < 16; e += 4) {
+            s0 += v[e]; s1 += v[e + 1]; s2 += v[e + 2]; s3 += v[e + 3];
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+            w[e] = *reinterpret_cast<uint32_t *>(&h2);
         }
         // UMMA K-major SW128 layout: block kb = 64 keys, row q at 128 B, 16-B chunk c ^ (q & 7)
         const int kb = c0 >> 6, c = (c0 & 63) >> 3;
@@ -146,6 +164,7 @@ __global__ void __launch_bounds__(kThreads)
         *reinterpret_cast<uint4 *>(rowp + (((c) ^ (q & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         *reinterpret_cast<uint4 *>(rowp + (((c + 1) ^ (q & 7)) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
     }
+    const float sum = (s0 + s1) + (s2 + s3);
     __syncthreads();                              // everyone has read red[] (max) before reuse
     red[half * 128 + q] = sum;
     ptx::fence_async_smem();                      // P (generic stores) -> tensor-core reads

@@ -286,3 +286,13 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 }
 }  // namespace ptx
 }  // namespace nimble
+
+namespace nimble {
+namespace ptx {
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+}  // namespace ptx
+}  // namespace nimble
