@@ -6,15 +6,15 @@
 // bmm_dyn -> softmax_rows -> bmm_dyn triple and never writes S or P to HBM.
 //
 // CTA = (query tile of 128, head, request), 288 threads, online softmax over 128-key blocks:
-//   warp 8 lane 0  TMA producer: Q tile, then K_j [128 x 64] and V_j (MN-major, two 64-key
-//                  boxes) of every key block into a 2-stage ring.
+//   warp 8 lane 0  TMA producer: Q tile, then per key block K_j [128 x 64] (single buffer) and
+//                  V_j (MN-major, two 64-key boxes, 2-stage ring).
 //   warp 8 lane 1  MMA issuer: S = Q K_j^T into TMEM cols [0,128) as soon as the previous S
 //                  has been read; O += P_j V_j into TMEM cols [128,192) once P_j is written.
 //   warps 0-7      softmax: row q = TMEM lane 32*(w%4)+lane, key half (w/4) of the block held
 //                  in registers; running max / sum; unnormalised P_j written as bf16 straight
 //                  into the UMMA K-major swizzled smem layout; O rescaled in TMEM when the
 //                  running max grows; epilogue O / rowsum -> bf16.
-// TMEM 256 columns and ~113 KB smem per CTA: two CTAs share an SM.  Keys >= L_i get P = 0;
+// TMEM 256 columns and ~99 KB smem per CTA: two CTAs share an SM.  Keys >= L_i get P = 0;
 // query rows >= L_i are computed but never stored.
 #include <cstdint>
 
@@ -29,7 +29,7 @@ constexpr int kSoftmaxThreads = 256;     // warps 0-7
 constexpr int kThreads = kSoftmaxThreads + 32;   // + warp 8: lane 0 TMA producer, lane 1 MMA issuer
 constexpr int kTile = 128 * 64 * 2;       // Q tile / K block / V block (128 keys) / P half: 16 KiB
 constexpr int kVBox = 64 * 64 * 2;        // one V TMA box (64 keys): 8 KiB
-constexpr int kSmemBytes = 1024 + 7 * kTile + 2048 + 256;
+constexpr int kSmemBytes = 1024 + 6 * kTile + 2048 + 256;   // ~99 KB: two CTAs per SM
 
 struct AttnParams {
     const int32_t *seq_off;   // [R + 1] prefix sums of request lengths (device)
@@ -66,24 +66,26 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (q0 >= L) return;                          // request shorter than this query tile
     const int nk = (L + 127) / 128;               // key blocks
     uint8_t *sQ = smem;
-    uint8_t *sK = smem + kTile;                   // [2] K blocks
-    uint8_t *sV = smem + 3 * kTile;               // [2] V blocks (two 64-key boxes each)
-    uint8_t *sP = smem + 5 * kTile;               // P block: 2 x (64 keys) K-major atoms = 32 KiB
-    float *red = reinterpret_cast<float *>(smem + 7 * kTile);          // [2][128] row max
+    uint8_t *sK = smem + kTile;                   // K block (single buffer: only the short S MMA reads it)
+    uint8_t *sV = smem + 2 * kTile;               // [2] V blocks (two 64-key boxes each)
+    uint8_t *sP = smem + 4 * kTile;               // P block: 2 x (64 keys) K-major atoms = 32 KiB
+    float *red = reinterpret_cast<float *>(smem + 6 * kTile);          // [2][128] row max
     float *redl = red + 256;                                            // [2][128] row sums
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 7 * kTile + 2048);
-    uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *s_full = bar + 5, *s_used = bar + 6,
-             *p_ready = bar + 7, *pv_done = bar + 8;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 9);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 6 * kTile + 2048);
+    uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 2, *v_full = bar + 3, *v_empty = bar + 5,
+             *s_full = bar + 7, *s_used = bar + 8, *p_ready = bar + 9, *pv_done = bar + 10;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 11);
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
 
     if (threadIdx.x == 0) {
         ptx::prefetch_tmap(&tmQK);
         ptx::prefetch_tmap(&tmV);
         ptx::mbar_init(q_full, 1);
+        ptx::mbar_init(k_full, 1);
+        ptx::mbar_init(k_empty, 1);
         for (int i = 0; i < 2; ++i) {
-            ptx::mbar_init(&kv_full[i], 1);
-            ptx::mbar_init(&kv_empty[i], 1);
+            ptx::mbar_init(&v_full[i], 1);
+            ptx::mbar_init(&v_empty[i], 1);
         }
         ptx::mbar_init(s_full, 1);
         ptx::mbar_init(s_used, kSoftmaxThreads / 32);
@@ -105,26 +107,28 @@ __global__ void __launch_bounds__(kThreads, 2)
         ptx::tma_load_3d(sQ, &tmQK, q_full, 0, h, o + q0);
         for (int j = 0; j < nk; ++j) {
             const int st = j & 1, use = j >> 1;
-            if (use > 0) ptx::mbar_wait(&kv_empty[st], (use - 1) & 1);
-            ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * kTile);
-            ptx::tma_load_3d(sK + st * kTile, &tmQK, &kv_full[st], 0, p.heads + h, o + j * 128);
-            ptx::tma_load_3d(sV + st * kTile, &tmV, &kv_full[st], 0, 2 * p.heads + h, o + j * 128);
-            ptx::tma_load_3d(sV + st * kTile + kVBox, &tmV, &kv_full[st], 0, 2 * p.heads + h, o + j * 128 + 64);
+            if (j > 0) ptx::mbar_wait(k_empty, (j - 1) & 1);          // S_{j-1} has read K
+            ptx::mbar_arrive_expect_tx(k_full, kTile);
+            ptx::tma_load_3d(sK, &tmQK, k_full, 0, p.heads + h, o + j * 128);
+            if (use > 0) ptx::mbar_wait(&v_empty[st], (use - 1) & 1); // PV_{j-2} has read V
+            ptx::mbar_arrive_expect_tx(&v_full[st], kTile);
+            ptx::tma_load_3d(sV + st * kTile, &tmV, &v_full[st], 0, 2 * p.heads + h, o + j * 128);
+            ptx::tma_load_3d(sV + st * kTile + kVBox, &tmV, &v_full[st], 0, 2 * p.heads + h, o + j * 128 + 64);
         }
       } else if (lane == 1) {
         // ---------------- MMA issuer
         const uint32_t idesc_s = ptx::idesc_bf16(128, 128, 0);
         const uint32_t idesc_o = ptx::idesc_bf16(128, 64, 1);
         const uint64_t qd = ptx::smem_desc_sw128(ptx::smem_u32(sQ), 0, 1024);
+        const uint64_t kd = ptx::smem_desc_sw128(ptx::smem_u32(sK), 0, 1024);
         auto issue_s = [&](int j) {
-            const int st = j & 1;
-            ptx::mbar_wait(&kv_full[st], (j >> 1) & 1);
+            ptx::mbar_wait(k_full, j & 1);
             ptx::tc_fence_after();
-            const uint64_t kd = ptx::smem_desc_sw128(ptx::smem_u32(sK + st * kTile), 0, 1024);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
                 ptx::umma_bf16(tmem, qd + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idesc_s, kk > 0 ? 1u : 0u);
             ptx::umma_commit(s_full);
+            ptx::umma_commit(k_empty);
         };
         ptx::mbar_wait(q_full, 0);
         issue_s(0);
@@ -134,8 +138,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                 issue_s(j + 1);
             }
             ptx::mbar_wait(p_ready, j & 1);       // P_j written, O rescaled
-            ptx::tc_fence_after();
             const int st = j & 1;
+            ptx::mbar_wait(&v_full[st], (j >> 1) & 1);
+            ptx::tc_fence_after();
 #pragma unroll
             for (int kb = 0; kb < 2; ++kb) {
                 const uint64_t pd = ptx::smem_desc_sw128(ptx::smem_u32(sP + kb * kTile), 0, 1024);
@@ -146,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                                    (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
             }
             ptx::umma_commit(pv_done);
-            ptx::umma_commit(&kv_empty[st]);
+            ptx::umma_commit(&v_empty[st]);
         }
       }
       __syncwarp();
