@@ -314,11 +314,18 @@ def main():
             ach, pk, unit = fl / tm / 1e12, peaks["tc_sus"], "TFLOP/s"
         else:
             ach, pk, unit = by / tm / 1e9, peaks["hbm"], "GB/s"
-        roof = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit, "frac": ach / pk, "traffic": None,
+        traffic = None
+        try:        # DRAM bytes per launch from the committed ncu --set full capture of this config
+            with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+                traffic = json.load(f)["traffic_bytes_per_launch"]
+        except Exception:
+            pass
+        roof = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit, "frac": ach / pk, "traffic": traffic,
                 "kernel": "nimble::umma_gemm_kernel (dense_dyn bf16: QKV, O, FFN1, FFN2 at M = packed tokens)",
                 "launches": n, "avg_launch_us": 1e6 * tm / max(n, 1),
                 "algorithmic_flops_per_launch": fl / max(n, 1), "algorithmic_bytes_per_launch": by / max(n, 1),
                 "frac_of_burst_peak": fl / tm / 1e12 / peaks["tc"],
+                "traffic_source": "profiles/gemm_traffic.json (ncu --set full, dram__bytes_read+write per launch)",
                 "peak_note": f"{peaks['src']}: sustained bf16 {peaks['tc_sus']} TFLOP/s (burst {peaks['tc']}), "
                              f"HBM {peaks['hbm']} GB/s"}
 

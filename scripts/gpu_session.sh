@@ -23,7 +23,9 @@ if [[ $STEPS == *ncu* ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
       python bench.py --profile --steps 1 --warmup 1 > $OUT/ncu_launch.log 2>&1; echo "ncu-launch rc=$?" >> $OUT/ncu_launch.log
   tail -3 $OUT/ncu_launch.log
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:umma_gemm -s 100 -c 4 -o $OUT/prof_gemm -f \
-      python bench.py --profile --steps 1 --warmup 1 --requests-per-gpu 16 > $OUT/ncu_full.log 2>&1; echo "ncu-full rc=$?" >> $OUT/ncu_full.log
+  # the bench configuration itself (64 requests, M = 17.4k tokens): one layer's four GEMM launches
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:umma_gemm -s 96 -c 4 -o $OUT/prof_gemm -f \
+      python bench.py --profile --steps 1 --warmup 1 > $OUT/ncu_full.log 2>&1; echo "ncu-full rc=$?" >> $OUT/ncu_full.log
+  python scripts/gemm_traffic.py $OUT/prof_gemm.ncu-rep > $OUT/gemm_traffic.json
   tail -3 $OUT/ncu_full.log
 fi
