@@ -143,12 +143,19 @@ __device__ __forceinline__ float ld_shared_cluster_f32(uint32_t addr) {
 }
 
 // ----------------------------------------------------------------- math
-// GELU(z) = z/2 (1 + erf(z / sqrt 2)).  erf by Abramowitz & Stegun 7.1.26 (max abs error
-// 1.5e-7, far below the bf16 output rounding of 2^-9), one exp2 + one rcp + 5 FMAs.
-__device__ __forceinline__ float erf_as(float x) {
+// GELU(z) = z/2 (1 + erf(z / sqrt 2)).
+// erf_as26: Abramowitz & Stegun 7.1.26 (max abs error 1.5e-7): one exp2 + one rcp (2 MUFU).
+// erf_as28: Abramowitz & Stegun 7.1.28, erf(x) = 1 - (1 + a1 x + ... + a6 x^6)^-16 (max abs
+//           error 2.6e-7 in exact arithmetic, ~2e-6 in fp32): one rcp + FMAs (1 MUFU op).
+// Both are far below the bf16 output rounding (2^-9 relative) of the fused epilogue.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float erf_as26(float x) {
     const float ax = fabsf(x);
-    float t;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, ax, 1.0f)));
+    const float t = rcp_approx(fmaf(0.3275911f, ax, 1.0f));
     float poly = fmaf(1.061405429f, t, -1.453152027f);
     poly = fmaf(poly, t, 1.421413741f);
     poly = fmaf(poly, t, -0.284496736f);
@@ -157,6 +164,23 @@ __device__ __forceinline__ float erf_as(float x) {
     const float e = exp2f(-ax * ax * 1.4426950408889634f);
     return copysignf(fmaf(-poly, e, 1.0f), x);
 }
+__device__ __forceinline__ float erf_as28(float x) {
+    const float ax = fminf(fabsf(x), 8.0f);
+    float p = fmaf(4.30638e-5f, ax, 2.765672e-4f);
+    p = fmaf(p, ax, 1.520143e-4f);
+    p = fmaf(p, ax, 9.2705272e-3f);
+    p = fmaf(p, ax, 4.22820123e-2f);
+    p = fmaf(p, ax, 7.05230784e-2f);
+    p = fmaf(p, ax, 1.0f);
+    float r = rcp_approx(p);
+    r *= r; r *= r; r *= r; r *= r;                  // p^-16
+    return copysignf(1.0f - r, x);
+}
+#ifdef NIMBLE_ERF_AS26
+__device__ __forceinline__ float erf_as(float x) { return erf_as26(x); }
+#else
+__device__ __forceinline__ float erf_as(float x) { return erf_as28(x); }
+#endif
 #ifdef NIMBLE_GELU_ERFF
 __device__ __forceinline__ float gelu_erf(float z) { return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f)); }
 #else
