@@ -189,6 +189,18 @@ int nimble_lstm_seq(const float *G, int64_t ldg, const float *W_hh, int64_t ldw,
                     const float *c0, float *H_seq, int64_t ldh, float *hT, float *cT, int64_t T,
                     int64_t H, void *workspace, void *stream);
 
+/* Two stacked layers as ONE persistent wavefront kernel (layer 2 runs one step behind
+ * layer 1; one grid barrier per step serves both, T + 1 barriers in all).  G1 [T x ldg] =
+ * X W_ih1^T + (b_ih1 + b_hh1) (hoisted, nimble_dense_dyn); W_hh1, W_ih2, W_hh2 [4H x ldw]
+ * (PyTorch row blocks i, f, g, o; layer 2's input is h1, so W_ih2 is [4H x H]); b2 [4H] =
+ * b_ih2 + b_hh2; zero initial states.  Writes H1 [T x ldh], H2 [T x ldh] and hT, cT
+ * [2 x H] (layer 0 then layer 1).  workspace: nimble_lstm2_workspace_bytes(H) bytes.
+ * H <= 1024 (E_UNSUPPORTED beyond: the weights must fit in shared memory). */
+size_t nimble_lstm2_workspace_bytes(int64_t H);
+int nimble_lstm2_seq(const float *G1, int64_t ldg, const float *W_hh1, const float *W_ih2, const float *W_hh2,
+                     int64_t ldw, const float *b2, float *H1, float *H2, int64_t ldh, float *hT, float *cT,
+                     int64_t T, int64_t H, void *workspace, void *stream);
+
 /* ---------------------------------------------------------------------------
  * One Tree-LSTM level (binary N-ary cell; reading 13):
  * a level-batched dense_dyn over the M nodes of one height plus the cell epilogue.

@@ -416,6 +416,23 @@ extern "C" int nimble_lstm_seq(const float *G, int64_t ldg, const float *W_hh, i
     return NIMBLE_OK;
 }
 
+extern "C" size_t nimble_lstm2_workspace_bytes(int64_t H) { return H >= 1 ? lstm2_workspace_bytes(H) : 0; }
+
+extern "C" int nimble_lstm2_seq(const float *G1, int64_t ldg, const float *W_hh1, const float *W_ih2,
+                                const float *W_hh2, int64_t ldw, const float *b2, float *H1, float *H2, int64_t ldh,
+                                float *hT, float *cT, int64_t T, int64_t H, void *workspace, void *stream) {
+    if (!G1 || !W_hh1 || !W_ih2 || !W_hh2 || !b2 || !H1 || !H2 || !hT || !cT || !workspace)
+        return fail(NIMBLE_E_NULL, "nimble_lstm2_seq: NULL pointer");
+    if (!ext_ok(T) || !ext_ok(H)) return fail(NIMBLE_E_EXTENT, "nimble_lstm2_seq: T and H must be >= 1");
+    if (ldg < 4 * H || ldw < H || ldh < H) return fail(NIMBLE_E_SHAPE, "nimble_lstm2_seq: leading dimension too small");
+    if (H > 1024) return fail(NIMBLE_E_UNSUPPORTED, "nimble_lstm2_seq: H > 1024 not built");
+    cudaError_t e = launch_lstm2_seq(G1, ldg, W_hh1, W_ih2, W_hh2, ldw, b2, H1, H2, ldh, hT, cT, T, H, workspace,
+                                     static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("nimble_lstm2_seq launch", e);
+    clear_error();
+    return NIMBLE_OK;
+}
+
 // ------------------------------------------------------------------ Tree-LSTM
 extern "C" int nimble_treelstm_level(const int32_t *nodes, const float *A, int64_t lda, const int32_t *a_rows,
                                      const float *W, int64_t ldw, const float *bias, const int32_t *parent_slot,

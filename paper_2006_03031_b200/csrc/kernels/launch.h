@@ -102,6 +102,11 @@ cudaError_t launch_lstm_seq(const float *G, int64_t ldg, const float *W_hh, int6
                             const float *c0, float *H_seq, int64_t ldh, float *hT, float *cT, int64_t T,
                             int64_t H, void *workspace, cudaStream_t s);
 
+size_t lstm2_workspace_bytes(int64_t H);
+cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, const float *Wih2, const float *Whh2,
+                             int64_t ldw, const float *b2, float *H1, float *H2, int64_t ldh, float *hT, float *cT,
+                             int64_t T, int64_t H, void *workspace, cudaStream_t s);
+
 struct TreeParams {
     const int32_t *nodes;
     const float *A; int64_t lda;

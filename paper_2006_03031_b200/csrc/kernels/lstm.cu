@@ -95,8 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_seq_kernel(const LstmArgs a)
             // grid barrier: release our h slice, wait for every CTA's
             __syncthreads();
             if (threadIdx.x == 0) {
-                __threadfence();
-                atomicAdd(a.counter, 1u);
+                asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.counter), "r"(1u) : "memory");
                 const unsigned target = (unsigned)(t + 1) * nct;
                 uint32_t spins = 0;
                 while (ld_acquire(a.counter) < target) {

@@ -1,0 +1,181 @@
+// Two stacked LSTM layers over a runtime-length sequence as ONE persistent wavefront kernel
+// (Nimble's LSTM LM; config 2 "2 layers, hidden 650", BJ:8).
+//
+// At global step s = 0..T, layer-1 CTAs compute h1_s (from the hoisted projection
+// G1[s] = x_s W_ih1^T + b1 and W_hh1 h1_{s-1}) while layer-2 CTAs compute h2_{s-1} (from
+// W_ih2 h1_{s-1} + W_hh2 h2_{s-2} + b2): both only need h1_{s-1}, so one grid barrier per
+// step serves both layers -> T + 1 barriers instead of 2T.  Every CTA keeps its gate rows
+// of the weights resident in shared memory for the whole sequence; layer-2 CTAs own twice
+// the rows (W_ih2 and W_hh2).  Barrier: red.release.gpu arrive + ld.acquire.gpu poll.
+#include "launch.h"
+#include "ptx.cuh"
+
+namespace nimble {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+struct Lstm2Args {
+    const float *G1; int64_t ldg;
+    const float *Whh1, *Wih2, *Whh2; int64_t ldw;
+    const float *b2;
+    float *H1, *H2; int64_t ldh;
+    float *hT, *cT;              // [2][H]
+    float *hbuf;                 // [2 layers][2 ping-pong][H]
+    unsigned *counter;
+    int T, H, n1, JB1, JB2;      // n1 layer-1 CTAs (JB1 units each), the rest layer 2 (JB2 units)
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release(unsigned *p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// dot(w, x) over n elements, one warp, result in all lanes
+__device__ __forceinline__ float warp_dot(const float *w, const float *x, int n, int lane) {
+    float a0 = 0.f, a1 = 0.f;
+    int k = lane;
+    for (; k + 32 < n; k += 64) {
+        a0 = fmaf(w[k], x[k], a0);
+        a1 = fmaf(w[k + 32], x[k + 32], a1);
+    }
+    if (k < n) a0 = fmaf(w[k], x[k], a0);
+    float a = a0 + a1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    return a;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
+    extern __shared__ float sm[];
+    const int H = a.H;
+    const bool l2 = (int)blockIdx.x >= a.n1;
+    const int cta = l2 ? (int)blockIdx.x - a.n1 : (int)blockIdx.x;
+    const int JB = l2 ? a.JB2 : a.JB1;
+    const int j0 = cta * JB;
+    const int R = 4 * JB;                       // gate rows per matrix
+    const int nmat = l2 ? 2 : 1;
+    float *W = sm;                              // [nmat][R][H]
+    float *x1 = W + (size_t)nmat * R * H;       // h1_{s-1}
+    float *x2 = x1 + H;                         // h2_{s-2} (layer 2 only)
+    float *z = x2 + H;                          // [R]
+    float *cs = z + R;                          // [JB]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    for (int m = 0; m < nmat; ++m) {
+        const float *src = l2 ? (m == 0 ? a.Wih2 : a.Whh2) : a.Whh1;
+        for (int e = threadIdx.x; e < R * H; e += kThreads) {
+            const int r = e / H, k = e % H, g = r / JB, u = r % JB, j = j0 + u;
+            W[(size_t)m * R * H + e] = (j < H) ? src[(int64_t)(g * H + j) * a.ldw + k] : 0.f;
+        }
+    }
+    for (int u = threadIdx.x; u < JB; u += kThreads) cs[u] = 0.f;
+    for (int k = threadIdx.x; k < H; k += kThreads) { x1[k] = 0.f; x2[k] = 0.f; }
+    __syncthreads();
+    const unsigned nct = gridDim.x;
+
+    for (int s = 0; s <= a.T; ++s) {
+        const int t = l2 ? s - 1 : s;           // the time step this CTA computes
+        const bool active = t >= 0 && t < a.T;
+        if (s > 0) {
+            // h1_{s-1} (both layers), h2_{s-2} (layer 2)
+            const float *h1 = a.hbuf + (size_t)((s - 1) & 1) * H;
+            for (int k = threadIdx.x; k < H; k += kThreads) x1[k] = __ldcg(h1 + k);
+            if (l2 && s >= 2) {
+                const float *h2 = a.hbuf + (size_t)(2 + ((s - 2) & 1)) * H;
+                for (int k = threadIdx.x; k < H; k += kThreads) x2[k] = __ldcg(h2 + k);
+            }
+            __syncthreads();
+        }
+        if (active) {
+            for (int r = warp; r < R; r += kWarps) {
+                float acc;
+                if (l2) acc = warp_dot(W + (size_t)r * H, x1, H, lane) + warp_dot(W + (size_t)(R + r) * H, x2, H, lane);
+                else acc = warp_dot(W + (size_t)r * H, x1, H, lane);
+                if (lane == 0) z[r] = acc;
+            }
+            __syncthreads();
+            if (threadIdx.x < JB) {
+                const int u = threadIdx.x, j = j0 + u;
+                if (j < H) {
+                    float zi, zf, zg, zo;
+                    if (l2) {
+                        zi = z[u] + a.b2[j]; zf = z[JB + u] + a.b2[H + j];
+                        zg = z[2 * JB + u] + a.b2[2 * H + j]; zo = z[3 * JB + u] + a.b2[3 * H + j];
+                    } else {
+                        const float *g = a.G1 + (int64_t)t * a.ldg;
+                        zi = z[u] + g[j]; zf = z[JB + u] + g[H + j]; zg = z[2 * JB + u] + g[2 * H + j];
+                        zo = z[3 * JB + u] + g[3 * H + j];
+                    }
+                    const float c = ptx::sigmoidf_(zf) * cs[u] + ptx::sigmoidf_(zi) * tanhf(zg);
+                    const float h = ptx::sigmoidf_(zo) * tanhf(c);
+                    cs[u] = c;
+                    a.hbuf[(size_t)((l2 ? 2 : 0) + (t & 1)) * H + j] = h;
+                    (l2 ? a.H2 : a.H1)[(int64_t)t * a.ldh + j] = h;
+                    if (t == a.T - 1) {
+                        a.hT[(l2 ? H : 0) + j] = h;
+                        a.cT[(l2 ? H : 0) + j] = c;
+                    }
+                }
+            }
+        }
+        if (s < a.T) {
+            // grid barrier: publish this step's h, wait for every CTA's
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                red_release(a.counter, 1u);
+                const unsigned target = (unsigned)(s + 1) * nct;
+                uint32_t spins = 0;
+                while (ld_acquire(a.counter) < target) {
+                    if (++spins == (1u << 28)) __trap();
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+}  // namespace
+
+size_t lstm2_workspace_bytes(int64_t H) { return sizeof(float) * 4 * (size_t)H + 256; }
+
+cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, const float *Wih2, const float *Whh2,
+                             int64_t ldw, const float *b2, float *H1, float *H2, int64_t ldh, float *hT, float *cT,
+                             int64_t T, int64_t H, void *workspace, cudaStream_t s) {
+    // 3 : 1 split of the SMs (layer-2 CTAs own two matrices), <= 148 co-resident CTAs
+    int n1 = 48;
+    const int JB1 = (int)((H + n1 - 1) / n1);
+    n1 = (int)((H + JB1 - 1) / JB1);
+    int n2 = 2 * n1;
+    const int JB2 = (int)((H + n2 - 1) / n2);
+    n2 = (int)((H + JB2 - 1) / JB2);
+    const size_t smem1 = sizeof(float) * ((size_t)4 * JB1 * H + 2 * H + 4 * JB1 + JB1);
+    const size_t smem2 = sizeof(float) * ((size_t)8 * JB2 * H + 2 * H + 4 * JB2 + JB2);
+    const size_t smem = smem1 > smem2 ? smem1 : smem2;
+    if (smem > 232448 || n1 + n2 > 148) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(lstm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    Lstm2Args a;
+    a.G1 = G1; a.ldg = ldg; a.Whh1 = Whh1; a.Wih2 = Wih2; a.Whh2 = Whh2; a.ldw = ldw; a.b2 = b2;
+    a.H1 = H1; a.H2 = H2; a.ldh = ldh; a.hT = hT; a.cT = cT;
+    a.hbuf = static_cast<float *>(workspace);
+    a.counter = reinterpret_cast<unsigned *>(static_cast<char *>(workspace) + sizeof(float) * 4 * (size_t)H);
+    a.T = (int)T; a.H = (int)H; a.n1 = n1; a.JB1 = JB1; a.JB2 = JB2;
+    cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    void *args[] = {&a};
+    return cudaLaunchCooperativeKernel((const void *)lstm2_kernel, dim3((unsigned)(n1 + n2)), dim3(kThreads), args,
+                                       smem, s);
+}
+
+}  // namespace nimble

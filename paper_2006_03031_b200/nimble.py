@@ -73,6 +73,7 @@ _SIGS = {
                               _i64, C.c_int, _vp],
     "nimble_partition_lpt": [_i64p, _i64, C.c_int32, _i32p],
     "nimble_debug_trace": [_vp],
+    "nimble_lstm2_seq": [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp],
     "nimble_attention_varlen": [_vp, _i64, _i64, _vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, _vp,
                                 _i64, _vp],
 }
@@ -85,11 +86,13 @@ _lib.nimble_last_error.argtypes = []
 _lib.nimble_version.restype = C.c_char_p
 _lib.nimble_lstm_workspace_bytes.restype = C.c_size_t
 _lib.nimble_lstm_workspace_bytes.argtypes = [_i64]
+_lib.nimble_lstm2_workspace_bytes.restype = C.c_size_t
+_lib.nimble_lstm2_workspace_bytes.argtypes = [_i64]
 _lib.nimble_request_cost.restype = C.c_int64
 _lib.nimble_request_cost.argtypes = [_i64]
 
 EXPORTED = sorted(list(_SIGS) + ["nimble_last_error", "nimble_version", "nimble_lstm_workspace_bytes",
-                                 "nimble_request_cost"])
+                                 "nimble_lstm2_workspace_bytes", "nimble_request_cost"])
 
 
 def _check(st: int):
@@ -260,6 +263,18 @@ def lstm_seq(G, W_hh, H_seq, hT, cT, workspace, T=None, h0=None, c0=None, stream
     H = W_hh.shape[1]
     _check(_lib.nimble_lstm_seq(_ptr(G), G.stride(0), _ptr(W_hh), W_hh.stride(0), _ptr(h0), _ptr(c0), _ptr(H_seq),
                                 H_seq.stride(0), _ptr(hT), _ptr(cT), T, H, _ptr(workspace), _stream(stream)))
+
+
+def lstm2_workspace_bytes(H: int) -> int:
+    return int(_lib.nimble_lstm2_workspace_bytes(int(H)))
+
+
+def lstm2_seq(G1, W_hh1, W_ih2, W_hh2, b2, H1, H2, hT, cT, workspace, T=None, stream=None):
+    T = G1.shape[0] if T is None else T
+    H = W_hh1.shape[1]
+    _check(_lib.nimble_lstm2_seq(_ptr(G1), G1.stride(0), _ptr(W_hh1), _ptr(W_ih2), _ptr(W_hh2), W_hh1.stride(0),
+                                 _ptr(b2), _ptr(H1), _ptr(H2), H1.stride(0), _ptr(hT), _ptr(cT), T, H,
+                                 _ptr(workspace), _stream(stream)))
 
 
 def treelstm_level(nodes, A, a_rows, W, bias, parent_slot, hcat, ccat, h_out, c_out, M, K, H, is_leaf,

@@ -72,6 +72,23 @@ def test_lstm_two_layers_650(nb, orc, T):
         assert _abs_err(st.cT[l], states[l][1]) <= 1e-4
 
 
+def test_lstm_wavefront_equals_layerwise(nb, orc):
+    from paper_2006_03031_b200.rnn import LSTMStack
+    I = H = 650
+    T = 50
+    layers = synth.lstm_weights(I, H, 2, seed=7)
+    x = synth.lstm_input(T, I, seed=8)
+    st = LSTMStack(layers, max_T=T)
+    xp = torch.zeros((T, st.Ip), dtype=torch.float32, device="cuda")
+    xp[:, :I] = x.cuda()
+    a = st.forward(xp, T, wavefront=True).clone()
+    b = st.forward(xp, T, wavefront=False).clone()
+    torch.cuda.synchronize()
+    ref, _, _ = orc.lstm(x.numpy(), [(w1.numpy(), w2.numpy(), bb.numpy()) for w1, w2, bb in layers])
+    assert _abs_err(a, ref) <= 1e-4 and _abs_err(b, ref) <= 1e-4
+    assert float((a - b).abs().max()) <= 1e-5
+
+
 def test_lstm_paper_sizes_300_512(nb, orc):
     from paper_2006_03031_b200.rnn import LSTMStack
     I, H, T = 300, 512, 20
