@@ -3,10 +3,13 @@
 //
 // At global step s = 0..T, layer-1 CTAs compute h1_s (from the hoisted projection
 // G1[s] = x_s W_ih1^T + b1 and W_hh1 h1_{s-1}) while layer-2 CTAs compute h2_{s-1} (from
-// W_ih2 h1_{s-1} + W_hh2 h2_{s-2} + b2): both only need h1_{s-1}, so one grid barrier per
-// step serves both layers -> T + 1 barriers instead of 2T.  Every CTA keeps its gate rows
-// of the weights resident in shared memory for the whole sequence; layer-2 CTAs own twice
-// the rows (W_ih2 and W_hh2).  Barrier: red.release.gpu arrive + ld.acquire.gpu poll.
+// W_ih2 h1_{s-1} + W_hh2 h2_{s-2} + b2): both only need h1_{s-1}, so one synchronisation
+// per step serves both layers -> T + 1 instead of 2T.  Every CTA keeps its gate rows of the
+// weights resident in shared memory for the whole sequence; layer-2 CTAs own twice the rows
+// (W_ih2 and W_hh2).  No separate grid barrier: h_t is published as tagged 64-bit words
+// (t + 1, h) in parity ping-pong buffers and consumers poll the data itself (one L2 round
+// trip per step); a producer can only overwrite slot t & 1 after it consumed every CTA's
+// step-(t+1) output, so the ping-pong is safe.
 #include "launch.h"
 #include "ptx.cuh"
 
@@ -23,18 +26,28 @@ struct Lstm2Args {
     const float *b2;
     float *H1, *H2; int64_t ldh;
     float *hT, *cT;              // [2][H]
-    float *hbuf;                 // [2 layers][2 ping-pong][H]
-    unsigned *counter;
+    unsigned long long *hbuf;    // [2 layers][2 ping-pong][H] tagged (t + 1) << 32 | float bits
     int T, H, n1, JB1, JB2;      // n1 layer-1 CTAs (JB1 units each), the rest layer 2 (JB2 units)
 };
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void red_release(unsigned *p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// read H tagged values of step `tag` into smem, spinning until each word carries the tag
+__device__ __forceinline__ void gather_h(float *dst, const unsigned long long *src, int H, unsigned tag) {
+    for (int k = threadIdx.x; k < H; k += blockDim.x) {
+        unsigned long long w;
+        uint32_t spins = 0;
+        while (((w = ld_relaxed_u64(src + k)) >> 32) != tag) {
+            if (++spins == (1u << 28)) __trap();       // never hang the GPU on a protocol bug
+        }
+        dst[k] = __uint_as_float((unsigned)(w & 0xffffffffu));
+    }
 }
 
 // dot(w, x) over n elements, one warp, result in all lanes
@@ -78,19 +91,14 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
     for (int u = threadIdx.x; u < JB; u += kThreads) cs[u] = 0.f;
     for (int k = threadIdx.x; k < H; k += kThreads) { x1[k] = 0.f; x2[k] = 0.f; }
     __syncthreads();
-    const unsigned nct = gridDim.x;
 
     for (int s = 0; s <= a.T; ++s) {
         const int t = l2 ? s - 1 : s;           // the time step this CTA computes
         const bool active = t >= 0 && t < a.T;
         if (s > 0) {
-            // h1_{s-1} (both layers), h2_{s-2} (layer 2)
-            const float *h1 = a.hbuf + (size_t)((s - 1) & 1) * H;
-            for (int k = threadIdx.x; k < H; k += kThreads) x1[k] = __ldcg(h1 + k);
-            if (l2 && s >= 2) {
-                const float *h2 = a.hbuf + (size_t)(2 + ((s - 2) & 1)) * H;
-                for (int k = threadIdx.x; k < H; k += kThreads) x2[k] = __ldcg(h2 + k);
-            }
+            // h1_{s-1} (both layers), h2_{s-2} (layer 2): poll the tagged words themselves
+            gather_h(x1, a.hbuf + (size_t)((s - 1) & 1) * H, H, (unsigned)s);
+            if (l2 && s >= 2) gather_h(x2, a.hbuf + (size_t)(2 + ((s - 2) & 1)) * H, H, (unsigned)(s - 1));
             __syncthreads();
         }
         if (active) {
@@ -116,7 +124,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
                     const float c = ptx::sigmoidf_(zf) * cs[u] + ptx::sigmoidf_(zi) * tanhf(zg);
                     const float h = ptx::sigmoidf_(zo) * tanhf(c);
                     cs[u] = c;
-                    a.hbuf[(size_t)((l2 ? 2 : 0) + (t & 1)) * H + j] = h;
+                    st_relaxed_u64(a.hbuf + (size_t)((l2 ? 2 : 0) + (t & 1)) * H + j,
+                                   ((unsigned long long)(t + 1) << 32) | __float_as_uint(h));
                     (l2 ? a.H2 : a.H1)[(int64_t)t * a.ldh + j] = h;
                     if (t == a.T - 1) {
                         a.hT[(l2 ? H : 0) + j] = h;
@@ -125,25 +134,13 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
                 }
             }
         }
-        if (s < a.T) {
-            // grid barrier: publish this step's h, wait for every CTA's
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                red_release(a.counter, 1u);
-                const unsigned target = (unsigned)(s + 1) * nct;
-                uint32_t spins = 0;
-                while (ld_acquire(a.counter) < target) {
-                    if (++spins == (1u << 28)) __trap();
-                }
-            }
-            __syncthreads();
-        }
+        __syncthreads();                        // z / x reuse in the next step
     }
 }
 
 }  // namespace
 
-size_t lstm2_workspace_bytes(int64_t H) { return sizeof(float) * 4 * (size_t)H + 256; }
+size_t lstm2_workspace_bytes(int64_t H) { return sizeof(unsigned long long) * 4 * (size_t)H; }
 
 cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, const float *Wih2, const float *Whh2,
                              int64_t ldw, const float *b2, float *H1, float *H2, int64_t ldh, float *hT, float *cT,
@@ -168,10 +165,9 @@ cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, co
     Lstm2Args a;
     a.G1 = G1; a.ldg = ldg; a.Whh1 = Whh1; a.Wih2 = Wih2; a.Whh2 = Whh2; a.ldw = ldw; a.b2 = b2;
     a.H1 = H1; a.H2 = H2; a.ldh = ldh; a.hT = hT; a.cT = cT;
-    a.hbuf = static_cast<float *>(workspace);
-    a.counter = reinterpret_cast<unsigned *>(static_cast<char *>(workspace) + sizeof(float) * 4 * (size_t)H);
+    a.hbuf = static_cast<unsigned long long *>(workspace);
     a.T = (int)T; a.H = (int)H; a.n1 = n1; a.JB1 = JB1; a.JB2 = JB2;
-    cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned), s);
+    cudaError_t e = cudaMemsetAsync(workspace, 0, lstm2_workspace_bytes(H), s);   // tag 0 = not yet written
     if (e != cudaSuccess) return e;
     void *args[] = {&a};
     return cudaLaunchCooperativeKernel((const void *)lstm2_kernel, dim3((unsigned)(n1 + n2)), dim3(kThreads), args,
