@@ -8,8 +8,9 @@
 // weights resident in shared memory for the whole sequence; layer-2 CTAs own twice the rows
 // (W_ih2 and W_hh2).  No separate grid barrier: h_t is published as tagged 64-bit words
 // (t + 1, h) in parity ping-pong buffers and consumers poll the data itself (one L2 round
-// trip per step); a producer can only overwrite slot t & 1 after it consumed every CTA's
-// step-(t+1) output, so the ping-pong is safe.
+// trip per step).  Ping-pong safety: before a CTA overwrites slot t & 1 it has polled every
+// CTA's later output (h1_{t-1} from layer 1, h2_{t-2} from layer 2), and each CTA produces
+// those only after it consumed what the slot held.
 #include "launch.h"
 #include "ptx.cuh"
 
@@ -98,7 +99,9 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
         if (s > 0) {
             // h1_{s-1} (both layers), h2_{s-2} (layer 2): poll the tagged words themselves
             gather_h(x1, a.hbuf + (size_t)((s - 1) & 1) * H, H, (unsigned)s);
-            if (l2 && s >= 2) gather_h(x2, a.hbuf + (size_t)(2 + ((s - 2) & 1)) * H, H, (unsigned)(s - 1));
+            // layer 2 gathers h2_{s-2}; layer 1 polls it too: every layer-2 CTA writes h2_{s-2}
+            // only after consuming h1_{s-2}, so slot (s & 1) of h1 is free to overwrite
+            if (s >= 2) gather_h(x2, a.hbuf + (size_t)(2 + ((s - 2) & 1)) * H, H, (unsigned)(s - 1));
             __syncthreads();
         }
         if (active) {
