@@ -39,31 +39,49 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// read H tagged values of step `tag` into smem, spinning until each word carries the tag
+constexpr int kMaxPer = 4;                      // H <= kMaxPer * blockDim (1024)
+// read H tagged values of step `tag` into smem: all of this thread's words are requested
+// at once (one L2 round trip), then only stale words are re-polled
 __device__ __forceinline__ void gather_h(float *dst, const unsigned long long *src, int H, unsigned tag) {
-    for (int k = threadIdx.x; k < H; k += blockDim.x) {
-        unsigned long long w;
-        uint32_t spins = 0;
-        while (((w = ld_relaxed_u64(src + k)) >> 32) != tag) {
-            if (++spins == (1u << 28)) __trap();       // never hang the GPU on a protocol bug
+    unsigned long long w[kMaxPer];
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i) {
+        const int k = threadIdx.x + i * blockDim.x;
+        w[i] = (k < H) ? ld_relaxed_u64(src + k) : ((unsigned long long)tag << 32);
+    }
+    uint32_t spins = 0;
+    for (;;) {
+        bool done = true;
+#pragma unroll
+        for (int i = 0; i < kMaxPer; ++i) {
+            if ((w[i] >> 32) != tag) {
+                done = false;
+                w[i] = ld_relaxed_u64(src + threadIdx.x + i * blockDim.x);
+            }
         }
-        dst[k] = __uint_as_float((unsigned)(w & 0xffffffffu));
+        if (done) break;
+        if (++spins == (1u << 26)) __trap();           // never hang the GPU on a protocol bug
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i) {
+        const int k = threadIdx.x + i * blockDim.x;
+        if (k < H) dst[k] = __uint_as_float((unsigned)(w[i] & 0xffffffffu));
     }
 }
 
-// dot(w, x) over n elements, one warp, result in all lanes
-__device__ __forceinline__ float warp_dot(const float *w, const float *x, int n, int lane) {
-    float a0 = 0.f, a1 = 0.f;
-    int k = lane;
-    for (; k + 32 < n; k += 64) {
-        a0 = fmaf(w[k], x[k], a0);
-        a1 = fmaf(w[k + 32], x[k + 32], a1);
-    }
-    if (k < n) a0 = fmaf(w[k], x[k], a0);
-    float a = a0 + a1;
+constexpr int kNC = 32;                         // x chunks per lane: H <= 32 * kNC
+// dot(w, x) with x held in registers (xr[i] = x[lane + 32 i]); four independent chains
+__device__ __forceinline__ float warp_dot_reg(const float *w, const float (&xr)[kNC], int H, int lane) {
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    return a;
+    for (int i = 0; i < kNC; ++i) {
+        const int k = lane + 32 * i;
+        if (32 * i < H && k < H) a[i & 3] = fmaf(w[k], xr[i], a[i & 3]);
+    }
+    float r = (a[0] + a[1]) + (a[2] + a[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    return r;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
@@ -105,10 +123,16 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
             __syncthreads();
         }
         if (active) {
+            float xr1[kNC], xr2[kNC];
+#pragma unroll
+            for (int i = 0; i < kNC; ++i) {
+                const int k = lane + 32 * i;
+                xr1[i] = (k < H) ? x1[k] : 0.f;
+                xr2[i] = (l2 && k < H) ? x2[k] : 0.f;
+            }
             for (int r = warp; r < R; r += kWarps) {
-                float acc;
-                if (l2) acc = warp_dot(W + (size_t)r * H, x1, H, lane) + warp_dot(W + (size_t)(R + r) * H, x2, H, lane);
-                else acc = warp_dot(W + (size_t)r * H, x1, H, lane);
+                float acc = warp_dot_reg(W + (size_t)r * H, xr1, H, lane);
+                if (l2) acc += warp_dot_reg(W + (size_t)(R + r) * H, xr2, H, lane);
                 if (lane == 0) z[r] = acc;
             }
             __syncthreads();
