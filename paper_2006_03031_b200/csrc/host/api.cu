@@ -119,6 +119,9 @@ bool ext_ok(int64_t x) { return x >= 1 && x <= kMaxExtent; }
 // Pipeline depth / smem from the tile geometry, then the launch grid: the dispatch record's
 // tile grid as is for split-K clusters, else min(tiles, 148) persistent CTAs.
 unsigned long long *g_trace = nullptr;     // debug: per-CTA phase timestamps (nimble_debug_trace)
+}  // namespace
+unsigned long long *lstm_trace_buffer() { return g_trace; }
+namespace {
 
 void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
     L.p.trace = g_trace;

@@ -16,6 +16,8 @@
 
 namespace nimble {
 
+unsigned long long *lstm_trace_buffer();     // api.cu: the nimble_debug_trace buffer
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -29,6 +31,7 @@ struct Lstm2Args {
     float *hT, *cT;              // [2][H]
     unsigned long long *hbuf;    // [2 layers][2 ping-pong][H] tagged (t + 1) << 32 | float bits
     int T, H, n1, JB1, JB2;      // n1 layer-1 CTAs (JB1 units each), the rest layer 2 (JB2 units)
+    unsigned long long *trace;   // debug: [2 CTAs][T+1 steps][4 stamps] or NULL
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
@@ -111,9 +114,13 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
     for (int k = threadIdx.x; k < H; k += kThreads) { x1[k] = 0.f; x2[k] = 0.f; }
     __syncthreads();
 
+    unsigned long long *tr = nullptr;
+    if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || (int)blockIdx.x == a.n1))
+        tr = a.trace + (size_t)(blockIdx.x == 0 ? 0 : 1) * (a.T + 1) * 4;
     for (int s = 0; s <= a.T; ++s) {
         const int t = l2 ? s - 1 : s;           // the time step this CTA computes
         const bool active = t >= 0 && t < a.T;
+        if (tr) tr[s * 4 + 0] = ptx::globaltimer();
         if (s > 0) {
             // h1_{s-1} (both layers), h2_{s-2} (layer 2): poll the tagged words themselves
             gather_h(x1, a.hbuf + (size_t)((s - 1) & 1) * H, H, (unsigned)s);
@@ -122,6 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
             if (s >= 2) gather_h(x2, a.hbuf + (size_t)(2 + ((s - 2) & 1)) * H, H, (unsigned)(s - 1));
             __syncthreads();
         }
+        if (tr) tr[s * 4 + 1] = ptx::globaltimer();
         if (active) {
             float xr1[kNC], xr2[kNC];
 #pragma unroll
@@ -136,6 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
                 if (lane == 0) z[r] = acc;
             }
             __syncthreads();
+            if (tr) tr[s * 4 + 2] = ptx::globaltimer();
             if (threadIdx.x < JB) {
                 const int u = threadIdx.x, j = j0 + u;
                 if (j < H) {
@@ -162,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
             }
         }
         __syncthreads();                        // z / x reuse in the next step
+        if (tr) tr[s * 4 + 3] = ptx::globaltimer();
     }
 }
 
@@ -194,6 +204,7 @@ cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, co
     a.H1 = H1; a.H2 = H2; a.ldh = ldh; a.hT = hT; a.cT = cT;
     a.hbuf = static_cast<unsigned long long *>(workspace);
     a.T = (int)T; a.H = (int)H; a.n1 = n1; a.JB1 = JB1; a.JB2 = JB2;
+    a.trace = lstm_trace_buffer();
     cudaError_t e = cudaMemsetAsync(workspace, 0, lstm2_workspace_bytes(H), s);   // tag 0 = not yet written
     if (e != cudaSuccess) return e;
     void *args[] = {&a};
