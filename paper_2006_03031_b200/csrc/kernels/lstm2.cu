@@ -72,19 +72,19 @@ __device__ __forceinline__ void gather_h(float *dst, const unsigned long long *s
     }
 }
 
-constexpr int kNC = 32;                         // x chunks per lane: H <= 32 * kNC
-// dot(w, x) with x held in registers (xr[i] = x[lane + 32 i]); four independent chains
-__device__ __forceinline__ float warp_dot_reg(const float *w, const float (&xr)[kNC], int H, int lane) {
-    float a[4] = {0.f, 0.f, 0.f, 0.f};
+constexpr int kRowsPerWarp = 8;                 // gate rows per matrix per CTA <= 8 * kWarps
+// acc[rr] += W[row_rr] . x over the zero-padded row length Hp (multiple of 32): all of the
+// warp's rows advance together, one independent FMA chain each, no per-element guards.
+__device__ __forceinline__ void warp_rows_dot(float (&acc)[kRowsPerWarp], const float *W, const float *x, int Hp,
+                                              int warp, int nrows, int lane) {
+    for (int k = lane; k < Hp; k += 32) {
+        const float xv = x[k];
 #pragma unroll
-    for (int i = 0; i < kNC; ++i) {
-        const int k = lane + 32 * i;
-        if (32 * i < H && k < H) a[i & 3] = fmaf(w[k], xr[i], a[i & 3]);
+        for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+            const int r = warp + kWarps * rr;
+            if (r < nrows) acc[rr] = fmaf(W[(size_t)r * Hp + k], xv, acc[rr]);
+        }
     }
-    float r = (a[0] + a[1]) + (a[2] + a[3]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    return r;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
@@ -96,22 +96,23 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
     const int j0 = cta * JB;
     const int R = 4 * JB;                       // gate rows per matrix
     const int nmat = l2 ? 2 : 1;
-    float *W = sm;                              // [nmat][R][H]
-    float *x1 = W + (size_t)nmat * R * H;       // h1_{s-1}
-    float *x2 = x1 + H;                         // h2_{s-2} (layer 2 only)
-    float *z = x2 + H;                          // [R]
+    const int Hp = 32 * ((H + 31) / 32);        // rows zero-padded to whole warp chunks
+    float *W = sm;                              // [nmat][R][Hp]
+    float *x1 = W + (size_t)nmat * R * Hp;      // h1_{s-1} (zero-padded to Hp)
+    float *x2 = x1 + Hp;                        // h2_{s-2} (layer 2 only)
+    float *z = x2 + Hp;                         // [R]
     float *cs = z + R;                          // [JB]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     for (int m = 0; m < nmat; ++m) {
         const float *src = l2 ? (m == 0 ? a.Wih2 : a.Whh2) : a.Whh1;
-        for (int e = threadIdx.x; e < R * H; e += kThreads) {
-            const int r = e / H, k = e % H, g = r / JB, u = r % JB, j = j0 + u;
-            W[(size_t)m * R * H + e] = (j < H) ? src[(int64_t)(g * H + j) * a.ldw + k] : 0.f;
+        for (int e = threadIdx.x; e < R * Hp; e += kThreads) {
+            const int r = e / Hp, k = e % Hp, g = r / JB, u = r % JB, j = j0 + u;
+            W[(size_t)m * R * Hp + e] = (j < H && k < H) ? src[(int64_t)(g * H + j) * a.ldw + k] : 0.f;
         }
     }
     for (int u = threadIdx.x; u < JB; u += kThreads) cs[u] = 0.f;
-    for (int k = threadIdx.x; k < H; k += kThreads) { x1[k] = 0.f; x2[k] = 0.f; }
+    for (int k = threadIdx.x; k < Hp; k += kThreads) { x1[k] = 0.f; x2[k] = 0.f; }
     __syncthreads();
 
     unsigned long long *tr = nullptr;
@@ -131,17 +132,20 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
         }
         if (tr) tr[s * 4 + 1] = ptx::globaltimer();
         if (active) {
-            float xr1[kNC], xr2[kNC];
+            float acc[kRowsPerWarp];
 #pragma unroll
-            for (int i = 0; i < kNC; ++i) {
-                const int k = lane + 32 * i;
-                xr1[i] = (k < H) ? x1[k] : 0.f;
-                xr2[i] = (l2 && k < H) ? x2[k] : 0.f;
+            for (int rr = 0; rr < kRowsPerWarp; ++rr) acc[rr] = 0.f;
+            warp_rows_dot(acc, W, x1, Hp, warp, R, lane);
+            if (l2) warp_rows_dot(acc, W + (size_t)R * Hp, x2, Hp, warp, R, lane);
+#pragma unroll
+            for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
             }
-            for (int r = warp; r < R; r += kWarps) {
-                float acc = warp_dot_reg(W + (size_t)r * H, xr1, H, lane);
-                if (l2) acc += warp_dot_reg(W + (size_t)(R + r) * H, xr2, H, lane);
-                if (lane == 0) z[r] = acc;
+            if (lane == 0) {
+#pragma unroll
+                for (int rr = 0; rr < kRowsPerWarp; ++rr)
+                    if (warp + kWarps * rr < R) z[warp + kWarps * rr] = acc[rr];
             }
             __syncthreads();
             if (tr) tr[s * 4 + 2] = ptx::globaltimer();
@@ -189,10 +193,11 @@ cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, co
     int n2 = 2 * n1;
     const int JB2 = (int)((H + n2 - 1) / n2);
     n2 = (int)((H + JB2 - 1) / JB2);
-    const size_t smem1 = sizeof(float) * ((size_t)4 * JB1 * H + 2 * H + 4 * JB1 + JB1);
-    const size_t smem2 = sizeof(float) * ((size_t)8 * JB2 * H + 2 * H + 4 * JB2 + JB2);
+    const int64_t Hp = 32 * ((H + 31) / 32);
+    const size_t smem1 = sizeof(float) * ((size_t)4 * JB1 * Hp + 2 * Hp + 4 * JB1 + JB1);
+    const size_t smem2 = sizeof(float) * ((size_t)8 * JB2 * Hp + 2 * Hp + 4 * JB2 + JB2);
     const size_t smem = smem1 > smem2 ? smem1 : smem2;
-    if (smem > 232448 || n1 + n2 > 148) return cudaErrorInvalidValue;
+    if (smem > 232448 || n1 + n2 > 148 || 4 * JB1 > 8 * kWarps || 4 * JB2 > 8 * kWarps) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(lstm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
