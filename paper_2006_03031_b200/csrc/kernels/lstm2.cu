@@ -77,6 +77,7 @@ constexpr int kRowsPerWarp = 8;                 // gate rows per matrix per CTA 
 // warp's rows advance together, one independent FMA chain each, no per-element guards.
 __device__ __forceinline__ void warp_rows_dot(float (&acc)[kRowsPerWarp], const float *W, const float *x, int Hp,
                                               int warp, int nrows, int lane) {
+#pragma unroll 4
     for (int k = lane; k < Hp; k += 32) {
         const float xv = x[k];
 #pragma unroll
@@ -122,6 +123,13 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
         const int t = l2 ? s - 1 : s;           // the time step this CTA computes
         const bool active = t >= 0 && t < a.T;
         if (tr) tr[s * 4 + 0] = ptx::globaltimer();
+        // layer 1: prefetch this step's hoisted input projection while the gather waits
+        float gpre[4] = {0.f, 0.f, 0.f, 0.f};
+        if (!l2 && active && threadIdx.x < JB && j0 + (int)threadIdx.x < H) {
+            const float *g = a.G1 + (int64_t)t * a.ldg + j0 + threadIdx.x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) gpre[q] = __ldg(g + q * H);
+        }
         if (s > 0) {
             // h1_{s-1} (both layers), h2_{s-2} (layer 2): poll the tagged words themselves
             gather_h(x1, a.hbuf + (size_t)((s - 1) & 1) * H, H, (unsigned)s);
@@ -157,9 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
                         zi = z[u] + a.b2[j]; zf = z[JB + u] + a.b2[H + j];
                         zg = z[2 * JB + u] + a.b2[2 * H + j]; zo = z[3 * JB + u] + a.b2[3 * H + j];
                     } else {
-                        const float *g = a.G1 + (int64_t)t * a.ldg;
-                        zi = z[u] + g[j]; zf = z[JB + u] + g[H + j]; zg = z[2 * JB + u] + g[2 * H + j];
-                        zo = z[3 * JB + u] + g[3 * H + j];
+                        zi = z[u] + gpre[0]; zf = z[JB + u] + gpre[1]; zg = z[2 * JB + u] + gpre[2];
+                        zo = z[3 * JB + u] + gpre[3];
                     }
                     const float c = ptx::sigmoidf_(zf) * cs[u] + ptx::sigmoidf_(zi) * tanhf(zg);
                     const float h = ptx::sigmoidf_(zo) * tanhf(c);
