@@ -29,15 +29,26 @@ def shard(lens: np.ndarray, world: int, rank: int) -> np.ndarray:
 
 
 class GraphCache:
-    """Per-L CUDA graphs of a full encoder forward reading a static input buffer and
-    writing the [CLS] row into a static output row."""
+    """Per-L CUDA graphs of a full encoder forward for ONE request (batch 1), reading a static
+    input buffer and writing the [CLS] row into a static output row.  The encoder is either a
+    BertPacked over a single request (7 launches per layer, fused attention) or a BertEncoder
+    (9 launches per layer: bmm_dyn -> softmax -> bmm_dyn attention)."""
 
     def __init__(self, encoder, device="cuda"):
         self.enc = encoder
-        self.xin = torch.zeros((encoder.max_len, encoder.d), dtype=torch.bfloat16, device=device)
+        self.packed = hasattr(encoder, "max_tokens")
+        max_len = encoder.max_tokens if self.packed else encoder.max_len
+        self.xin = torch.zeros((max_len, encoder.d), dtype=torch.bfloat16, device=device)
         self.cls = torch.zeros((encoder.d,), dtype=torch.bfloat16, device=device)
+        self.offs = {}
         self.graphs = {}
         self.stream = torch.cuda.Stream(device=device)
+
+    def _forward(self, L: int):
+        if self.packed:
+            off = self.offs.setdefault(L, torch.tensor([0, L], dtype=torch.int32, device=self.xin.device))
+            return self.enc.forward(self.xin, off, L, T=L)
+        return self.enc.forward(self.xin, L)
 
     def capture(self, L: int):
         if L in self.graphs:
@@ -46,9 +57,9 @@ class GraphCache:
         s = self.stream
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            self.enc.forward(self.xin, L)          # warm (lazy attribute setup) outside capture
+            self._forward(L)                       # warm (lazy attribute setup) outside capture
             with torch.cuda.graph(g, stream=s):
-                y = self.enc.forward(self.xin, L)
+                y = self._forward(L)
                 self.cls.copy_(y[0])
         torch.cuda.current_stream().wait_stream(s)
         self.graphs[L] = g

@@ -53,7 +53,7 @@ def main():
     # ---- config 3 (batch-1 graphs, every L in 1..128)
     cfg = dict(synth.BERT_BASE)
     w = synth.bert_weights_device(cfg, seed=0)
-    enc = BertEncoder(cfg, w, max_len=128)
+    enc = BertPacked(cfg, w, max_tokens=128)          # batch 1 = packed batch of one request
     cache = GraphCache(enc)
     c3 = []
     out = torch.empty((cfg["d"],), dtype=torch.bfloat16, device="cuda")
@@ -61,7 +61,7 @@ def main():
         cache.capture(L)
         x = synth.device_normal(L, cfg["d"], seed=L)
         t = ev_time(lambda: cache.run(x, L, out), reps=5, warm=2)
-        fl = enc.flops(L)
+        fl = BertPacked.flops([L], cfg["d"], cfg["ffn"], cfg["layers"])
         c3.append({"L": L, "us": t * 1e6, "us_per_token": t * 1e6 / L, "tflops": fl / t / 1e12})
     rep["config3_bert_base_batch1"] = c3
     print(json.dumps({k: c3[i] for k, i in (("L1", 0), ("L64", 63), ("L128", 127))}), flush=True)
