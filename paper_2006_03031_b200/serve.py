@@ -46,8 +46,9 @@ class GraphCache:
 
     def _forward(self, L: int):
         if self.packed:
-            off = self.offs.setdefault(L, torch.tensor([0, L], dtype=torch.int32, device=self.xin.device))
-            return self.enc.forward(self.xin, off, L, T=L)
+            if L not in self.offs:                  # created before capture (no H2D inside a graph)
+                self.offs[L] = torch.tensor([0, L], dtype=torch.int32, device=self.xin.device)
+            return self.enc.forward(self.xin, self.offs[L], L, T=L)
         return self.enc.forward(self.xin, L)
 
     def capture(self, L: int):
