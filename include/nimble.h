@@ -221,6 +221,26 @@ int nimble_treelstm_level(const int32_t *nodes, const float *A, int64_t lda, con
                           int64_t ldo, int64_t M, int64_t K, int64_t H, int is_leaf, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * A whole Tree-LSTM forest in ONE launch (same cell as nimble_treelstm_level; the level
+ * loop of P:586's "small kernels plus control flow" runs on the device).  The schedule is
+ * device data: nodes, rows, parent_slot are int32 [n_nodes] grouped by height, level l
+ * occupying [level_off[l], level_off[l+1]) (level_off: device int32 [n_levels + 1]).
+ * Level 0 holds exactly the leaves (height 0): A row = X + rows[m]*ldx (K = I), W = W_l
+ * [3H x I] (row stride I).  Levels >= 1 hold internal nodes whose children sit in lower
+ * levels: A row = hcat + rows[m]*ldcat (K = 2H), W = U [5H x 2H] (row stride 2H), [c_l|c_r]
+ * from ccat + nodes[m]*ldcat.  Outputs and parent-slot writes as nimble_treelstm_level.
+ * max_level = the largest level size (sizes the grid).  workspace: NIMBLE_TREE_WORKSPACE_BYTES
+ * device bytes (level-barrier counter; reset by the call, stream-ordered).  All CTAs must be
+ * co-resident (cooperative launch): a launch that cannot be returns NIMBLE_E_CUDA.
+ * ------------------------------------------------------------------------- */
+#define NIMBLE_TREE_WORKSPACE_BYTES 256
+int nimble_treelstm_forest(const float *X, int64_t ldx, const float *W_l, const float *b_l, const float *U,
+                           const float *b_u, int64_t I, int64_t H, const int32_t *level_off, int64_t n_levels,
+                           int64_t max_level, const int32_t *nodes, const int32_t *rows, const int32_t *parent_slot,
+                           float *hcat, float *ccat, int64_t ldcat, float *h_out, float *c_out, int64_t ldo,
+                           void *workspace, void *stream);
+
+/* ---------------------------------------------------------------------------
  * Request sharding (BJ:5): deterministic LPT partition of R requests of lengths
  * lens[R] over G ranks on cost(L) = 24 (25165824 L + 4096 L^2) (BERT-large flops):
  * sort by (cost desc, id asc), give each to the least-loaded rank (ties -> lowest).

@@ -455,3 +455,26 @@ extern "C" int nimble_treelstm_level(const int32_t *nodes, const float *A, int64
     clear_error();
     return NIMBLE_OK;
 }
+
+extern "C" int nimble_treelstm_forest(const float *X, int64_t ldx, const float *W_l, const float *b_l, const float *U,
+                                      const float *b_u, int64_t I, int64_t H, const int32_t *level_off,
+                                      int64_t n_levels, int64_t max_level, const int32_t *nodes, const int32_t *rows,
+                                      const int32_t *parent_slot, float *hcat, float *ccat, int64_t ldcat,
+                                      float *h_out, float *c_out, int64_t ldo, void *workspace, void *stream) {
+    if (!X || !W_l || !b_l || !U || !b_u || !level_off || !nodes || !rows || !parent_slot || !hcat || !ccat ||
+        !h_out || !c_out || !workspace)
+        return fail(NIMBLE_E_NULL, "nimble_treelstm_forest: NULL pointer");
+    if (!ext_ok(I) || !ext_ok(H) || !ext_ok(n_levels) || !ext_ok(max_level))
+        return fail(NIMBLE_E_EXTENT, "nimble_treelstm_forest: extents must be >= 1");
+    if (ldx < I || ldcat < 2 * H || ldo < H) return fail(NIMBLE_E_SHAPE, "nimble_treelstm_forest: ld too small");
+    if (!aligned16(X) || !aligned16(W_l) || !aligned16(U) || !aligned16(hcat) || ldx % 4 || ldcat % 4 || I % 4 ||
+        (2 * H) % 4)
+        return fail(NIMBLE_E_ALIGN, "nimble_treelstm_forest: X/W_l/U/hcat need 16-B alignment; ldx, ldcat, I, 2H multiples of 4");
+    TreeForestParams p{X, ldx, W_l, b_l, U, b_u, level_off, nodes, rows, parent_slot, hcat, ccat, ldcat, h_out, c_out,
+                       ldo, static_cast<unsigned *>(workspace), nullptr, (int32_t)n_levels, (int32_t)I, (int32_t)H,
+                       (int32_t)max_level};
+    cudaError_t e = launch_treelstm_forest(p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("nimble_treelstm_forest launch", e);
+    clear_error();
+    return NIMBLE_OK;
+}

@@ -120,4 +120,19 @@ struct TreeParams {
 };
 cudaError_t launch_treelstm_level(const TreeParams &p, cudaStream_t s);
 
+// Whole forest in one persistent launch: levels in height order, grid barrier between levels.
+struct TreeForestParams {
+    const float *X; int64_t ldx;            // word vectors (leaf inputs)
+    const float *W_l, *b_l;                 // [3H x I], [3H]
+    const float *U, *b_u;                   // [5H x 2H], [5H]
+    const int32_t *level_off;               // [n_levels + 1], level 0 = leaves
+    const int32_t *nodes, *rows, *pslot;    // [n_nodes] in level order
+    float *hcat, *ccat; int64_t ldcat;
+    float *h_out, *c_out; int64_t ldo;
+    unsigned *counter;
+    unsigned long long *trace;              // debug (nimble_debug_trace): [cta][level][2] stamps
+    int32_t n_levels, I, H, max_level;
+};
+cudaError_t launch_treelstm_forest(const TreeForestParams &p, cudaStream_t s);
+
 }  // namespace nimble

@@ -71,6 +71,8 @@ _SIGS = {
     "nimble_lstm_seq": [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp],
     "nimble_treelstm_level": [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _i64,
                               _i64, C.c_int, _vp],
+    "nimble_treelstm_forest": [_vp, _i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
+                               _i64, _vp, _vp, _i64, _vp, _vp],
     "nimble_partition_lpt": [_i64p, _i64, C.c_int32, _i32p],
     "nimble_debug_trace": [_vp],
     "nimble_lstm2_seq": [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp],
@@ -275,6 +277,18 @@ def lstm2_seq(G1, W_hh1, W_ih2, W_hh2, b2, H1, H2, hT, cT, workspace, T=None, st
     _check(_lib.nimble_lstm2_seq(_ptr(G1), G1.stride(0), _ptr(W_hh1), _ptr(W_ih2), _ptr(W_hh2), W_hh1.stride(0),
                                  _ptr(b2), _ptr(H1), _ptr(H2), H1.stride(0), _ptr(hT), _ptr(cT), T, H,
                                  _ptr(workspace), _stream(stream)))
+
+
+TREE_WORKSPACE_BYTES = 256
+
+
+def treelstm_forest(X, W_l, b_l, U, b_u, level_off, n_levels, max_level, nodes, rows, parent_slot, hcat, ccat,
+                    h_out, c_out, workspace, stream=None):
+    I, H = W_l.shape[1], U.shape[1] // 2
+    _check(_lib.nimble_treelstm_forest(_ptr(X), X.stride(0), _ptr(W_l), _ptr(b_l), _ptr(U), _ptr(b_u), I, H,
+                                       _ptr(level_off), n_levels, max_level, _ptr(nodes), _ptr(rows),
+                                       _ptr(parent_slot), _ptr(hcat), _ptr(ccat), hcat.stride(0), _ptr(h_out),
+                                       _ptr(c_out), h_out.stride(0), _ptr(workspace), _stream(stream)))
 
 
 def treelstm_level(nodes, A, a_rows, W, bias, parent_slot, hcat, ccat, h_out, c_out, M, K, H, is_leaf,

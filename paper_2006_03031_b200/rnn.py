@@ -8,9 +8,10 @@ the device.  Feature dims are padded to a multiple of 4 with zero columns for th
 fp32 vector loads; the padding contributes exact zeros.
 
 Tree-LSTM (config 4): the recursion over the tree ADT
-becomes a host schedule of levels (node height); each level is one
-nimble_treelstm_level launch over all nodes of that height in the forest, whose
-epilogue writes (h, c) straight into the parent's input row.
+becomes a schedule of levels (node height), built once on the host and kept on the
+device; the whole forest is one nimble_treelstm_forest launch that loops over the
+levels on the device (or, fused=False, one nimble_treelstm_level launch per level).
+Each level's epilogue writes (h, c) straight into the parent's input row.
 """
 from __future__ import annotations
 
@@ -100,6 +101,12 @@ class TreeSchedule:
             to = lambda a: torch.tensor(a, dtype=torch.int32, device=device)
             self.levels.append((to(ids), to(rows), to([parent_slot[i] for i in ids]), len(ids)))
         self.n_leaves = sum(1 for i in range(n) if left[i] < 0)
+        # the same schedule as flat device arrays for the one-launch forest kernel
+        cat = lambda k: torch.cat([lv[k] for lv in self.levels])
+        self.nodes_all, self.rows_all, self.pslot_all = cat(0), cat(1), cat(2)
+        self.level_off = torch.tensor(np.concatenate([[0], np.cumsum([lv[3] for lv in self.levels])]),
+                                      dtype=torch.int32, device=device)
+        self.max_level = max(lv[3] for lv in self.levels)
 
 
 class TreeLSTM:
@@ -109,19 +116,27 @@ class TreeLSTM:
         assert self.I % 4 == 0 and (2 * self.H) % 4 == 0
         self.W_l, self.b_l = W_l.to(device).contiguous(), b_l.to(device).contiguous()
         self.U, self.b_u = U.to(device).contiguous(), b_u.to(device).contiguous()
+        self.ws = torch.zeros((nb.TREE_WORKSPACE_BYTES,), dtype=torch.uint8, device=device)
 
     def flops(self, sched: TreeSchedule) -> int:
         n_int = sched.n_nodes - sched.n_leaves
         return sched.n_leaves * 2 * 3 * self.H * self.I + n_int * 2 * 5 * self.H * 2 * self.H
 
-    def forward(self, X: torch.Tensor, sched: TreeSchedule):
-        """X [n_words x I] fp32 on device; returns (h [n_nodes x H], c [n_nodes x H])."""
+    def forward(self, X: torch.Tensor, sched: TreeSchedule, fused: bool = True):
+        """X [n_words x I] fp32 on device; returns (h [n_nodes x H], c [n_nodes x H]).
+        fused: the whole forest in one nimble_treelstm_forest launch; else one
+        nimble_treelstm_level launch per level."""
         H, n = self.H, sched.n_nodes
         dev = X.device
-        hcat = torch.zeros((n, 2 * H), dtype=torch.float32, device=dev)
-        ccat = torch.zeros((n, 2 * H), dtype=torch.float32, device=dev)
+        hcat = torch.empty((n, 2 * H), dtype=torch.float32, device=dev)     # every internal row is written
+        ccat = torch.empty((n, 2 * H), dtype=torch.float32, device=dev)     # by its two children first
         h = torch.empty((n, H), dtype=torch.float32, device=dev)
         c = torch.empty((n, H), dtype=torch.float32, device=dev)
+        if fused:
+            nb.treelstm_forest(X, self.W_l, self.b_l, self.U, self.b_u, sched.level_off, len(sched.levels),
+                               sched.max_level, sched.nodes_all, sched.rows_all, sched.pslot_all, hcat, ccat, h, c,
+                               self.ws)
+            return h, c
         for lvl, (ids, rows, pslot, M) in enumerate(sched.levels):
             if lvl == 0:
                 nb.treelstm_level(ids, X, rows, self.W_l, self.b_l, pslot, hcat, ccat, h, c, M, self.I, H, 1)

@@ -37,8 +37,20 @@ def ev_time(fn, reps=10, warm=3):
 
 
 def main():
+    only = set(sys.argv[1].split(",")) if len(sys.argv) > 1 else {"2", "3", "4"}
     rep = {}
-    # ---- config 2
+    if "2" in only:
+        config2(rep)
+    if "3" in only:
+        config3(rep)
+    if "4" in only:
+        config4(rep)
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/configs_report.json", "w") as f:
+        json.dump(rep, f, indent=1)
+
+
+def config2(rep):
     I = H = 650
     st = LSTMStack(synth.lstm_weights(I, H, 2, seed=0), max_T=512)
     c2 = []
@@ -50,7 +62,10 @@ def main():
                    "gflops": st.flops_per_token() * T / t / 1e9})
         print(json.dumps(c2[-1]), flush=True)
     rep["config2_lstm_650x2"] = c2
-    # ---- config 3 (batch-1 graphs, every L in 1..128)
+
+
+def config3(rep):
+    # batch-1 graphs, every L in 1..128
     cfg = dict(synth.BERT_BASE)
     w = synth.bert_weights_device(cfg, seed=0)
     enc = BertPacked(cfg, w, max_tokens=128)          # batch 1 = packed batch of one request
@@ -76,23 +91,24 @@ def main():
                                         "us_per_token": t * 1e6 / Tt,
                                         "tflops": BertPacked.flops(lens, cfg["d"], cfg["ffn"], cfg["layers"]) / t / 1e12}
     print(json.dumps(rep["config3_bert_base_packed64"]), flush=True)
-    # ---- config 4
+
+
+def config4(rep):
     I, Hh = 300, 150
     W_l, b_l, U, b_u = synth.tree_weights(I, Hh)
     model = TreeLSTM(W_l, b_l, U, b_u)
     c4 = []
-    for n in (1, 32):
+    for n in (1, 32, 256):
         trees, nw = synth.random_forest(n, seed=2)
         sched = TreeSchedule(trees)
         X = synth.normal((nw, I), 1.0, 4, torch.float32).cuda()
         t = ev_time(lambda: model.forward(X, sched))
+        t_lv = ev_time(lambda: model.forward(X, sched, fused=False))
         c4.append({"trees": n, "leaves": sched.n_leaves, "levels": len(sched.levels), "us_per_forest": t * 1e6,
-                   "us_per_tree": t * 1e6 / n, "us_per_leaf": t * 1e6 / sched.n_leaves})
+                   "us_per_tree": t * 1e6 / n, "us_per_leaf": t * 1e6 / sched.n_leaves,
+                   "gflops": model.flops(sched) / t / 1e9, "per_level_launches_us_per_forest": t_lv * 1e6})
         print(json.dumps(c4[-1]), flush=True)
     rep["config4_treelstm_300_150"] = c4
-    os.makedirs("gpurun_out", exist_ok=True)
-    with open("gpurun_out/configs_report.json", "w") as f:
-        json.dump(rep, f, indent=1)
 
 
 if __name__ == "__main__":

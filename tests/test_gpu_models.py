@@ -102,16 +102,38 @@ def test_lstm_paper_sizes_300_512(nb, orc):
     assert _abs_err(out, ref) <= 1e-4
 
 
-@pytest.mark.parametrize("n_trees", [1, 5, 32])
-def test_treelstm_forest(nb, orc, n_trees):
+def _caterpillar(n_leaves, first_word=0):
+    """Maximally deep binary tree: every internal node has a leaf as its left child."""
+    left, right, word = [-1], [-1], [first_word]
+    top = 0
+    for i in range(1, n_leaves):
+        left.append(-1); right.append(-1); word.append(first_word + i)
+        leaf = len(left) - 1
+        left.append(leaf); right.append(top); word.append(-1)
+        top = len(left) - 1
+    return top, left, right, word
+
+
+def _forest(kind):
+    if kind == "single_leaf":            # a root that is a leaf (one level) next to a 2-leaf tree
+        return [(0, [-1], [-1], [0]), (2, [-1, -1, 0], [-1, -1, 1], [1, 2, -1])], 3
+    if kind == "caterpillar":            # 40 levels -> 39 device barriers
+        return [_caterpillar(40)], 40
+    n = int(kind)
+    return synth.random_forest(n, seed=2 + n)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("kind", ["1", "5", "32", "256", "single_leaf", "caterpillar"])
+def test_treelstm_forest(nb, orc, kind, fused):
     from paper_2006_03031_b200.rnn import TreeLSTM, TreeSchedule
     I, H = 300, 150
-    trees, n_words = synth.random_forest(n_trees, seed=2 + n_trees)
-    X = synth.normal((n_words, I), 1.0, 400 + n_trees, torch.float32)
+    trees, n_words = _forest(kind)
+    X = synth.normal((n_words, I), 1.0, 400 + len(trees), torch.float32)
     W_l, b_l, U, b_u = synth.tree_weights(I, H)
     sched = TreeSchedule(trees)
     model = TreeLSTM(W_l, b_l, U, b_u)
-    h, c = model.forward(X.cuda(), sched)
+    h, c = model.forward(X.cuda(), sched, fused=fused)
     torch.cuda.synchronize()
     off = 0
     for (root, l, r, w) in trees:
