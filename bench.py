@@ -35,6 +35,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "dynamic-seq-len BERT GEMM TFLOP/s & % TC peak vs static shape; req/s @1/2/4/8 GPU"
 UNIT = "req/s"
+DEFAULT_SCHEDULES = os.path.join(os.path.dirname(os.path.abspath(__file__)), "paper_2006_03031_b200", "tuned",
+                                 "bert_dense_schedules.json")
 WORKLOAD = "config5: BERT-large (d=1024, 16 heads, ffn 4096, 24 layers) variable-length request stream, L~U{1..512}, batch 1 per request"
 
 
@@ -175,6 +177,8 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nimble", choices=["nimble", "reference"])
+    ap.add_argument("--schedules", default=DEFAULT_SCHEDULES,
+                    help="tuned dense schedules (scripts/tune_symbolic.py output) to register; 'none' = default rule")
     ap.add_argument("--mode", default="packed", choices=["packed", "batch1"],
                     help="packed: a rank's whole shard as one token-packed forward (M = sum L_i); "
                          "batch1: one request at a time from per-L CUDA graphs")
@@ -226,6 +230,10 @@ def main():
     max_len = int(my_lens.max()) if len(my_lens) else 1
 
     t_setup = time.perf_counter()
+    sched_used = None
+    if args.schedules != "none" and os.path.exists(args.schedules):
+        nb.load_dense_schedules(args.schedules)      # P:392-406 tuned tiles (small-M dense ops)
+        sched_used = os.path.relpath(args.schedules, os.path.dirname(os.path.abspath(__file__)))
     if args.mode == "packed":
         enc = BertPacked(cfg, weights, max_tokens=max(my_tokens, 1))
         launches_per_step = enc.launches_per_forward()
@@ -380,7 +388,7 @@ def main():
                           "execution": ("token-packed forward: 7 launches/layer (dense_dyn M=sum L_i x4, "
                                         "attention_varlen, layernorm x2)" if args.mode == "packed" else
                                         "per-L CUDA graphs of one-request packed forwards (batch 1)"),
-                          "setup_s": round(t_setup, 2)},
+                          "tuned_schedules": sched_used, "setup_s": round(t_setup, 2)},
                "tflops": tflops, "pct_tc_peak": tflops / peaks["tc_sus"],
                "gpu_launches": gpu_launches, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk}
         print(json.dumps(res))

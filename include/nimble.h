@@ -99,6 +99,22 @@ int nimble_shape_bmm(const int64_t a_shape[3], const int64_t b_shape[3], int tra
 int nimble_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, nimble_dispatch *out);
 int nimble_dispatch_bmm(int64_t batch, int64_t M, int64_t N, int64_t K, int trans_b, int dt,
                         nimble_dispatch *out);
+
+/* ---------------------------------------------------------------------------
+ * Tuned schedules (Nimble §3.5 symbolic tuning: "tune with Any := 64, keep the
+ * top-k, cross-evaluate on powers of two <= 256, pick the best average"; the procedure is
+ * scripts/tune_symbolic.py).  A schedule registered for a bf16 dense op with weight
+ * shape (N, K) replaces family 1's token tile t (the residue tile: x = t k + r, classes
+ * ceil(r/16) in 0..t/16, so t/16 + 1 variants) and caps its split-K factor (t = 256 runs
+ * without split-K: the fp32 exchange buffers would not fit shared memory); it applies to
+ * nimble_dispatch_dense and nimble_dense_dyn with M < 2048 (family 3 and the static twin are
+ * not tuned).  tile_t in {32, 64, 128, 256} (0 removes the entry), split_max in {1, 2, 4, 8};
+ * anything else -> NIMBLE_E_EXTENT.  Process-wide, thread-safe.  get: tile_t = 0 when no
+ * schedule is registered (the default t = 128, split_max = 8 applies).
+ * ------------------------------------------------------------------------- */
+int nimble_set_dense_schedule(int64_t N, int64_t K, int32_t tile_t, int32_t split_max);
+int nimble_get_dense_schedule(int64_t N, int64_t K, int32_t *tile_t, int32_t *split_max);
+
 /* c = total number of generated kernels ("dispatch/k"); 0 = all (default).
  * c < 0 -> E_EXTENT.  Process-global. */
 int nimble_set_variant_limit(int c);

@@ -71,6 +71,8 @@ def _declare(L):
     L.orc_shape_dense.argtypes = [_i64p, _i64p, _i64p]
     L.orc_shape_bmm.argtypes = [_i64p, _i64p, C.c_int, _i64p]
     L.orc_dispatch_dense.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.POINTER(Dispatch)]
+    L.orc_dispatch_dense_sched.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int32, C.c_int32,
+                                           C.POINTER(Dispatch)]
     L.orc_dispatch_bmm.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
                                    C.POINTER(Dispatch)]
     L.orc_gelu.argtypes = [C.c_double]
@@ -126,9 +128,13 @@ def shape_bmm(a_shape, b_shape, trans_b=0):
 
 
 # ---------------------------------------------------------------- O2 dispatch
-def dispatch_dense(M, N, K, dt, c=0):
+def dispatch_dense(M, N, K, dt, c=0, tile_t=0, split_max=8):
+    """tile_t / split_max: a tuned family-1 schedule (DISPATCH.md); 0 = default."""
     d = Dispatch()
-    st = lib().orc_dispatch_dense(M, N, K, dt, c, C.byref(d))
+    if tile_t:
+        st = lib().orc_dispatch_dense_sched(M, N, K, dt, c, tile_t, split_max, C.byref(d))
+    else:
+        st = lib().orc_dispatch_dense(M, N, K, dt, c, C.byref(d))
     return st, (d.as_dict() if st == 0 else None)
 
 

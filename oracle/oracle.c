@@ -100,21 +100,29 @@ static int orc_variant(int32_t cls, int32_t n_classes, int c) {
 
 static int64_t orc_ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-static int32_t orc_split(int64_t tiles, int64_t K) {
+static int32_t orc_split_cap(int64_t tiles, int64_t K, int32_t cap) {
     int64_t kb = orc_ceil_div(K, 64);
     int32_t s = 1;
-    while (s < 8 && tiles * 2 * s <= 148 && kb >= 8 * (int64_t)s) s *= 2;
+    while (s < cap && tiles * 2 * s <= 148 && kb >= 8 * (int64_t)s) s *= 2;
     return s;
 }
+
+static int32_t orc_split(int64_t tiles, int64_t K) { return orc_split_cap(tiles, K, 8); }
 
 #define ORC_MAXEXT 2147483647LL
 
 /* families 1 / 3, UMMA_T: tokens (symbolic M) on the UMMA-N slot, granule 16;
  * t = 128 for M < 2048 (family 1, split-K allowed), t = 256 for M >= 2048 (family 3). */
-static int orc_umma_t(int64_t batch, int64_t M, int64_t N, int64_t K, int c, orc_dispatch *d) {
+/* tile_t / split_max: a tuned schedule for family 1 (DISPATCH.md "Tuned schedules",
+ * P:392-406 three-step symbolic tuning picks them); tile_t = 0 -> the default (128, 8). */
+static int orc_umma_t_sched(int64_t batch, int64_t M, int64_t N, int64_t K, int c, int32_t tile_t,
+                            int32_t split_max, orc_dispatch *d) {
     memset(d, 0, sizeof(*d));
-    int32_t t = (M < 2048) ? 128 : 256;
-    d->family = (t == 128) ? 1 : 3; d->tile_t = t; d->granule = 16; d->n_classes = t / 16 + 1;
+    int wide = (M >= 2048);
+    int32_t t = wide ? 256 : (tile_t > 0 ? tile_t : 128);
+    /* split-K exchanges two fp32 [128 x t] buffers through smem: only t <= 128 fits */
+    int32_t cap = (!wide && tile_t > 0) ? (t <= 128 ? split_max : 1) : 8;
+    d->family = wide ? 3 : 1; d->tile_t = t; d->granule = 16; d->n_classes = t / 16 + 1;
     d->k = M / t; d->r = M % t;                      /* x = t k + r */
     d->residue_class = (int32_t)orc_ceil_div(d->r, 16);
     d->variant = orc_variant(d->residue_class, d->n_classes, c);
@@ -122,12 +130,16 @@ static int orc_umma_t(int64_t batch, int64_t M, int64_t N, int64_t K, int c, orc
     if (d->r == 0) d->umma_n_tail = 0;
     else d->umma_n_tail = (d->variant >= 0) ? 16 * d->residue_class : t;
     int64_t mt = orc_ceil_div(N, 128), nt = d->k + (d->r > 0);
-    d->split_k = (t == 128) ? orc_split(mt * nt * batch, K) : 1;
+    d->split_k = wide ? 1 : orc_split_cap(mt * nt * batch, K, cap);
     d->grid[0] = (int32_t)mt; d->grid[1] = (int32_t)nt; d->grid[2] = (int32_t)(batch * d->split_k);
     /* family 3 runs CTA pairs (tcgen05 cta_group::2): one 256-row MMA per pair */
-    d->cluster[0] = (t == 128) ? 1 : 2; d->cluster[1] = 1; d->cluster[2] = d->split_k;
-    if (t == 256) d->umma_m = 256;
+    d->cluster[0] = wide ? 2 : 1; d->cluster[1] = 1; d->cluster[2] = d->split_k;
+    if (wide) d->umma_m = 256;
     return ORC_OK;
+}
+
+static int orc_umma_t(int64_t batch, int64_t M, int64_t N, int64_t K, int c, orc_dispatch *d) {
+    return orc_umma_t_sched(batch, M, N, K, c, 0, 8, d);
 }
 
 int orc_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, int c, orc_dispatch *d) {
@@ -148,6 +160,17 @@ int orc_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, int c, orc_dispa
     }
     if (dt != 1) return ORC_E_DTYPE;
     return orc_umma_t(1, M, N, K, c, d);
+}
+
+int orc_dispatch_dense_sched(int64_t M, int64_t N, int64_t K, int dt, int c, int32_t tile_t, int32_t split_max,
+                             orc_dispatch *d) {
+    if (tile_t == 0) return orc_dispatch_dense(M, N, K, dt, c, d);
+    if (dt != 1) return ORC_E_DTYPE;                 /* schedules exist for the bf16 family only */
+    if (!(tile_t == 32 || tile_t == 64 || tile_t == 128 || tile_t == 256)) return ORC_E_EXTENT;
+    if (!(split_max == 1 || split_max == 2 || split_max == 4 || split_max == 8)) return ORC_E_EXTENT;
+    if (M < 1 || N < 1 || K < 1 || M > ORC_MAXEXT || N > ORC_MAXEXT || K > ORC_MAXEXT) return ORC_E_EXTENT;
+    if (c < 0) return ORC_E_EXTENT;
+    return orc_umma_t_sched(1, M, N, K, c, tile_t, split_max, d);
 }
 
 int orc_dispatch_bmm(int64_t batch, int64_t M, int64_t N, int64_t K, int trans_b, int dt, int c,

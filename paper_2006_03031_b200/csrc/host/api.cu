@@ -207,7 +207,11 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     if (!aligned16(x) || !aligned16(W) || !aligned16(y) || ((ldx * 2) % 16) || ((ldw * 2) % 16) || ((ldy * 2) % 16) ||
         (epi == NIMBLE_EPI_BIAS_RESIDUAL && (!aligned16(residual) || (ldr * 2) % 16)))
         return fail(NIMBLE_E_ALIGN, "nimble_dense_dyn(bf16): TMA needs 16-B aligned x/W/y/residual and ld*2 % 16 == 0");
-    dispatch_umma_t(1, M, N, K, &d);
+    {
+        int32_t t = 0, cap = 8;                       // tuned schedule for this op, if registered
+        if (!static_twin) dense_schedule(N, K, &t, &cap);  // (static twins are compiled for t = 128)
+        dispatch_umma_t(1, M, N, K, &d, t, cap);
+    }
     UmmaLaunch L;
     std::memset(&L, 0, sizeof(L));
     L.b_mn_major = 0;

@@ -5,6 +5,8 @@
 // fallback.  The rule is DISPATCH.md; the oracle implements it independently.
 #include <atomic>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "internal.h"
 
@@ -36,13 +38,13 @@ int32_t select_variant(const ResidueFamily &f, int32_t cls) {
 }
 
 // split-K factor (cluster size along K): grow while the grown grid still fits one
-// wave of 148 CTAs and every split keeps >= 4 k-blocks of 64.
-int32_t choose_split(int64_t ctas, int64_t K) {
+// wave of 148 CTAs and every split keeps >= 4 k-blocks of 64; at most `cap`.
+int32_t choose_split(int64_t ctas, int64_t K, int32_t cap = 8) {
     const int64_t kblocks = cdiv(K, 64);
     int32_t s = 1;
     for (;;) {
         const int32_t next = s * 2;
-        if (next > 8 || ctas * next > kNumSMs || kblocks / next < 4) break;
+        if (next > cap || ctas * next > kNumSMs || kblocks / next < 4) break;
         s = next;
     }
     return s;
@@ -72,9 +74,16 @@ int dispatch_simt8(int64_t M, int64_t N, nimble_dispatch *d) {
     return NIMBLE_OK;
 }
 
-int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, nimble_dispatch *d) {
+int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, nimble_dispatch *d,
+                    int32_t tile_t, int32_t split_max) {
     *d = nimble_dispatch{};
-    const ResidueFamily &f = (M_tokens >= kWideTileFrom) ? kUMMA_T256 : kUMMA_T;
+    const bool wide = M_tokens >= kWideTileFrom;
+    // a tuned schedule replaces family 1's token tile t (residue classes
+    // t/16 + 1) and caps its split-K; family 3 (M >= 2048) is not tuned.
+    const ResidueFamily tuned{kUMMA_T.id, tile_t, 16, tile_t / 16 + 1};
+    const ResidueFamily &f = wide ? kUMMA_T256 : (tile_t > 0 ? tuned : kUMMA_T);
+    // split-K parks and receives fp32 [128 x t] slices in smem: only t <= 128 fits 227 KB
+    const int32_t cap = (!wide && tile_t > 0) ? (tile_t <= 128 ? split_max : 1) : 8;
     split_residue(f, M_tokens, d);
     d->residue_class = static_cast<int32_t>(cdiv(d->r, f.granule));
     d->variant = select_variant(f, d->residue_class);
@@ -83,7 +92,7 @@ int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, 
     d->umma_n_tail = d->r == 0 ? 0 : (d->variant < 0 ? f.t : f.granule * d->residue_class);
     const int64_t m_tiles = cdiv(N_rows, 128);
     const int64_t n_tiles = d->k + (d->r ? 1 : 0);
-    d->split_k = (f.id == kUMMA_T.id) ? choose_split(m_tiles * n_tiles * batch, K) : 1;
+    d->split_k = (f.id == kUMMA_T.id) ? choose_split(m_tiles * n_tiles * batch, K, cap) : 1;
     static const int force = [] { const char *e = std::getenv("NIMBLE_FORCE_SPLIT"); return e ? std::atoi(e) : 0; }();
     if (force > 0) d->split_k = force;      // experiment-only override (breaks oracle parity)
     d->grid[0] = static_cast<int32_t>(m_tiles);
@@ -117,9 +126,55 @@ int dispatch_umma_d(int64_t batch, int64_t M, int64_t N, int64_t K, nimble_dispa
     return NIMBLE_OK;
 }
 
+// ---------------------------------------------------------------- tuned schedules
+namespace {
+struct ScheduleEntry {
+    int64_t N, K;
+    int32_t tile_t, split_max;
+};
+std::mutex g_sched_mu;
+std::vector<ScheduleEntry> g_sched;
+}  // namespace
+
+void dense_schedule(int64_t N, int64_t K, int32_t *tile_t, int32_t *split_max) {
+    std::lock_guard<std::mutex> lk(g_sched_mu);
+    *tile_t = 0;
+    *split_max = 8;
+    for (const auto &e : g_sched)
+        if (e.N == N && e.K == K) {
+            *tile_t = e.tile_t;
+            *split_max = e.split_max;
+            return;
+        }
+}
+
 }  // namespace nimble
 
 using namespace nimble;
+
+extern "C" int nimble_set_dense_schedule(int64_t N, int64_t K, int32_t tile_t, int32_t split_max) {
+    if (N < 1 || K < 1 || N > kMaxExtent || K > kMaxExtent)
+        return fail(NIMBLE_E_EXTENT, "nimble_set_dense_schedule: extents must be in [1, 2^31-1]");
+    if (tile_t != 0 && tile_t != 32 && tile_t != 64 && tile_t != 128 && tile_t != 256)
+        return fail(NIMBLE_E_EXTENT, "nimble_set_dense_schedule: tile_t must be 0, 32, 64, 128 or 256");
+    if (split_max != 1 && split_max != 2 && split_max != 4 && split_max != 8)
+        return fail(NIMBLE_E_EXTENT, "nimble_set_dense_schedule: split_max must be 1, 2, 4 or 8");
+    std::lock_guard<std::mutex> lk(g_sched_mu);
+    for (size_t i = 0; i < g_sched.size(); ++i)
+        if (g_sched[i].N == N && g_sched[i].K == K) {
+            if (tile_t == 0) g_sched.erase(g_sched.begin() + (long)i);
+            else g_sched[i].tile_t = tile_t, g_sched[i].split_max = split_max;
+            return NIMBLE_OK;
+        }
+    if (tile_t != 0) g_sched.push_back({N, K, tile_t, split_max});
+    return NIMBLE_OK;
+}
+
+extern "C" int nimble_get_dense_schedule(int64_t N, int64_t K, int32_t *tile_t, int32_t *split_max) {
+    if (!tile_t || !split_max) return fail(NIMBLE_E_NULL, "nimble_get_dense_schedule: NULL output");
+    dense_schedule(N, K, tile_t, split_max);
+    return NIMBLE_OK;
+}
 
 static bool extents_valid(std::initializer_list<int64_t> xs) {
     for (int64_t x : xs)
@@ -139,7 +194,11 @@ extern "C" int nimble_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, ni
     if (!out) return fail(NIMBLE_E_NULL, "nimble_dispatch_dense: out is NULL");
     if (!extents_valid({M, N, K})) return fail(NIMBLE_E_EXTENT, "nimble_dispatch_dense: extents must be in [1, 2^31-1]");
     if (dt == NIMBLE_F32) return dispatch_simt8(M, N, out);
-    if (dt == NIMBLE_BF16) return dispatch_umma_t(1, M, N, K, out);
+    if (dt == NIMBLE_BF16) {
+        int32_t t, cap;
+        dense_schedule(N, K, &t, &cap);
+        return dispatch_umma_t(1, M, N, K, out, t, cap);
+    }
     return fail(NIMBLE_E_DTYPE, "nimble_dispatch_dense: unknown dtype");
 }
 

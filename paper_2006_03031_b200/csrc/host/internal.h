@@ -21,7 +21,10 @@ bool extent_ok(int64_t d);
 // dispatch (dispatch.cc) — DISPATCH.md
 int variant_limit();
 int dispatch_simt8(int64_t M, int64_t N, nimble_dispatch *d);
-int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, nimble_dispatch *d);
+int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, nimble_dispatch *d,
+                    int32_t tile_t = 0, int32_t split_max = 8);
+// bf16 dense: the tuned schedule registered for (N, K) (nimble_set_dense_schedule), if any
+void dense_schedule(int64_t N, int64_t K, int32_t *tile_t, int32_t *split_max);
 int dispatch_umma_d(int64_t batch, int64_t M, int64_t N, int64_t K, nimble_dispatch *d);
 
 }  // namespace nimble

@@ -60,6 +60,8 @@ _SIGS = {
     "nimble_dispatch_dense": [_i64, _i64, _i64, C.c_int, C.POINTER(Dispatch)],
     "nimble_dispatch_bmm": [_i64, _i64, _i64, _i64, C.c_int, C.c_int, C.POINTER(Dispatch)],
     "nimble_set_variant_limit": [C.c_int],
+    "nimble_set_dense_schedule": [_i64, _i64, C.c_int32, C.c_int32],
+    "nimble_get_dense_schedule": [_i64, _i64, _i32p, _i32p],
     "nimble_get_variant_limit": [],
     "nimble_last_dispatch": [C.POINTER(Dispatch)],
     "nimble_dense_dyn": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, C.c_int, C.c_int, _vp],
@@ -153,6 +155,28 @@ def set_variant_limit(c: int):
 
 def get_variant_limit() -> int:
     return _lib.nimble_get_variant_limit()
+
+
+def set_dense_schedule(N: int, K: int, tile_t: int, split_max: int = 8):
+    """Register a tuned family-1 schedule for bf16 dense ops with weight shape (N, K)
+    (tile_t = 0 removes it).  See include/nimble.h and scripts/tune_symbolic.py."""
+    _check(_lib.nimble_set_dense_schedule(N, K, tile_t, split_max))
+
+
+def get_dense_schedule(N: int, K: int):
+    t, s = C.c_int32(), C.c_int32()
+    _check(_lib.nimble_get_dense_schedule(N, K, C.byref(t), C.byref(s)))
+    return t.value, s.value
+
+
+def load_dense_schedules(path: str):
+    """Register every schedule of a tuning table written by scripts/tune_symbolic.py."""
+    import json
+    with open(path) as f:
+        table = json.load(f)
+    for e in table["schedules"]:
+        set_dense_schedule(e["N"], e["K"], e["tile_t"], e["split_max"])
+    return table["schedules"]
 
 
 def last_dispatch():

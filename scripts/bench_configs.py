@@ -16,10 +16,14 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2006_03031_b200 import synth  # noqa: E402
+from paper_2006_03031_b200 import nimble as nb, synth  # noqa: E402
 from paper_2006_03031_b200.bert import BertEncoder, BertPacked  # noqa: E402
 from paper_2006_03031_b200.rnn import LSTMStack, TreeLSTM, TreeSchedule  # noqa: E402
 from paper_2006_03031_b200.serve import GraphCache  # noqa: E402
+
+
+SCHEDULES = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2006_03031_b200",
+                         "tuned", "bert_dense_schedules.json")
 
 
 def ev_time(fn, reps=10, warm=3):
@@ -65,21 +69,27 @@ def config2(rep):
 
 
 def config3(rep):
-    # batch-1 graphs, every L in 1..128
+    # batch-1 graphs, every L in 1..128; default dispatch rule, then the tuned schedules
     cfg = dict(synth.BERT_BASE)
     w = synth.bert_weights_device(cfg, seed=0)
-    enc = BertPacked(cfg, w, max_tokens=128)          # batch 1 = packed batch of one request
-    cache = GraphCache(enc)
-    c3 = []
     out = torch.empty((cfg["d"],), dtype=torch.bfloat16, device="cuda")
-    for L in range(1, 129):
-        cache.capture(L)
-        x = synth.device_normal(L, cfg["d"], seed=L)
-        t = ev_time(lambda: cache.run(x, L, out), reps=5, warm=2)
-        fl = BertPacked.flops([L], cfg["d"], cfg["ffn"], cfg["layers"])
-        c3.append({"L": L, "us": t * 1e6, "us_per_token": t * 1e6 / L, "tflops": fl / t / 1e12})
-    rep["config3_bert_base_batch1"] = c3
-    print(json.dumps({k: c3[i] for k, i in (("L1", 0), ("L64", 63), ("L128", 127))}), flush=True)
+    for tag in ("", "_tuned"):
+        if tag:
+            nb.load_dense_schedules(SCHEDULES)
+        enc = BertPacked(cfg, w, max_tokens=128)          # batch 1 = packed batch of one request
+        cache = GraphCache(enc)
+        c3 = []
+        for L in range(1, 129):
+            cache.capture(L)
+            x = synth.device_normal(L, cfg["d"], seed=L)
+            t = ev_time(lambda: cache.run(x, L, out), reps=5, warm=2)
+            fl = BertPacked.flops([L], cfg["d"], cfg["ffn"], cfg["layers"])
+            c3.append({"L": L, "us": t * 1e6, "us_per_token": t * 1e6 / L, "tflops": fl / t / 1e12})
+        rep["config3_bert_base_batch1" + tag] = c3
+        print(tag, json.dumps({k: c3[i] for k, i in (("L1", 0), ("L64", 63), ("L128", 127))}), flush=True)
+        del cache, enc
+    for op in json.load(open(SCHEDULES))["schedules"]:
+        nb.set_dense_schedule(op["N"], op["K"], 0, 8)
     # packed BERT-base: 64 requests with L ~ U{1..128}
     lens = synth.request_lengths(64, seed=2, hi=128)
     Tt = int(lens.sum())

@@ -25,7 +25,7 @@ def test_exports_every_declared_symbol(nb):
     hdr = open(os.path.join(ROOT, "include", "nimble.h")).read()
     hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)          # drop comments
     declared = set(re.findall(r"\b(nimble_[a-z_0-9]+)\s*\(", hdr))
-    assert len(declared) == 24
+    assert len(declared) == 26
     for name in declared:
         assert hasattr(nb._lib, name), name
     assert set(nb.EXPORTED) <= declared | {"nimble_last_error", "nimble_version"}
@@ -71,6 +71,34 @@ def test_dispatch_bmm_bit_exact(nb, orc, c):
             assert nb.dispatch_bmm(*bad)[0] == orc.dispatch_bmm(*bad, c)[0]
     finally:
         nb.set_variant_limit(0)
+
+
+@pytest.mark.parametrize("tile_t,split_max", [(32, 8), (64, 1), (64, 4), (128, 2), (256, 8), (256, 1)])
+def test_dispatch_tuned_schedule_bit_exact(nb, orc, tile_t, split_max):
+    """A registered schedule changes the residue tile and split cap identically
+    in the library and the oracle; other (N, K) keep the default; removal restores it."""
+    N, K = 1024, 4096
+    nb.set_dense_schedule(N, K, tile_t, split_max)
+    try:
+        assert nb.get_dense_schedule(N, K) == (tile_t, split_max)
+        for c in (0, 2):
+            nb.set_variant_limit(c)
+            for M in range(1, 2200):
+                assert nb.dispatch_dense(M, N, K, 1) == orc.dispatch_dense(M, N, K, 1, c, tile_t, split_max), (M, c)
+        nb.set_variant_limit(0)
+        for M in (1, 77, 300):
+            assert nb.dispatch_dense(M, 128, 128, 1) == orc.dispatch_dense(M, 128, 128, 1)
+    finally:
+        nb.set_variant_limit(0)
+        nb.set_dense_schedule(N, K, 0, 8)
+    assert nb.get_dense_schedule(N, K) == (0, 8)
+    assert nb.dispatch_dense(100, N, K, 1) == orc.dispatch_dense(100, N, K, 1)
+
+
+def test_dense_schedule_validation(nb):
+    for bad in ((1024, 4096, 48, 8), (1024, 4096, 128, 3), (0, 4096, 128, 8), (1024, 4096, -1, 8)):
+        with pytest.raises(nb.NimbleError):
+            nb.set_dense_schedule(*bad)
 
 
 def test_dispatch_errors_match(nb, orc):

@@ -108,6 +108,30 @@ def test_bf16_dense_vs_oracle(nb, orc, N, K):
             assert nb.last_dispatch() == orc.dispatch_dense(M, N, K, 1)[1]
 
 
+@pytest.mark.parametrize("tile_t,split_max", [(32, 8), (64, 1), (64, 8), (128, 1), (256, 2), (256, 8)])
+def test_bf16_tuned_schedule_vs_oracle(nb, orc, tile_t, split_max):
+    """Every tunable schedule (token tile t, split-K cap) computes the same op: parity with
+    the oracle at residues of t (incl. the tail widths 16..t) and the dispatch record equals
+    the oracle's schedule-aware dispatch."""
+    N, K = 1024, 4096
+    W = synth.normal((N, K), 0.05, 71)
+    b = synth.normal((N,), 0.1, 72, torch.float32)
+    nb.set_dense_schedule(N, K, tile_t, split_max)
+    try:
+        for M in (1, 15, 17, 31, 33, 64, 65, 100, 129, 200, 255, 257, 513, 1000):
+            x = synth.normal((M, K), 1.0, 2000 + M)
+            for epi in (nb.EPI_BIAS, nb.EPI_BIAS_RESIDUAL):
+                res = synth.normal((M, N), 1.0, 77 + M) if epi == nb.EPI_BIAS_RESIDUAL else None
+                y = _dense_gpu(nb, x, W, b, epi, res)
+                ref, D = orc.dense(x.double().numpy(), W.double().numpy(), b.numpy(),
+                                   None if res is None else res.double().numpy(), epi)
+                e = _err(y, ref, D)
+                assert e <= TOL_BF16, (tile_t, split_max, M, epi, e)
+                assert nb.last_dispatch() == orc.dispatch_dense(M, N, K, 1, 0, tile_t, split_max)[1]
+    finally:
+        nb.set_dense_schedule(N, K, 0, 8)
+
+
 @pytest.mark.parametrize("N,K", [(256, 256), (1024, 4096), (3072, 1024)])
 def test_bf16_integer_exact_bitwise(nb, orc, N, K):
     W = synth.ternary((N, K), 31, torch.bfloat16)

@@ -157,3 +157,31 @@ def test_dispatch_bmm_families(orc):
     st, d = orc.dispatch_bmm(16, 300, 64, 300, 1, 1)
     assert st == 0 and d["family"] == 2 and d["k"] == 2 and d["r"] == 44
     assert d["umma_n_full"] == 64 and d["umma_n_tail"] == 64 and d["grid"][1] == 1
+
+
+@pytest.mark.parametrize("tile_t,split_max", [(32, 8), (64, 2), (128, 8), (256, 4)])
+def test_oracle_tuned_schedule_invariants(orc, tile_t, split_max):
+    """Pins of the schedule-parameterised dispatch (DISPATCH.md "Tuned schedules"): the
+    decomposition x = t k + r with 0 <= r < t, class = ceil(r / 16), t/16 + 1 classes, the
+    tail width 16 class, one token tile per t tokens (+1 for a residue), split-K a power of
+    two <= split_max that keeps one wave (tiles * 2s <= 148) — and (128, 8) reproduces the
+    default schedule exactly; M >= 2048 ignores the schedule."""
+    N, K = 1024, 4096
+    m_tiles = -(-N // 128)
+    for M in list(range(1, 600)) + [1000, 2047]:
+        st, d = orc.dispatch_dense(M, N, K, 1, 0, tile_t, split_max)
+        assert st == 0 and d["family"] == 1 and d["tile_t"] == tile_t
+        assert d["k"] * tile_t + d["r"] == M and 0 <= d["r"] < tile_t
+        assert d["residue_class"] == -(-d["r"] // 16) and d["n_classes"] == tile_t // 16 + 1
+        assert d["umma_n_full"] == tile_t
+        assert d["umma_n_tail"] == (0 if d["r"] == 0 else 16 * d["residue_class"])
+        n_tiles = d["k"] + (d["r"] > 0)
+        assert list(d["grid"][:2]) == [m_tiles, n_tiles]
+        s = d["split_k"]
+        assert s in (1, 2, 4, 8) and s <= split_max and (s == 1 or m_tiles * n_tiles * s <= 148)
+        assert tile_t <= 128 or s == 1
+        assert d["grid"][2] == s and list(d["cluster"]) == [1, 1, s]
+        if tile_t == 128 and split_max == 8:
+            assert d == orc.dispatch_dense(M, N, K, 1)[1]
+    for M in (2048, 5000):
+        assert orc.dispatch_dense(M, N, K, 1, 0, tile_t, split_max)[1] == orc.dispatch_dense(M, N, K, 1)[1]
