@@ -147,6 +147,25 @@ int nimble_dense_static(const void *x, int64_t ldx, const void *W, int64_t ldw, 
                         const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
                         int64_t K, int dt, int epi, void *stream);
 
+/* nimble_dense_dyn_dev — device-resident extent and dispatch (the "upper bound" shape
+ * function of P:269-271 plus on-device dispatch, so one captured CUDA graph serves every
+ * extent; P:709-710 hides dispatch behind GPU execution).  bf16 only.  The caller
+ * allocates by the bound M_max (1 <= M_max < 2048; nimble_shape_dense on (M_max, K) x
+ * (N, K)); the true extent M is the int32 at M_dev (device memory, 1 <= M <= M_max, read
+ * by the kernel after its grid-dependency wait, so an earlier kernel or copy on the stream
+ * may write it).  The kernel runs the residue dispatch on the device: family 1 of
+ * DISPATCH.md with split_k = 1 and the token tile of the registered schedule (else 128),
+ * the variant limit c current at launch.  Writes y rows [0, M) only (the store's tensor
+ * map is re-encoded on the device with extent M; rows [M, M_max) of y are untouched);
+ * x rows in [M, M_max) are read but only feed unstored columns.  dispatch_dev: NULL or a
+ * device nimble_dispatch that receives the device's dispatch decision.  A device extent
+ * outside [1, M_max] traps (the error surfaces at the next synchronisation).  Uses a
+ * library-owned ring of 64 per-launch tensor-map slot blocks per device: at most 64
+ * nimble_dense_dyn_dev launches may be in flight at once. */
+int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+                         const void *residual, int64_t ldr, void *y, int64_t ldy, const int32_t *M_dev,
+                         int64_t M_max, int64_t N, int64_t K, int epi, nimble_dispatch *dispatch_dev, void *stream);
+
 /* ---------------------------------------------------------------------------
  * nimble_bmm_dyn — C[b] = alpha . A[b] . Bhat[b] over a strided batch (attention
  * heads), bf16 inputs, fp32 accumulation; out_dt = NIMBLE_F32 or NIMBLE_BF16.

@@ -4,6 +4,7 @@
 // encoding and asynchronous launches on the caller's stream.
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -267,6 +268,98 @@ extern "C" int nimble_dense_static(const void *x, int64_t ldx, const void *W, in
                                    const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
                                    int64_t K, int dt, int epi, void *stream) {
     return dense_impl(x, ldx, W, ldw, bias, residual, ldr, y, ldy, M, N, K, dt, epi, stream, true);
+}
+
+// ------------------------------------------------------------------ dense_dyn_dev
+namespace nimble {
+namespace {
+// Library-owned ring of per-CTA tensor-map slots for device-extent launches: launch i uses
+// block i % kSlotRing, so a kernel never patches a slot an in-flight neighbour still reads
+// (PDL overlaps adjacent kernels only).  One ring per device, allocated on first use.
+constexpr int kSlotRing = 64;
+std::mutex g_slot_mu;
+CUtensorMap *g_slots[64] = {};
+std::atomic<uint32_t> g_slot_seq{0};
+
+cudaError_t next_slot_block(CUtensorMap **out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    {
+        std::lock_guard<std::mutex> lk(g_slot_mu);
+        if (!g_slots[dev]) {
+            e = cudaMalloc(&g_slots[dev], sizeof(CUtensorMap) * (size_t)kSlotRing * kNumSMs);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    *out = g_slots[dev] + (size_t)(g_slot_seq.fetch_add(1) % kSlotRing) * kNumSMs;
+    return cudaSuccess;
+}
+}  // namespace
+}  // namespace nimble
+
+extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+                                    const void *residual, int64_t ldr, void *y, int64_t ldy, const int32_t *M_dev,
+                                    int64_t M_max, int64_t N, int64_t K, int epi, nimble_dispatch *dispatch_dev,
+                                    void *stream) {
+    if (!ext_ok(M_max) || !ext_ok(N) || !ext_ok(K)) return fail(NIMBLE_E_EXTENT, "nimble_dense_dyn_dev: extents must be in [1, 2^31-1]");
+    if (M_max >= 2048) return fail(NIMBLE_E_UNSUPPORTED, "nimble_dense_dyn_dev: M_max must be < 2048 (family 1)");
+    const int64_t xs[2] = {M_max, K}, ws[2] = {N, K};
+    int64_t os[2];
+    int st = nimble_shape_dense(xs, ws, os);           // upper-bound shape
+    if (st != NIMBLE_OK) return st;
+    if (!x || !W || !y || !M_dev) return fail(NIMBLE_E_NULL, "nimble_dense_dyn_dev: x, W, y and M_dev must be non-NULL");
+    if (epi < NIMBLE_EPI_NONE || epi > NIMBLE_EPI_BIAS_RESIDUAL) return fail(NIMBLE_E_DTYPE, "nimble_dense_dyn_dev: unknown epilogue");
+    if (epi >= NIMBLE_EPI_BIAS && !bias) return fail(NIMBLE_E_NULL, "nimble_dense_dyn_dev: bias required by the epilogue");
+    if (epi == NIMBLE_EPI_BIAS_RESIDUAL && !residual) return fail(NIMBLE_E_NULL, "nimble_dense_dyn_dev: residual required");
+    if (ldx < K || ldw < K || ldy < N || (epi == NIMBLE_EPI_BIAS_RESIDUAL && ldr < N))
+        return fail(NIMBLE_E_SHAPE, "nimble_dense_dyn_dev: leading dimension smaller than the row length");
+    if (!aligned16(x) || !aligned16(W) || !aligned16(y) || ((ldx * 2) % 16) || ((ldw * 2) % 16) || ((ldy * 2) % 16) ||
+        (epi == NIMBLE_EPI_BIAS_RESIDUAL && (!aligned16(residual) || (ldr * 2) % 16)))
+        return fail(NIMBLE_E_ALIGN, "nimble_dense_dyn_dev: TMA needs 16-B aligned x/W/y/residual and ld*2 % 16 == 0");
+    int32_t t = 0, cap = 8;
+    dense_schedule(N, K, &t, &cap);                    // tuned token tile (split is always 1 here)
+    nimble_dispatch d;
+    dispatch_umma_t(1, M_max, N, K, &d, t > 0 ? t : 128, 1);   // launch geometry for the bound
+    UmmaLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    L.p.rows_a = (int32_t)N;
+    L.p.rows_b = (int32_t)M_max;
+    L.p.n_full = d.umma_n_full;
+    L.p.n_tail = d.r ? d.umma_n_tail : d.umma_n_full;
+    L.p.box_n = d.umma_n_full;                         // fixed box: the tail width is decided on device
+    L.p.kb_total = (int32_t)((K + 63) / 64);
+    L.p.split = 1;
+    L.epi = epi;
+    L.transposed = 1;
+    L.p.alpha = 1.f;
+    L.p.out = y;
+    L.p.ld_out = ldy;
+    L.p.bias = bias;
+    L.p.res = residual;
+    L.p.ld_res = ldr;
+    L.p.a_static = pdl_enabled() ? 1 : 0;
+    L.p.m_dev = M_dev;
+    L.p.var_c = variant_limit();
+    L.p.rec = dispatch_dev;
+    if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
+    if ((st = encode_operand(&L.tmB, x, K, M_max, ldx, 1, 0, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+    if ((st = encode_out(&L.tmOut, y, false, N, M_max, ldy, 1, 0, L.p.box_n, &L.p.out_batch_mid)) != NIMBLE_OK) return st;
+    if (epi == NIMBLE_EPI_BIAS_RESIDUAL) {
+        int mid = 0;
+        if ((st = encode_out(&L.tmRes, const_cast<void *>(residual), false, N, M_max, ldr, 1, 0, L.p.box_n, &mid)) != NIMBLE_OK) return st;
+    } else {
+        L.tmRes = L.tmOut;
+    }
+    cudaError_t e = next_slot_block(&L.p.out_slot);
+    if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn_dev slot ring", e);
+    plan_pipeline(L, d);
+    L.stream = static_cast<cudaStream_t>(stream);
+    e = launch_umma_gemm(L);
+    if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn_dev launch", e);
+    clear_error();
+    return NIMBLE_OK;
 }
 
 // ------------------------------------------------------------------ bmm_dyn

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
+#include "nimble.h"
+
 namespace nimble {
 
 // Parameters of one tcgen05 GEMM launch (families UMMA_T / UMMA_D, DISPATCH.md).
@@ -36,6 +38,13 @@ struct UmmaParams {
     int64_t ld_res;
     unsigned long long *trace;   // optional per-CTA phase timestamps (globaltimer ns), NULL = off
     int32_t dbg;                 // experiment bits (NIMBLE_DBG env): 1 skip split stores, 2 skip recv reads
+    // device-resident extent (nimble_dense_dyn_dev): the symbolic token extent is read from
+    // m_dev after the grid-dependency wait and the residue dispatch runs on the device;
+    // rows_b / tiles_n / n_tail above then describe the upper bound M_max.
+    const int32_t *m_dev;        // NULL = host extent
+    int32_t var_c;               // variant limit c for the device dispatch
+    CUtensorMap *out_slot;       // per-CTA global slots for the extent-patched output map
+    nimble_dispatch *rec;        // optional device record of the device dispatch (CTA 0 writes it)
 };
 
 struct UmmaLaunch {

@@ -208,6 +208,40 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *m, const void *s
                  "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                  : "memory");
 }
+// ---- on-device tensor-map patching (sm_90a / sm_100a "modifiable TMA"): a 128-B map copied
+// into shared memory gets one global_dim replaced, is written back to a global slot with a
+// release fence to the tensormap proxy (warp-wide .sync.aligned), and a consumer acquires it.
+template <int DIM>
+__device__ __forceinline__ void tmap_replace_dim_smem(void *smem_map, uint32_t extent) {
+    asm volatile("tensormap.replace.tile.global_dim.shared::cta.b1024.b32 [%0], %1, %2;" ::"r"(smem_u32(smem_map)),
+                 "n"(DIM), "r"(extent)
+                 : "memory");
+}
+__device__ __forceinline__ void tmap_cp_fence_release(void *gmem_map, const void *smem_map) {
+    asm volatile(
+        "tensormap.cp_fenceproxy.global.shared::cta.tensormap::generic.release.gpu.sync.aligned [%0], [%1], 128;" ::"l"(
+            reinterpret_cast<uint64_t>(gmem_map)),
+        "r"(smem_u32(smem_map))
+        : "memory");
+}
+__device__ __forceinline__ void tmap_fence_acquire(const void *gmem_map) {
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(gmem_map))
+                 : "memory");
+}
+// Copy a tensor map (param space) into smem, patch one extent, publish it to `slot` (global),
+// acquire it.  Called by one full warp; returns the map to use for TMA.
+template <int DIM>
+__device__ __forceinline__ const CUtensorMap *tmap_patch_extent(const CUtensorMap *tmpl, void *smem_map,
+                                                               CUtensorMap *slot, uint32_t extent, uint32_t lane) {
+    if (lane < 8) reinterpret_cast<uint4 *>(smem_map)[lane] = reinterpret_cast<const uint4 *>(tmpl)[lane];
+    __syncwarp();
+    if (lane == 0) tmap_replace_dim_smem<DIM>(smem_map, extent);
+    __syncwarp();
+    tmap_cp_fence_release(slot, smem_map);
+    tmap_fence_acquire(slot);
+    return slot;
+}
+
 __device__ __forceinline__ void tma_store_commit_wait() {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

@@ -82,6 +82,32 @@ __device__ __forceinline__ TileCoord tile_of(const Geo &g, int t) {
     return c;
 }
 
+// Device-side residue dispatch for nimble_dense_dyn_dev (DISPATCH.md family 1 with split 1,
+// the upper-bound form of P:268-271): M is data read after the grid-dependency wait, the
+// rule is the host's, so the recorded dispatch is bit-identical to the oracle's.
+__device__ __forceinline__ void devm_geometry(const UmmaParams &p, Geo &g, int &total_tiles, bool record) {
+    const int M = *p.m_dev;
+    if (M < 1 || M > p.rows_b) __trap();              // outside [1, M_max]: caller bug, fail loudly
+    const int t = g.n_full;
+    const int k = M / t, r = M - k * t;               // x = t k + r
+    const int cls = (r + 15) / 16, ncls = t / 16 + 1;
+    const int cc = (p.var_c <= 0 || p.var_c >= ncls) ? ncls : p.var_c;
+    const int variant = (cc == ncls || cls < cc - 1) ? cls : -1;
+    g.rows_b = M;
+    g.tiles_n = k + (r ? 1 : 0);
+    g.n_tail = r ? (variant >= 0 ? 16 * cls : t) : t;
+    total_tiles = g.tiles_m * g.tiles_n * p.batch;
+    if (record && p.rec) {
+        nimble_dispatch d{};
+        d.family = 1; d.tile_t = t; d.granule = 16; d.n_classes = ncls; d.residue_class = cls;
+        d.variant = variant; d.split_k = 1; d.umma_m = 128; d.umma_n_full = t;
+        d.umma_n_tail = r ? g.n_tail : 0; d.k = k; d.r = r;
+        d.grid[0] = g.tiles_m; d.grid[1] = g.tiles_n; d.grid[2] = p.batch;
+        d.cluster[0] = d.cluster[1] = d.cluster[2] = 1;
+        *p.rec = d;
+    }
+}
+
 template <int EPI>
 __device__ __forceinline__ float epi_math(float acc, float alpha, float bias_i) {
     if constexpr (EPI == 0) return acc * alpha;
@@ -95,7 +121,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
                      const UmmaParams p) {
     using OutT = typename std::conditional<OUT_F32, float, __nv_bfloat16>::type;
-    const Geo g = make_geo<SM, SN, SK>(p);
+    Geo g = make_geo<SM, SN, SK>(p);
+    const bool devm = p.m_dev != nullptr;          // extent on the device (dense_dyn_dev)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the 128-B swizzle atoms.  Offset the __shared__ array itself (no
     // integer round trip) so every derived pointer stays in the shared address space (STS/LDS,
@@ -118,10 +145,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *res_bar = tempty + 2;
     uint64_t *recv_bar = res_bar + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(recv_bar + 1);
+    uint8_t *smap = reinterpret_cast<uint8_t *>(full_bar) + 512;   // devm: 128-B output map being patched
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
-    const int total_tiles = g.tiles_m * g.tiles_n * p.batch;
+    int total_tiles = g.tiles_m * g.tiles_n * p.batch;   // devm: the M_max bound until M is read
     // PAIR: a cluster of 2 CTAs shares every 256-row tile (cta_group::2), rank r owns rows 128r..
     const uint32_t prank = PAIR ? ptx::cluster_ctarank() : 0u;
     constexpr int kRowsPerTile = PAIR ? 256 : 128;
@@ -175,6 +203,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         bool first = true;
+        // devm: the first tile (t_first < tiles_m) exists for every M >= 1, so its weights can
+        // still be requested before the wait; otherwise wait and read M first.
+        bool devm_pending = devm;
+        if (devm && !(p.a_static && t_first < g.tiles_m)) {
+            ptx::pdl_wait();
+            devm_geometry(p, g, total_tiles, blockIdx.x == 0);
+            devm_pending = false;
+        }
         for (int t = t_first; t < total_tiles; t += t_step) {
             const TileCoord c = tile_of(g, t);
             const int n_this_p = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
@@ -214,6 +250,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (p.a_static) load_a(s, kb0 + s);
                 }
                 ptx::pdl_wait();
+                if (devm_pending) {
+                    devm_geometry(p, g, total_tiles, blockIdx.x == 0);
+                    devm_pending = false;
+                }
                 for (int s = 0; s < npre; ++s) {
                     if (!p.a_static) load_a(s, kb0 + s);
                     load_b(s, kb0 + s);
@@ -233,6 +273,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1 && lane == 0 && (!PAIR || prank == 0)) {
         // ================= MMA issuer (single thread; the even CTA of a pair issues for both)
+        if (devm) {
+            ptx::pdl_wait();
+            devm_geometry(p, g, total_tiles, false);
+        }
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
@@ -273,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= kEpiWarp0) {
         // ================= epilogue warps
         ptx::pdl_wait();                                     // residual / output dependencies
+        if (devm) devm_geometry(p, g, total_tiles, false);
         const int ew = (int)warp - kEpiWarp0;
         const int quarter = (int)(warp & 3);
         const int half = ew >> 2;                            // column group 0..kEpiGroups-1
@@ -282,6 +327,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row_base = (int)prank * 128;
         int acc = 0;
         uint32_t acc_phase = 0, res_phase = 0;
+        // devm: stores must clip at the true M, so this CTA publishes a copy of the output map
+        // with the token extent (dim 1 of the dense output view) patched to M.
+        const CUtensorMap *om = &tmOut;
+        if (TRANS && devm && ew == 0 && t_first < total_tiles)
+            om = ptx::tmap_patch_extent<1>(&tmOut, smap, p.out_slot + blockIdx.x, (uint32_t)g.rows_b, lane);
         if (EPI == 3 && TRANS && !split && leader && t_first < total_tiles) {
             const TileCoord c = tile_of(g, t_first);
             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
@@ -335,8 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::fence_async_smem();
                     ptx::named_bar_sync(1, kEpiThreads);
                     if (leader) {
-                        if (p.out_batch_mid) ptx::tma_store_3d(&tmOut, stg, c.m * kRowsPerTile + row_base, c.b, j0);
-                        else ptx::tma_store_3d(&tmOut, stg, c.m * kRowsPerTile + row_base, j0, c.b);
+                        if (p.out_batch_mid) ptx::tma_store_3d(om, stg, c.m * kRowsPerTile + row_base, c.b, j0);
+                        else ptx::tma_store_3d(om, stg, c.m * kRowsPerTile + row_base, j0, c.b);
                         ptx::tma_store_commit_wait();                 // staging readable again
                         const int tn = t + t_step;
                         if (EPI == 3 && tn < total_tiles) {

@@ -65,6 +65,8 @@ _SIGS = {
     "nimble_get_variant_limit": [],
     "nimble_last_dispatch": [C.POINTER(Dispatch)],
     "nimble_dense_dyn": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, C.c_int, C.c_int, _vp],
+    "nimble_dense_dyn_dev": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, C.c_int, _vp,
+                             _vp],
     "nimble_dense_static": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, C.c_int, C.c_int, _vp],
     "nimble_bmm_dyn": [_vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
                        C.c_float, C.c_int, C.c_int, _vp],
@@ -228,6 +230,27 @@ def dense_dyn(x, W, bias, y, epi=EPI_BIAS, residual=None, M=None, stream=None):
                                  residual.stride(0) if residual is not None else 0, _ptr(y), y.stride(0),
                                  M, N, K, _dt(x), epi, _stream(stream)))
     return y
+
+
+def dense_dyn_dev(x, W, bias, y, M_dev, M_max=None, epi=EPI_BIAS, residual=None, record=None, stream=None):
+    """y[:M] = ep(x[:M] W^T + bias) (+ residual[:M]) with M = M_dev[0] read ON THE DEVICE (int32
+    tensor); buffers sized by the bound M_max (default x.shape[0]).  record: optional device
+    tensor of nimble_dispatch size (uint8) receiving the device-side dispatch decision."""
+    M_max = x.shape[0] if M_max is None else M_max
+    N, K = W.shape
+    _check(_lib.nimble_dense_dyn_dev(_ptr(x), x.stride(0), _ptr(W), W.stride(0), _ptr(bias), _ptr(residual),
+                                     residual.stride(0) if residual is not None else 0, _ptr(y), y.stride(0),
+                                     _ptr(M_dev), M_max, N, K, epi, _ptr(record), _stream(stream)))
+    return y
+
+
+DISPATCH_BYTES = C.sizeof(Dispatch)
+
+
+def dispatch_from_bytes(buf) -> dict:
+    """Decode a device dispatch record (uint8 tensor / bytes of nimble_dispatch) into a dict."""
+    raw = bytes(buf.cpu().numpy().tobytes()) if hasattr(buf, "cpu") else bytes(buf)
+    return Dispatch.from_buffer_copy(raw[:DISPATCH_BYTES]).as_dict()
 
 
 def dense_static(x, W, bias, y, epi=EPI_BIAS, residual=None, M=None, stream=None):

@@ -25,7 +25,7 @@ def test_exports_every_declared_symbol(nb):
     hdr = open(os.path.join(ROOT, "include", "nimble.h")).read()
     hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)          # drop comments
     declared = set(re.findall(r"\b(nimble_[a-z_0-9]+)\s*\(", hdr))
-    assert len(declared) == 26
+    assert len(declared) == 27
     for name in declared:
         assert hasattr(nb._lib, name), name
     assert set(nb.EXPORTED) <= declared | {"nimble_last_error", "nimble_version"}
@@ -93,6 +93,21 @@ def test_dispatch_tuned_schedule_bit_exact(nb, orc, tile_t, split_max):
         nb.set_dense_schedule(N, K, 0, 8)
     assert nb.get_dense_schedule(N, K) == (0, 8)
     assert nb.dispatch_dense(100, N, K, 1) == orc.dispatch_dense(100, N, K, 1)
+
+
+def test_dense_dyn_dev_validation(nb):
+    E = nb.NimbleError
+    L = nb._lib
+    # M_max >= 2048 is family 3: not available with a device extent
+    with pytest.raises(E) as ei:
+        nb._check(L.nimble_dense_dyn_dev(16, 1024, 16, 1024, 16, None, 0, 16, 1024, 16, 2048, 1024, 1024, 1, None, None))
+    assert ei.value.status == -7
+    with pytest.raises(E) as ei:     # NULL M_dev
+        nb._check(L.nimble_dense_dyn_dev(16, 1024, 16, 1024, 16, None, 0, 16, 1024, None, 100, 1024, 1024, 1, None, None))
+    assert ei.value.status == -1
+    with pytest.raises(E) as ei:     # K mismatch is impossible here; bad extent
+        nb._check(L.nimble_dense_dyn_dev(16, 1024, 16, 1024, 16, None, 0, 16, 1024, 16, 0, 1024, 1024, 1, None, None))
+    assert ei.value.status == -4
 
 
 def test_dense_schedule_validation(nb):
