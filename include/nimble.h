@@ -196,6 +196,16 @@ int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const void *B, i
 int nimble_attention_varlen(const void *qkv, int64_t ld_qkv, int64_t T, const int32_t *seq_off, int32_t R,
                             int32_t max_len, int32_t heads, int32_t head_dim, float scale, void *out,
                             int64_t ld_out, void *stream);
+/* nimble_attention_varlen_dev: the same op with the total token count on the device: T =
+ * seq_off[R] is read by the kernel (T_max, the caller's allocation bound, sizes the launch
+ * templates); each CTA re-encodes its Q/K and V tensor maps with extent T on the device, so
+ * key rows at and beyond T read as zeros exactly as with a host T.  Request lengths, the
+ * query-tile grid bound max_len and R keep their meaning; ceil(max_len/128) * heads * R must
+ * be <= 512 (else E_UNSUPPORTED).  Uses a library-owned ring of 64 slot blocks per device:
+ * at most 64 such launches in flight. */
+int nimble_attention_varlen_dev(const void *qkv, int64_t ld_qkv, int64_t T_max, const int32_t *seq_off, int32_t R,
+                                int32_t max_len, int32_t heads, int32_t head_dim, float scale, void *out,
+                                int64_t ld_out, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Row ops used around bmm_dyn in BERT (the paper is silent: DESIGN.md readings 8-10).
@@ -209,6 +219,12 @@ int nimble_softmax_rows(const float *S, int64_t ldS, int64_t strideS, void *P, i
                         int64_t strideP, int64_t batch, int64_t rows, int64_t L, void *stream);
 int nimble_layernorm(const void *X, int64_t ldx, const float *gamma, const float *beta, float eps,
                      void *Y, int64_t ldy, int64_t rows, int64_t d, void *stream);
+/* nimble_layernorm_dev: nimble_layernorm over rows [0, *rows_dev) where the row count is
+ * read on the device (device int32, 1 <= *rows_dev <= rows_max, else the kernel traps);
+ * the launch covers rows_max (the upper bound the caller allocated).  Rows at and beyond
+ * *rows_dev are untouched. */
+int nimble_layernorm_dev(const void *X, int64_t ldx, const float *gamma, const float *beta, float eps, void *Y,
+                         int64_t ldy, const int32_t *rows_dev, int64_t rows_max, int64_t d, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Fused dynamic-length LSTM layer (control flow as a device loop).

@@ -159,6 +159,41 @@ class BertPacked:
                          nb.BF16, nb.EPI_BIAS_RESIDUAL, stream)
         nb._check(nb._lib.nimble_layernorm(p["O"], d, w["g2"], w["be2"], 1e-12, out_ptr, d, T, d, stream))
 
+    def layer_dev(self, x_ptr, out_ptr, n_ptr, seq_off_ptr, R, max_len, li, stream):
+        """layer() with the token count read on the device (n_ptr -> int32 T; seq_off[R] = T):
+        the *_dev entry points dispatch on the device, so one captured graph serves every T."""
+        d, f, H, Tm = self.d, self.f, self.H, self.max_tokens
+        w, p = self._lp[li], self._p
+        nb.dense_dyn_dev_raw(x_ptr, d, w["Wqkv"], d, w["bqkv"], None, 0, p["qkv"], 3 * d, n_ptr, Tm, 3 * d, d,
+                             nb.EPI_BIAS, stream)
+        nb._check(nb._lib.nimble_attention_varlen_dev(p["qkv"], 3 * d, Tm, seq_off_ptr, R, max_len, H, self.dh,
+                                                      1.0 / float(self.dh) ** 0.5, p["ctx"], d, stream))
+        nb.dense_dyn_dev_raw(p["ctx"], d, w["Wo"], d, w["bo"], x_ptr, d, p["A"], d, n_ptr, Tm, d, d,
+                             nb.EPI_BIAS_RESIDUAL, stream)
+        nb._check(nb._lib.nimble_layernorm_dev(p["A"], d, w["g1"], w["be1"], 1e-12, p["H1"], d, n_ptr, Tm, d, stream))
+        nb.dense_dyn_dev_raw(p["H1"], d, w["W1"], d, w["b1"], None, 0, p["F"], f, n_ptr, Tm, f, d,
+                             nb.EPI_BIAS_GELU, stream)
+        nb.dense_dyn_dev_raw(p["F"], f, w["W2"], f, w["b2"], p["H1"], d, p["O"], d, n_ptr, Tm, d, f,
+                             nb.EPI_BIAS_RESIDUAL, stream)
+        nb._check(nb._lib.nimble_layernorm_dev(p["O"], d, w["g2"], w["be2"], 1e-12, out_ptr, d, n_ptr, Tm, d, stream))
+
+    def forward_dev(self, x: torch.Tensor, seq_off: torch.Tensor, max_len: int | None = None,
+                    stream: int | None = None) -> torch.Tensor:
+        """forward() with the token count T = seq_off[R] living on the device (NEXT-4): no host
+        value of T is needed, so the launch sequence is capturable once for every T <= max_tokens
+        (max_tokens < 2048).  Returns the full [max_tokens x d] output buffer; rows < T are valid."""
+        R = seq_off.shape[0] - 1
+        max_len = self.max_tokens if max_len is None else max_len
+        s = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        src = x.data_ptr()
+        so = seq_off.data_ptr()
+        n_ptr = so + 4 * R
+        for li in range(len(self.layers)):
+            dst = self.X[li & 1].data_ptr()
+            self.layer_dev(src, dst, n_ptr, so, R, max_len, li, s)
+            src = dst
+        return self.X[(len(self.layers) - 1) & 1]
+
     def forward(self, x: torch.Tensor, seq_off: torch.Tensor, max_len: int, T: int | None = None,
                 stream: int | None = None) -> torch.Tensor:
         """x [>=T x d] bf16 (packed requests), seq_off device int32 [R+1]; returns [T x d] view."""

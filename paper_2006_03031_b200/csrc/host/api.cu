@@ -277,23 +277,28 @@ namespace {
 // block i % kSlotRing, so a kernel never patches a slot an in-flight neighbour still reads
 // (PDL overlaps adjacent kernels only).  One ring per device, allocated on first use.
 constexpr int kSlotRing = 64;
-std::mutex g_slot_mu;
-CUtensorMap *g_slots[64] = {};
-std::atomic<uint32_t> g_slot_seq{0};
+struct SlotRing {
+    int per_launch;                       // maps per launch block
+    std::mutex mu;
+    CUtensorMap *buf[64] = {};            // per device
+    std::atomic<uint32_t> seq{0};
+};
+SlotRing g_gemm_slots{kNumSMs};           // one output map per persistent CTA
+SlotRing g_attn_slots{2 * 512};           // Q/K and V maps per CTA, <= 512 CTAs
 
-cudaError_t next_slot_block(CUtensorMap **out) {
+cudaError_t next_slot_block(SlotRing &ring, CUtensorMap **out) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     {
-        std::lock_guard<std::mutex> lk(g_slot_mu);
-        if (!g_slots[dev]) {
-            e = cudaMalloc(&g_slots[dev], sizeof(CUtensorMap) * (size_t)kSlotRing * kNumSMs);
+        std::lock_guard<std::mutex> lk(ring.mu);
+        if (!ring.buf[dev]) {
+            e = cudaMalloc(&ring.buf[dev], sizeof(CUtensorMap) * (size_t)kSlotRing * ring.per_launch);
             if (e != cudaSuccess) return e;
         }
     }
-    *out = g_slots[dev] + (size_t)(g_slot_seq.fetch_add(1) % kSlotRing) * kNumSMs;
+    *out = ring.buf[dev] + (size_t)(ring.seq.fetch_add(1) % kSlotRing) * ring.per_launch;
     return cudaSuccess;
 }
 }  // namespace
@@ -352,7 +357,7 @@ extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, i
     } else {
         L.tmRes = L.tmOut;
     }
-    cudaError_t e = next_slot_block(&L.p.out_slot);
+    cudaError_t e = next_slot_block(g_gemm_slots, &L.p.out_slot);
     if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn_dev slot ring", e);
     plan_pipeline(L, d);
     L.stream = static_cast<cudaStream_t>(stream);
@@ -436,9 +441,9 @@ extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const
 }
 
 // ------------------------------------------------------------------ varlen attention
-extern "C" int nimble_attention_varlen(const void *qkv, int64_t ld_qkv, int64_t T, const int32_t *seq_off, int32_t R,
+static int attention_impl(const void *qkv, int64_t ld_qkv, int64_t T, const int32_t *seq_off, int32_t R,
                                        int32_t max_len, int32_t heads, int32_t head_dim, float scale, void *out,
-                                       int64_t ld_out, void *stream) {
+                                       int64_t ld_out, void *stream, bool dev) {
     if (!qkv || !seq_off || !out) return fail(NIMBLE_E_NULL, "nimble_attention_varlen: NULL pointer");
     if (!ext_ok(T) || R < 1 || max_len < 1 || heads < 1 || head_dim < 1)
         return fail(NIMBLE_E_EXTENT, "nimble_attention_varlen: extents must be >= 1");
@@ -464,11 +469,30 @@ extern "C" int nimble_attention_varlen(const void *qkv, int64_t ld_qkv, int64_t 
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(NIMBLE_E_CUDA, "cuTensorMapEncodeTiled(attention) failed (code " + std::to_string((int)r) + ")");
+    CUtensorMap *slots = nullptr;
+    if (dev) {
+        if ((int64_t)((max_len + 127) / 128) * heads * R > 512)
+            return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen_dev: more than 512 CTAs (query tiles x heads x R)");
+        e = next_slot_block(g_attn_slots, &slots);
+        if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen_dev slot ring", e);
+    }
     e = launch_attention_varlen(tmQK, tmV, seq_off, R, max_len, heads, scale, static_cast<__nv_bfloat16 *>(out), ld_out,
-                                static_cast<cudaStream_t>(stream));
+                                static_cast<cudaStream_t>(stream), slots);
     if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen launch", e);
     clear_error();
     return NIMBLE_OK;
+}
+
+extern "C" int nimble_attention_varlen(const void *qkv, int64_t ld_qkv, int64_t T, const int32_t *seq_off, int32_t R,
+                                       int32_t max_len, int32_t heads, int32_t head_dim, float scale, void *out,
+                                       int64_t ld_out, void *stream) {
+    return attention_impl(qkv, ld_qkv, T, seq_off, R, max_len, heads, head_dim, scale, out, ld_out, stream, false);
+}
+
+extern "C" int nimble_attention_varlen_dev(const void *qkv, int64_t ld_qkv, int64_t T_max, const int32_t *seq_off,
+                                           int32_t R, int32_t max_len, int32_t heads, int32_t head_dim, float scale,
+                                           void *out, int64_t ld_out, void *stream) {
+    return attention_impl(qkv, ld_qkv, T_max, seq_off, R, max_len, heads, head_dim, scale, out, ld_out, stream, true);
 }
 
 // ------------------------------------------------------------------ row ops
@@ -495,6 +519,22 @@ extern "C" int nimble_layernorm(const void *X, int64_t ldx, const float *gamma, 
     cudaError_t e = launch_layernorm(static_cast<const __nv_bfloat16 *>(X), ldx, gamma, beta, eps,
                                      static_cast<__nv_bfloat16 *>(Y), ldy, rows, d, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail("nimble_layernorm launch", e);
+    clear_error();
+    return NIMBLE_OK;
+}
+
+extern "C" int nimble_layernorm_dev(const void *X, int64_t ldx, const float *gamma, const float *beta, float eps,
+                                    void *Y, int64_t ldy, const int32_t *rows_dev, int64_t rows_max, int64_t d,
+                                    void *stream) {
+    if (!X || !gamma || !beta || !Y || !rows_dev) return fail(NIMBLE_E_NULL, "nimble_layernorm_dev: NULL pointer");
+    if (!ext_ok(rows_max) || !ext_ok(d)) return fail(NIMBLE_E_EXTENT, "nimble_layernorm_dev: extents must be >= 1");
+    if (d > 4096) return fail(NIMBLE_E_UNSUPPORTED, "nimble_layernorm_dev: d > 4096 not built");
+    if (d % 8 || ldx % 8 || ldy % 8 || !aligned16(X) || !aligned16(Y) || !aligned16(gamma) || !aligned16(beta))
+        return fail(NIMBLE_E_ALIGN, "nimble_layernorm_dev: d, ldx, ldy multiples of 8; X, Y, gamma, beta 16-B aligned");
+    cudaError_t e = launch_layernorm(static_cast<const __nv_bfloat16 *>(X), ldx, gamma, beta, eps,
+                                     static_cast<__nv_bfloat16 *>(Y), ldy, rows_max, d,
+                                     static_cast<cudaStream_t>(stream), rows_dev);
+    if (e != cudaSuccess) return cuda_fail("nimble_layernorm_dev launch", e);
     clear_error();
     return NIMBLE_OK;
 }

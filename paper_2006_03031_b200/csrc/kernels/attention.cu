@@ -29,7 +29,7 @@ constexpr int kSoftmaxThreads = 256;     // warps 0-7
 constexpr int kThreads = kSoftmaxThreads + 32;   // + warp 8: lane 0 TMA producer, lane 1 MMA issuer
 constexpr int kTile = 128 * 64 * 2;       // Q tile / K block / V block (128 keys) / P half: 16 KiB
 constexpr int kVBox = 64 * 64 * 2;        // one V TMA box (64 keys): 8 KiB
-constexpr int kSmemBytes = 1024 + 6 * kTile + 2048 + 256;   // ~99 KB: two CTAs per SM
+constexpr int kSmemBytes = 1024 + 6 * kTile + 2048 + 512;   // ~99 KB: two CTAs per SM
 
 struct AttnParams {
     const int32_t *seq_off;   // [R + 1] prefix sums of request lengths (device)
@@ -37,6 +37,7 @@ struct AttnParams {
     float scale_log2;         // scale * log2(e)
     __nv_bfloat16 *out;
     int64_t ld_out;
+    CUtensorMap *map_slots;   // device token count: 2 per-CTA slots for the extent-patched maps
 };
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 2, *v_full = bar + 3, *v_empty = bar + 5,
              *s_full = bar + 7, *s_used = bar + 8, *p_ready = bar + 9, *pv_done = bar + 10;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 11);
+    uint8_t *smaps = reinterpret_cast<uint8_t *>(bar) + 256;            // 2 x 128-B maps being patched
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
 
     if (threadIdx.x == 0) {
@@ -100,20 +102,31 @@ __global__ void __launch_bounds__(kThreads, 2)
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;             // S: cols [0,128), O: cols [128,192)
 
+    // device token count (nimble_attention_varlen_dev): T = seq_off[R] is data, so this CTA
+    // publishes copies of both maps with the token extent patched to T (rows past T then
+    // zero-fill exactly as with a host-encoded T).
+    const CUtensorMap *mQK = &tmQK, *mV = &tmV;
+    if (p.map_slots && warp == 8) {
+        const uint32_t T = (uint32_t)__ldg(p.seq_off + gridDim.z);
+        CUtensorMap *slot = p.map_slots + 2 * (size_t)((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+        mQK = ptx::tmap_patch_extent<2>(&tmQK, smaps, slot, T, lane);
+        mV = ptx::tmap_patch_extent<2>(&tmV, smaps + 128, slot + 1, T, lane);
+    }
+
     if (warp == 8) {
       if (lane == 0) {
         // ---------------- producer: Q once, then K_j / V_j through a 2-stage ring
         ptx::mbar_arrive_expect_tx(q_full, kTile);
-        ptx::tma_load_3d(sQ, &tmQK, q_full, 0, h, o + q0);
+        ptx::tma_load_3d(sQ, mQK, q_full, 0, h, o + q0);
         for (int j = 0; j < nk; ++j) {
             const int st = j & 1, use = j >> 1;
             if (j > 0) ptx::mbar_wait(k_empty, (j - 1) & 1);          // S_{j-1} has read K
             ptx::mbar_arrive_expect_tx(k_full, kTile);
-            ptx::tma_load_3d(sK, &tmQK, k_full, 0, p.heads + h, o + j * 128);
+            ptx::tma_load_3d(sK, mQK, k_full, 0, p.heads + h, o + j * 128);
             if (use > 0) ptx::mbar_wait(&v_empty[st], (use - 1) & 1); // PV_{j-2} has read V
             ptx::mbar_arrive_expect_tx(&v_full[st], kTile);
-            ptx::tma_load_3d(sV + st * kTile, &tmV, &v_full[st], 0, 2 * p.heads + h, o + j * 128);
-            ptx::tma_load_3d(sV + st * kTile + kVBox, &tmV, &v_full[st], 0, 2 * p.heads + h, o + j * 128 + 64);
+            ptx::tma_load_3d(sV + st * kTile, mV, &v_full[st], 0, 2 * p.heads + h, o + j * 128);
+            ptx::tma_load_3d(sV + st * kTile + kVBox, mV, &v_full[st], 0, 2 * p.heads + h, o + j * 128 + 64);
         }
       } else if (lane == 1) {
         // ---------------- MMA issuer
@@ -280,7 +293,7 @@ size_t attention_smem_bytes(int max_len) {
 
 cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const int32_t *seq_off,
                                     int R, int max_len, int heads, float scale, __nv_bfloat16 *out, int64_t ld_out,
-                                    cudaStream_t s) {
+                                    cudaStream_t s, CUtensorMap *map_slots) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(attention_varlen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -294,6 +307,7 @@ cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &
     p.scale_log2 = scale * 1.4426950408889634f;
     p.out = out;
     p.ld_out = ld_out;
+    p.map_slots = map_slots;
     const dim3 grid((unsigned)((max_len + 127) / 128), (unsigned)heads, (unsigned)R);
     return launch_pdl(attention_varlen_kernel, grid, dim3(kThreads), attention_smem_bytes(max_len), s, tmQK, tmV, p);
 }

@@ -99,12 +99,13 @@ cudaError_t launch_simt8_static(const Simt8Params &p, dim3 grid, cudaStream_t s)
 size_t attention_smem_bytes(int max_len);
 cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const int32_t *seq_off,
                                     int R, int max_len, int heads, float scale, __nv_bfloat16 *out, int64_t ld_out,
-                                    cudaStream_t s);
+                                    cudaStream_t s, CUtensorMap *map_slots = nullptr);
 
 cudaError_t launch_softmax_rows(const float *S, int64_t ldS, int64_t strideS, __nv_bfloat16 *P, int64_t ldP,
                                 int64_t strideP, int64_t batch, int64_t rows, int64_t L, cudaStream_t s);
 cudaError_t launch_layernorm(const __nv_bfloat16 *X, int64_t ldx, const float *g, const float *b, float eps,
-                             __nv_bfloat16 *Y, int64_t ldy, int64_t rows, int64_t d, cudaStream_t s);
+                             __nv_bfloat16 *Y, int64_t ldy, int64_t rows, int64_t d, cudaStream_t s,
+                             const int32_t *rows_dev = nullptr);
 
 size_t lstm_workspace_bytes(int64_t H);
 cudaError_t launch_lstm_seq(const float *G, int64_t ldg, const float *W_hh, int64_t ldw, const float *h0,

@@ -66,9 +66,14 @@ template <int CH>
 __global__ void __launch_bounds__(256) layernorm_warp_kernel(const __nv_bfloat16 *__restrict__ X, int64_t ldx,
                                                              const float *__restrict__ g, const float *__restrict__ be,
                                                              float eps, __nv_bfloat16 *__restrict__ Y, int64_t ldy,
-                                                             int64_t rows, int d) {
+                                                             int64_t rows, int d, const int32_t *__restrict__ rows_dev) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
+    if (rows_dev) {                      // device extent: the grid covers the bound `rows`
+        const int32_t r = *rows_dev;
+        if (r < 1 || r > rows) __trap();
+        rows = r;
+    }
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (row >= rows) return;
     const int lane = threadIdx.x & 31;
@@ -139,12 +144,15 @@ cudaError_t launch_softmax_rows(const float *S, int64_t ldS, int64_t strideS, __
 }
 
 cudaError_t launch_layernorm(const __nv_bfloat16 *X, int64_t ldx, const float *g, const float *b, float eps,
-                             __nv_bfloat16 *Y, int64_t ldy, int64_t rows, int64_t d, cudaStream_t s) {
+                             __nv_bfloat16 *Y, int64_t ldy, int64_t rows, int64_t d, cudaStream_t s,
+                             const int32_t *rows_dev) {
     if (d > 4096 || d % 8) return cudaErrorInvalidValue;
     const dim3 grid((unsigned)((rows + 7) / 8)), block(256);
-    if (d <= 1024) return launch_pdl(layernorm_warp_kernel<4>, grid, block, 0, s, X, ldx, g, b, eps, Y, ldy, rows, (int)d);
-    if (d <= 2048) return launch_pdl(layernorm_warp_kernel<8>, grid, block, 0, s, X, ldx, g, b, eps, Y, ldy, rows, (int)d);
-    return launch_pdl(layernorm_warp_kernel<16>, grid, block, 0, s, X, ldx, g, b, eps, Y, ldy, rows, (int)d);
+    if (d <= 1024)
+        return launch_pdl(layernorm_warp_kernel<4>, grid, block, 0, s, X, ldx, g, b, eps, Y, ldy, rows, (int)d, rows_dev);
+    if (d <= 2048)
+        return launch_pdl(layernorm_warp_kernel<8>, grid, block, 0, s, X, ldx, g, b, eps, Y, ldy, rows, (int)d, rows_dev);
+    return launch_pdl(layernorm_warp_kernel<16>, grid, block, 0, s, X, ldx, g, b, eps, Y, ldy, rows, (int)d, rows_dev);
 }
 
 }  // namespace nimble

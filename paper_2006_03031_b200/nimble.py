@@ -80,6 +80,9 @@ _SIGS = {
     "nimble_partition_lpt": [_i64p, _i64, C.c_int32, _i32p],
     "nimble_debug_trace": [_vp],
     "nimble_lstm2_seq": [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp],
+    "nimble_layernorm_dev": [_vp, _i64, _vp, _vp, C.c_float, _vp, _i64, _vp, _i64, _i64, _vp],
+    "nimble_attention_varlen_dev": [_vp, _i64, _i64, _vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, _vp,
+                                    _i64, _vp],
     "nimble_attention_varlen": [_vp, _i64, _i64, _vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, _vp,
                                 _i64, _vp],
 }
@@ -263,6 +266,11 @@ def dense_static(x, W, bias, y, epi=EPI_BIAS, residual=None, M=None, stream=None
     return y
 
 
+def dense_dyn_dev_raw(x_ptr, ldx, W_ptr, ldw, bias_ptr, res_ptr, ldr, y_ptr, ldy, m_ptr, M_max, N, K, epi, stream):
+    _check(_lib.nimble_dense_dyn_dev(x_ptr, ldx, W_ptr, ldw, bias_ptr, res_ptr, ldr, y_ptr, ldy, m_ptr, M_max, N, K,
+                                     epi, None, stream))
+
+
 def dense_dyn_raw(x_ptr, ldx, W_ptr, ldw, bias_ptr, res_ptr, ldr, y_ptr, ldy, M, N, K, dt, epi, stream):
     _check(_lib.nimble_dense_dyn(x_ptr, ldx, W_ptr, ldw, bias_ptr, res_ptr, ldr, y_ptr, ldy, M, N, K, dt, epi,
                                  stream))
@@ -298,6 +306,23 @@ def softmax_rows(S, ldS, strideS, P, ldP, strideP, batch, rows, L, stream=None):
     s = S if isinstance(S, int) else _ptr(S)
     p = P if isinstance(P, int) else _ptr(P)
     _check(_lib.nimble_softmax_rows(s, ldS, strideS, p, ldP, strideP, batch, rows, L, _stream(stream)))
+
+
+def layernorm_dev(X, gamma, beta, Y, rows_dev, rows_max=None, eps=1e-12, stream=None):
+    """LayerNorm over rows [0, rows_dev[0]) with the row count read on the device."""
+    rows_max = X.shape[0] if rows_max is None else rows_max
+    _check(_lib.nimble_layernorm_dev(_ptr(X), X.stride(0), _ptr(gamma), _ptr(beta), float(eps), _ptr(Y), Y.stride(0),
+                                     _ptr(rows_dev), rows_max, X.shape[1], _stream(stream)))
+    return Y
+
+
+def attention_varlen_dev(qkv, seq_off, R, max_len, heads, out, T_max=None, scale=None, head_dim=64, stream=None):
+    """attention_varlen with the token count T = seq_off[R] read on the device."""
+    T_max = qkv.shape[0] if T_max is None else T_max
+    scale = head_dim ** -0.5 if scale is None else scale
+    _check(_lib.nimble_attention_varlen_dev(_ptr(qkv), qkv.stride(0), T_max, _ptr(seq_off), R, max_len, heads,
+                                            head_dim, float(scale), _ptr(out), out.stride(0), _stream(stream)))
+    return out
 
 
 def layernorm(X, gamma, beta, Y, eps=1e-12, rows=None, stream=None):

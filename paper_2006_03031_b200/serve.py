@@ -76,6 +76,44 @@ class GraphCache:
         out_row.copy_(self.cls, non_blocking=True)
 
 
+class DeviceExtentGraph:
+    """ONE CUDA graph of the one-request packed forward whose token count lives on the device
+    (BertPacked.forward_dev: device-side dispatch, extent-patched tensor maps; SURVEY §8 f4 /
+    PAPER.md:268-271, 709-710).  It replays for every L <= max_tokens (< 2048): no per-L
+    capture, no per-L graph memory.  Same interface as GraphCache."""
+
+    def __init__(self, encoder, device="cuda"):
+        assert hasattr(encoder, "forward_dev") and encoder.max_tokens < 2048
+        self.enc = encoder
+        Tm = encoder.max_tokens
+        self.xin = torch.zeros((Tm, encoder.d), dtype=torch.bfloat16, device=device)
+        self.cls = torch.zeros((encoder.d,), dtype=torch.bfloat16, device=device)
+        self.seq_off = torch.tensor([0, Tm], dtype=torch.int32, device=device)
+        self.stream = torch.cuda.Stream(device=device)
+        self.graph = torch.cuda.CUDAGraph()
+        s = self.stream
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            encoder.forward_dev(self.xin, self.seq_off)          # warm outside capture
+            with torch.cuda.graph(self.graph, stream=s):
+                y = encoder.forward_dev(self.xin, self.seq_off)
+                self.cls.copy_(y[0])
+        torch.cuda.current_stream().wait_stream(s)
+
+    def capture(self, L: int):             # nothing to do: one graph serves every L
+        assert 1 <= L <= self.enc.max_tokens
+
+    def capture_all(self, lengths):
+        for L in lengths:
+            self.capture(int(L))
+
+    def run(self, x: torch.Tensor, L: int, out_row: torch.Tensor):
+        self.xin[:L].copy_(x, non_blocking=True)
+        self.seq_off[1:].fill_(L)          # the extent, written on the stream (no host sync)
+        self.graph.replay()
+        out_row.copy_(self.cls, non_blocking=True)
+
+
 def run_requests(cache: GraphCache, ids, lens, X_all: torch.Tensor, offsets, out: torch.Tensor):
     """Run whole requests (batch 1 each) in id order; out[i] = [CLS] of request ids[i]."""
     for i, rid in enumerate(ids):

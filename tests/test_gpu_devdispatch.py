@@ -123,3 +123,81 @@ def test_dense_dyn_dev_variant_limit_and_tuned_tile(nb, orc):
         finally:
             nb.set_variant_limit(0)
             nb.set_dense_schedule(N, K, 0, 8)
+
+
+def test_layernorm_dev_vs_oracle(nb, orc):
+    d, R_max = 1024, 300
+    X = synth.normal((R_max, d), 1.0, 71)
+    g = (1.0 + synth.normal((d,), 0.02, 72, torch.float32))
+    be = synth.normal((d,), 0.02, 73, torch.float32)
+    for rows in (1, 7, 8, 9, 299, 300):
+        Y = torch.full((R_max, d), float(POISON), dtype=torch.bfloat16, device="cuda")
+        nb.layernorm_dev(X.cuda(), g.cuda(), be.cuda(), Y, torch.tensor([rows], dtype=torch.int32, device="cuda"))
+        torch.cuda.synchronize()
+        ref = orc.layernorm(X[:rows].double().numpy(), g.double().numpy(), be.double().numpy())
+        ref = ref[0] if isinstance(ref, tuple) else ref
+        assert float(np.max(np.abs(Y[:rows].double().cpu().numpy() - ref) / np.maximum(np.abs(ref), 1))) <= 2e-2
+        assert bool((Y[rows:] == POISON.cuda()).all())
+
+
+def test_attention_dev_patched_maps_zero_fill_bitwise(nb):
+    """T = seq_off[R] on the device: rows in [T, T_max) hold NaN, yet the result equals the
+    host-T launch bit for bit (the re-encoded maps zero-fill past T exactly like host maps)."""
+    H, dh, T_max = 16, 64, 640
+    for lens in ([1], [77], [128], [129, 5], [300, 200, 100], [512]):
+        T = sum(lens)
+        qkv = synth.normal((T_max, 3 * H * dh), 1.0, 80 + T).cuda()
+        qkv[T:] = float("nan")
+        off = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
+        R, mx = len(lens), max(lens)
+        ref = torch.zeros((T_max, H * dh), dtype=torch.bfloat16, device="cuda")
+        nb.attention_varlen(qkv[:T].contiguous(), off, R, mx, H, ref, T=T)
+        got = torch.zeros((T_max, H * dh), dtype=torch.bfloat16, device="cuda")
+        nb.attention_varlen_dev(qkv, off, R, 512, H, got, T_max=T_max)
+        torch.cuda.synchronize()
+        assert torch.equal(got[:T], ref[:T]), lens
+        assert bool((got[T:] == 0).all())
+
+
+def _bert_large_2layers(nb):
+    from paper_2006_03031_b200.bert import BertPacked
+    cfg = dict(synth.BERT_LARGE)
+    cfg["layers"] = 2
+    w = synth.bert_weights_device(cfg, seed=0)
+    return cfg, w, BertPacked
+
+
+def test_bert_forward_dev_and_one_graph_bitwise(nb):
+    """forward_dev (device T) == forward (host T) bit for bit once the host path also runs the
+    split-1 schedule; and ONE captured DeviceExtentGraph reproduces per-L graph results."""
+    from paper_2006_03031_b200.serve import DeviceExtentGraph, GraphCache
+    cfg, w, BertPacked = _bert_large_2layers(nb)
+    d, f = cfg["d"], cfg["ffn"]
+    shapes = [(3 * d, d), (d, d), (f, d), (d, f)]
+    for N, K in shapes:
+        nb.set_dense_schedule(N, K, 128, 1)
+    try:
+        enc_h = BertPacked(cfg, w, max_tokens=512)
+        enc_d = BertPacked(cfg, w, max_tokens=512)
+        one = DeviceExtentGraph(enc_d)
+        per_l = GraphCache(enc_h)
+        out_a = torch.empty((d,), dtype=torch.bfloat16, device="cuda")
+        out_b = torch.empty((d,), dtype=torch.bfloat16, device="cuda")
+        for L in (1, 17, 128, 129, 300, 512, 3):
+            x = synth.device_normal(L, d, seed=900 + L)
+            off = torch.tensor([0, L], dtype=torch.int32, device="cuda")
+            y_h = enc_h.forward(x, off, L, T=L).clone()
+            xin = torch.zeros((512, d), dtype=torch.bfloat16, device="cuda")
+            xin[:L] = x
+            y_d = enc_d.forward_dev(xin, off.clone())
+            torch.cuda.synchronize()
+            assert torch.equal(y_h[:L], y_d[:L]), L
+            per_l.capture(L)
+            per_l.run(x, L, out_a)
+            one.run(x, L, out_b)
+            torch.cuda.synchronize()
+            assert torch.equal(out_a, out_b), L
+            assert torch.equal(out_b, y_h[0]), L
+    finally:
+        for N, K in shapes:
+            nb.set_dense_schedule(N, K, 0, 8)
