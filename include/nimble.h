@@ -189,8 +189,10 @@ int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const void *B, i
  * qkv [T x ld_qkv] bf16 with row blocks Q | K | V of width heads*head_dim (BERT's
  * fused QKV projection output); out [T x ld_out] bf16, head h in columns
  * [h*head_dim, (h+1)*head_dim).  seq_off: DEVICE int32 [R+1], seq_off[0] = 0,
- * nondecreasing, seq_off[R] = T.  max_len >= every L_i.  One launch; S and P stay
- * on chip (TMEM / smem).  head_dim must be 64 and max_len <= 512 (E_UNSUPPORTED
+ * nondecreasing, seq_off[R] = T.  max_len >= every L_i.  One persistent launch (at
+ * most 2 CTAs per SM walking a longest-request-first work list of (query tile, head,
+ * request) items built on the device from seq_off); S and P stay on chip (TMEM /
+ * smem).  head_dim must be 64, max_len <= 8192 and R <= 1024 (E_UNSUPPORTED
  * otherwise); qkv/out 16-byte aligned with ld*2 % 16 == 0 (E_ALIGN).
  * ------------------------------------------------------------------------- */
 int nimble_attention_varlen(const void *qkv, int64_t ld_qkv, int64_t T, const int32_t *seq_off, int32_t R,
@@ -200,9 +202,8 @@ int nimble_attention_varlen(const void *qkv, int64_t ld_qkv, int64_t T, const in
  * seq_off[R] is read by the kernel (T_max, the caller's allocation bound, sizes the launch
  * templates); each CTA re-encodes its Q/K and V tensor maps with extent T on the device, so
  * key rows at and beyond T read as zeros exactly as with a host T.  Request lengths, the
- * query-tile grid bound max_len and R keep their meaning; ceil(max_len/128) * heads * R must
- * be <= 512 (else E_UNSUPPORTED).  Uses a library-owned ring of 64 slot blocks per device:
- * at most 64 such launches in flight. */
+ * query-tile bound max_len and R keep their meaning.  Uses a library-owned ring of 64 slot
+ * blocks per device: at most 64 such launches in flight. */
 int nimble_attention_varlen_dev(const void *qkv, int64_t ld_qkv, int64_t T_max, const int32_t *seq_off, int32_t R,
                                 int32_t max_len, int32_t heads, int32_t head_dim, float scale, void *out,
                                 int64_t ld_out, void *stream);

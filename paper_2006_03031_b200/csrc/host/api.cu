@@ -284,7 +284,7 @@ struct SlotRing {
     std::atomic<uint32_t> seq{0};
 };
 SlotRing g_gemm_slots{kNumSMs};           // one output map per persistent CTA
-SlotRing g_attn_slots{2 * 512};           // Q/K and V maps per CTA, <= 512 CTAs
+SlotRing g_attn_slots{2 * 2 * kNumSMs};   // Q/K and V maps per persistent CTA (<= 2 per SM)
 
 cudaError_t next_slot_block(SlotRing &ring, CUtensorMap **out) {
     int dev = 0;
@@ -448,7 +448,10 @@ static int attention_impl(const void *qkv, int64_t ld_qkv, int64_t T, const int3
     if (!ext_ok(T) || R < 1 || max_len < 1 || heads < 1 || head_dim < 1)
         return fail(NIMBLE_E_EXTENT, "nimble_attention_varlen: extents must be >= 1");
     if (head_dim != 64) return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen: head_dim must be 64");
-    if (max_len > 512) return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen: max_len > 512 not built");
+    if (max_len > 8192) return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen: max_len > 8192 not built");
+    if (R > attention_max_requests())
+        return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen: more than " + std::to_string(attention_max_requests()) +
+                                              " requests in one launch");
     if (ld_qkv < 3LL * heads * head_dim || ld_out < (int64_t)heads * head_dim)
         return fail(NIMBLE_E_SHAPE, "nimble_attention_varlen: leading dimension too small");
     if (!aligned16(qkv) || !aligned16(out) || (ld_qkv * 2) % 16 || (ld_out * 2) % 16)
@@ -471,13 +474,11 @@ static int attention_impl(const void *qkv, int64_t ld_qkv, int64_t T, const int3
     if (r != CUDA_SUCCESS) return fail(NIMBLE_E_CUDA, "cuTensorMapEncodeTiled(attention) failed (code " + std::to_string((int)r) + ")");
     CUtensorMap *slots = nullptr;
     if (dev) {
-        if ((int64_t)((max_len + 127) / 128) * heads * R > 512)
-            return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen_dev: more than 512 CTAs (query tiles x heads x R)");
         e = next_slot_block(g_attn_slots, &slots);
         if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen_dev slot ring", e);
     }
     e = launch_attention_varlen(tmQK, tmV, seq_off, R, max_len, heads, scale, static_cast<__nv_bfloat16 *>(out), ld_out,
-                                static_cast<cudaStream_t>(stream), slots);
+                                static_cast<cudaStream_t>(stream), slots, g_trace);
     if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen launch", e);
     clear_error();
     return NIMBLE_OK;

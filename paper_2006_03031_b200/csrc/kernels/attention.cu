@@ -5,16 +5,23 @@
 // equal dynamic dims; P:575 BERT's dynamic sequence length).  It replaces the
 // bmm_dyn -> softmax_rows -> bmm_dyn triple and never writes S or P to HBM.
 //
-// CTA = (query tile of 128, head, request), 288 threads, online softmax over 128-key blocks:
+// Persistent: two CTAs per SM walk a shared list of work items (query tile of 128, head,
+// request).  Every CTA builds the same list from seq_off in its prologue — requests ordered
+// by key-block count, longest first (a stable counting sort), items of one (request, head)
+// adjacent so concurrently running CTAs share K/V in L2 — and takes items
+// blockIdx.x, blockIdx.x + gridDim.x, ...  The TMEM allocation, barrier setup and tensor-map
+// prefetch happen once per CTA, and the producer runs ahead into the next item (its Q and
+// first K/V blocks load while the current item finishes).
+// Per item, online softmax over 128-key blocks, 320 threads:
 //   warp 8 lane 0  TMA producer: Q tile, then per key block K_j [128 x 64] (single buffer) and
 //                  V_j (MN-major, two 64-key boxes, 2-stage ring).
-//   warp 8 lane 1  MMA issuer: S = Q K_j^T into TMEM cols [0,128) as soon as the previous S
+//   warp 9 lane 0  MMA issuer: S = Q K_j^T into TMEM cols [0,128) as soon as the previous S
 //                  has been read; O += P_j V_j into TMEM cols [128,192) once P_j is written.
 //   warps 0-7      softmax: row q = TMEM lane 32*(w%4)+lane, key half (w/4) of the block held
 //                  in registers; running max / sum; unnormalised P_j written as bf16 straight
 //                  into the UMMA K-major swizzled smem layout; O rescaled in TMEM when the
 //                  running max grows; epilogue O / rowsum -> bf16.
-// TMEM 256 columns and ~99 KB smem per CTA: two CTAs share an SM.  Keys >= L_i get P = 0;
+// TMEM 256 columns and ~107 KB smem per CTA: two CTAs share an SM.  Keys >= L_i get P = 0;
 // query rows >= L_i are computed but never stored.
 #include <cstdint>
 
@@ -26,18 +33,29 @@ namespace nimble {
 namespace {
 
 constexpr int kSoftmaxThreads = 256;     // warps 0-7
-constexpr int kThreads = kSoftmaxThreads + 32;   // + warp 8: lane 0 TMA producer, lane 1 MMA issuer
+// + warp 8 (lane 0: TMA producer) and warp 9 (lane 0: MMA issuer).  The two spin-waiting roles
+// must not share a warp: divergent lanes of one warp are scheduled one path at a time, so a
+// producer spinning on an mbarrier would delay the MMA issue (and vice versa) by microseconds.
+constexpr int kThreads = kSoftmaxThreads + 64;
 constexpr int kTile = 128 * 64 * 2;       // Q tile / K block / V block (128 keys) / P half: 16 KiB
 constexpr int kVBox = 64 * 64 * 2;        // one V TMA box (64 keys): 8 KiB
-constexpr int kSmemBytes = 1024 + 6 * kTile + 2048 + 512;   // ~99 KB: two CTAs per SM
+constexpr int kMaxReq = 1024;             // requests per launch (work-list arrays in smem)
+constexpr int kMaxQT = 64;                // query tiles per request (max_len <= 8192)
+constexpr int kRedBytes = 4 * 256 * 4;    // [2 parity][2 halves][128] row max + [2][128] row sums
+// rounded to 1 KiB: the barrier block after it holds the 128-B-aligned maps being patched
+constexpr int kListBytes = (2 * kMaxReq * 4 + kMaxReq * 2 + 2 * (kMaxQT + 1) * 4 + 1023) / 1024 * 1024;
+constexpr int kSmemBytes = 1024 + 6 * kTile + kRedBytes + kListBytes + 512;
+constexpr int kCtasPerSm = 2;
 
 struct AttnParams {
     const int32_t *seq_off;   // [R + 1] prefix sums of request lengths (device)
+    int32_t R;
     int32_t heads;
     float scale_log2;         // scale * log2(e)
     __nv_bfloat16 *out;
     int64_t ld_out;
     CUtensorMap *map_slots;   // device token count: 2 per-CTA slots for the extent-patched maps
+    unsigned long long *trace;   // debug (nimble_debug_trace): CTA 0 per-block clock64 stamps
 };
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
@@ -53,36 +71,97 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kThreads, 2)
+__device__ __forceinline__ int qtiles_of(const int32_t *seq_off, int r) {
+    const int L = __ldg(seq_off + r + 1) - __ldg(seq_off + r);
+    return (L + 127) / 128;
+}
+
+// The work list: requests ordered by query-tile count, descending (stable); per sorted position
+// i: so[i] = token offset, sl[i] = length, cum[i] = items of positions [0, i).  Item k -> the i
+// with cum[i] <= k < cum[i+1]; within a request, q-tile fastest.  Decoding touches shared memory
+// only: a dependent global load at an item boundary stalls every role for microseconds.
+struct Item {
+    int o, L, qt, h;
+};
+__device__ __forceinline__ Item decode_item(const int32_t *so, const int16_t *sl, const int32_t *cum, int R, int heads,
+                                            int k) {
+    int lo = 0, hi = R - 1;                        // largest i with cum[i] <= k
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cum[mid] <= k) lo = mid;
+        else hi = mid - 1;
+    }
+    Item it;
+    it.o = so[lo];
+    it.L = sl[lo];
+    const int nq = (it.L + 127) / 128;
+    const int rem = k - cum[lo];
+    it.qt = rem % nq;
+    it.h = rem / nq;
+    return it;
+}
+
+// This CTA's items k = blockIdx.x + n * gridDim.x.  Decoding is kept off the item boundary:
+// lookahead() decodes the item after next somewhere inside the current item (where the role
+// would be waiting anyway) and advance() only moves registers.  Shared-memory loads of the
+// single-thread roles queue behind the softmax warps' MUFU traffic in the MIO pipe, so a
+// decode at the boundary costs thousands of cycles.
+struct ItemIter {
+    const int32_t *so, *cum;
+    const int16_t *sl;
+    int R, H, n, k;
+    Item cur, nxt, nxt2;
+    __device__ __forceinline__ ItemIter(const int32_t *so_, const int16_t *sl_, const int32_t *cum_, int R_, int H_,
+                                        int n_)
+        : so(so_), cum(cum_), sl(sl_), R(R_), H(H_), n(n_), k((int)blockIdx.x) {
+        if (k < n) cur = decode_item(so, sl, cum, R, H, k);
+        if (k + (int)gridDim.x < n) nxt = decode_item(so, sl, cum, R, H, k + (int)gridDim.x);
+    }
+    __device__ __forceinline__ bool valid() const { return k < n; }
+    __device__ __forceinline__ bool has_next() const { return k + (int)gridDim.x < n; }
+    __device__ __forceinline__ void lookahead() {
+        if (k + 2 * (int)gridDim.x < n) nxt2 = decode_item(so, sl, cum, R, H, k + 2 * (int)gridDim.x);
+    }
+    __device__ __forceinline__ void advance() {
+        k += (int)gridDim.x;
+        cur = nxt;
+        nxt = nxt2;
+    }
+};
+
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     attention_varlen_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
                             const AttnParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int qt = blockIdx.x, h = blockIdx.y, req = blockIdx.z;
-    ptx::pdl_wait();                              // QKV comes from the previous kernel
-    ptx::pdl_trigger();
-    const int o = __ldg(p.seq_off + req);
-    const int L = __ldg(p.seq_off + req + 1) - o;
-    const int q0 = qt * 128;
-    if (q0 >= L) return;                          // request shorter than this query tile
-    const int nk = (L + 127) / 128;               // key blocks
     uint8_t *sQ = smem;
     uint8_t *sK = smem + kTile;                   // K block (single buffer: only the short S MMA reads it)
     uint8_t *sV = smem + 2 * kTile;               // [2] V blocks (two 64-key boxes each)
     uint8_t *sP = smem + 4 * kTile;               // P block: 2 x (64 keys) K-major atoms = 32 KiB
-    float *red = reinterpret_cast<float *>(smem + 6 * kTile);          // [2][128] row max
-    float *redl = red + 256;                                            // [2][128] row sums
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 6 * kTile + 2048);
-    uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 2, *v_full = bar + 3, *v_empty = bar + 5,
-             *s_full = bar + 7, *s_used = bar + 8, *p_ready = bar + 9, *pv_done = bar + 10;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 11);
+    float *red = reinterpret_cast<float *>(smem + 6 * kTile);           // [2 parity][2 halves][128] row max
+    float *redl = red + 512;                                             // [2 halves][128] row sums
+    int32_t *so = reinterpret_cast<int32_t *>(smem + 6 * kTile + kRedBytes);   // [R] sorted token offsets
+    int32_t *cum = so + kMaxReq;                                         // [R + 1]
+    int32_t *cnt = cum + kMaxReq;                                        // [kMaxQT + 1]
+    int32_t *start = cnt + kMaxQT + 1;                                   // [kMaxQT + 1]
+    int16_t *sl = reinterpret_cast<int16_t *>(start + kMaxQT + 1);       // [R] sorted lengths
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 6 * kTile + kRedBytes + kListBytes);
+    uint64_t *q_full = bar, *q_empty = bar + 1, *k_full = bar + 2, *k_empty = bar + 3, *v_full = bar + 4,
+             *v_empty = bar + 6, *s_full = bar + 8, *s_used = bar + 9, *p_ready = bar + 10, *pv_done = bar + 11,
+             *o_free = bar + 12, *info_read = bar + 15;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 13);
+    int4 *info = reinterpret_cast<int4 *>(bar + 16);                     // [2] published items (o, L, qt, h)
     uint8_t *smaps = reinterpret_cast<uint8_t *>(bar) + 256;            // 2 x 128-B maps being patched
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+    const int R = p.R, H = p.heads;
+    unsigned long long *trace = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
+#define ATT_TRACE(blk, ev) do { if (trace && (blk) < 512) trace[(blk) * 8 + (ev)] = clock64(); } while (0)
 
     if (threadIdx.x == 0) {
         ptx::prefetch_tmap(&tmQK);
         ptx::prefetch_tmap(&tmV);
         ptx::mbar_init(q_full, 1);
+        ptx::mbar_init(q_empty, 1);
         ptx::mbar_init(k_full, 1);
         ptx::mbar_init(k_empty, 1);
         for (int i = 0; i < 2; ++i) {
@@ -93,78 +172,161 @@ __global__ void __launch_bounds__(kThreads, 2)
         ptx::mbar_init(s_used, kSoftmaxThreads / 32);
         ptx::mbar_init(p_ready, kSoftmaxThreads / 32);
         ptx::mbar_init(pv_done, 1);
+        ptx::mbar_init(o_free, kSoftmaxThreads / 32);
+        ptx::mbar_init(info_read, kSoftmaxThreads / 32);
         ptx::fence_mbar_init();
         ptx::fence_async_smem();
     }
     if (warp == 8) ptx::tmem_alloc(tmem_slot, 256);
+    for (int i = threadIdx.x; i <= kMaxQT; i += kThreads) cnt[i] = 0;
+    ptx::pdl_wait();                              // QKV and seq_off come from earlier work
+    ptx::pdl_trigger();
+    __syncthreads();
+    // ---- work list (identical in every CTA): counting sort of the requests by query tiles, descending
+    for (int r = threadIdx.x; r < R; r += kThreads) atomicAdd(&cnt[min(qtiles_of(p.seq_off, r), kMaxQT)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int v = kMaxQT; v >= 0; --v) {
+            start[v] = s;
+            s += cnt[v];
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (int base = 0; base < R; base += 32) {     // stable: requests placed in index order
+            const int r = base + (int)lane;
+            const int v = r < R ? min(qtiles_of(p.seq_off, r), kMaxQT) : -1;
+            const uint32_t peers = __match_any_sync(0xffffffffu, v);
+            const int rank = __popc(peers & ((1u << lane) - 1u));
+            if (r < R) {
+                const int o = __ldg(p.seq_off + r);
+                so[start[v] + rank] = o;
+                sl[start[v] + rank] = (int16_t)(__ldg(p.seq_off + r + 1) - o);
+            }
+            __syncwarp();
+            if (v >= 0 && (int)lane == __ffs(peers) - 1) start[v] += __popc(peers);
+            __syncwarp();
+        }
+        int run = 0;                                    // cum: exclusive prefix of items per request
+        for (int base = 0; base < R; base += 32) {
+            const int i = base + (int)lane;
+            int c = i < R ? ((int)sl[i] + 127) / 128 * H : 0;
+            int incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, d);
+                if ((int)lane >= d) incl += t;
+            }
+            if (i < R) cum[i] = run + incl - c;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) cum[R] = run;
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;             // S: cols [0,128), O: cols [128,192)
+    const int n_items = cum[R];
 
     // device token count (nimble_attention_varlen_dev): T = seq_off[R] is data, so this CTA
     // publishes copies of both maps with the token extent patched to T (rows past T then
     // zero-fill exactly as with a host-encoded T).
     const CUtensorMap *mQK = &tmQK, *mV = &tmV;
     if (p.map_slots && warp == 8) {
-        const uint32_t T = (uint32_t)__ldg(p.seq_off + gridDim.z);
-        CUtensorMap *slot = p.map_slots + 2 * (size_t)((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+        const uint32_t T = (uint32_t)__ldg(p.seq_off + R);
+        CUtensorMap *slot = p.map_slots + 2 * (size_t)blockIdx.x;
         mQK = ptx::tmap_patch_extent<2>(&tmQK, smaps, slot, T, lane);
         mV = ptx::tmap_patch_extent<2>(&tmV, smaps + 128, slot + 1, T, lane);
     }
 
     if (warp == 8) {
       if (lane == 0) {
-        // ---------------- producer: Q once, then K_j / V_j through a 2-stage ring
-        ptx::mbar_arrive_expect_tx(q_full, kTile);
-        ptx::tma_load_3d(sQ, mQK, q_full, 0, h, o + q0);
-        for (int j = 0; j < nk; ++j) {
-            const int st = j & 1, use = j >> 1;
-            if (j > 0) ptx::mbar_wait(k_empty, (j - 1) & 1);          // S_{j-1} has read K
-            ptx::mbar_arrive_expect_tx(k_full, kTile);
-            ptx::tma_load_3d(sK, mQK, k_full, 0, p.heads + h, o + j * 128);
-            if (use > 0) ptx::mbar_wait(&v_empty[st], (use - 1) & 1); // PV_{j-2} has read V
-            ptx::mbar_arrive_expect_tx(&v_full[st], kTile);
-            ptx::tma_load_3d(sV + st * kTile, mV, &v_full[st], 0, 2 * p.heads + h, o + j * 128);
-            ptx::tma_load_3d(sV + st * kTile + kVBox, mV, &v_full[st], 0, 2 * p.heads + h, o + j * 128 + 64);
+        // ---------------- producer: the only role that decodes the work list.  Per item: publish
+        // (o, L, qt, h) in info[n & 1], then Q once, then K_j / V_j; runs ahead into the next item.
+        uint32_t nq = 0, nk_loaded = 0, nv = 0;
+        for (ItemIter iter(so, sl, cum, R, H, n_items); iter.valid(); iter.advance()) {
+            const Item it = iter.cur;
+            const int nk = (it.L + 127) / 128;
+            if (nq > 0) {
+                ptx::mbar_wait(q_empty, (nq - 1) & 1);                      // last S of the previous item read Q
+                // the softmax has read the previous item's info: q_full can never run two phases
+                // ahead of a softmax waiter (its parity wait would then block on the wrong phase)
+                ptx::mbar_wait(info_read, (nq - 1) & 1);
+            }
+            ATT_TRACE(256 + (int)nq, 0);
+            info[nq & 1] = make_int4(it.o, it.L, it.qt, it.h);              // released by the q_full arrive
+            ptx::mbar_arrive_expect_tx(q_full, kTile);
+            ptx::tma_load_3d(sQ, mQK, q_full, 0, it.h, it.o + it.qt * 128);
+            ++nq;
+            for (int j = 0; j < nk; ++j) {
+                if (nk_loaded > 0) ptx::mbar_wait(k_empty, (nk_loaded - 1) & 1);   // previous S read K
+                ATT_TRACE(256 + (int)nk_loaded, 1);
+                ptx::mbar_arrive_expect_tx(k_full, kTile);
+                ptx::tma_load_3d(sK, mQK, k_full, 0, H + it.h, it.o + j * 128);
+                ++nk_loaded;
+                const int st = (int)(nv & 1), use = (int)(nv >> 1);
+                if (use > 0) ptx::mbar_wait(&v_empty[st], (use - 1) & 1);   // PV two blocks back read V
+                ATT_TRACE(256 + (int)nv, 2);
+                ptx::mbar_arrive_expect_tx(&v_full[st], kTile);
+                ptx::tma_load_3d(sV + st * kTile, mV, &v_full[st], 0, 2 * H + it.h, it.o + j * 128);
+                ptx::tma_load_3d(sV + st * kTile + kVBox, mV, &v_full[st], 0, 2 * H + it.h, it.o + j * 128 + 64);
+                ++nv;
+                if (j == 0) iter.lookahead();           // while S_0 / the next k_empty are pending
+            }
         }
-      } else if (lane == 1) {
+      }
+      __syncwarp();
+    } else if (warp == 9) {
+      if (lane == 0) {
         // ---------------- MMA issuer
         const uint32_t idesc_s = ptx::idesc_bf16(128, 128, 0);
         const uint32_t idesc_o = ptx::idesc_bf16(128, 64, 1);
         const uint64_t qd = ptx::smem_desc_sw128(ptx::smem_u32(sQ), 0, 1024);
         const uint64_t kd = ptx::smem_desc_sw128(ptx::smem_u32(sK), 0, 1024);
-        auto issue_s = [&](int j) {
-            ptx::mbar_wait(k_full, j & 1);
-            ptx::tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-                ptx::umma_bf16(tmem, qd + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idesc_s, kk > 0 ? 1u : 0u);
-            ptx::umma_commit(s_full);
-            ptx::umma_commit(k_empty);
-        };
-        ptx::mbar_wait(q_full, 0);
-        issue_s(0);
-        for (int j = 0; j < nk; ++j) {
-            if (j + 1 < nk) {
-                ptx::mbar_wait(s_used, j & 1);    // softmax holds S_j in registers: buffer free
-                issue_s(j + 1);
-            }
-            ptx::mbar_wait(p_ready, j & 1);       // P_j written, O rescaled
-            const int st = j & 1;
-            ptx::mbar_wait(&v_full[st], (j >> 1) & 1);
-            ptx::tc_fence_after();
-#pragma unroll
-            for (int kb = 0; kb < 2; ++kb) {
-                const uint64_t pd = ptx::smem_desc_sw128(ptx::smem_u32(sP + kb * kTile), 0, 1024);
-                const uint64_t vd = ptx::smem_desc_sw128(ptx::smem_u32(sV + st * kTile + kb * kVBox), 8192, 1024);
+        uint32_t ns = 0, npv = 0, nitem = 0;
+        for (int k = (int)blockIdx.x; k < n_items; k += (int)gridDim.x) {
+            ATT_TRACE(384 + (int)nitem, 0);
+            ptx::mbar_wait(q_full, nitem & 1);
+            ATT_TRACE(256 + (int)nitem, 7);
+            const int nk = (info[nitem & 1].y + 127) / 128;
+            auto issue_s = [&](int j) {
+                if (ns > 0) ptx::mbar_wait(s_used, (ns - 1) & 1);      // softmax holds the previous S
+                ptx::mbar_wait(k_full, ns & 1);
+                ptx::tc_fence_after();
+                ATT_TRACE(ns, 6);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    ptx::umma_bf16(tmem + 128, pd + (uint64_t)(kk * 2), vd + (uint64_t)(kk * 128), idesc_o,
-                                   (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+                    ptx::umma_bf16(tmem, qd + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idesc_s, kk > 0 ? 1u : 0u);
+                ptx::umma_commit(s_full);
+                ptx::umma_commit(k_empty);
+                if (j == nk - 1) ptx::umma_commit(q_empty);
+                ++ns;
+            };
+            issue_s(0);
+            for (int j = 0; j < nk; ++j) {
+                if (j + 1 < nk) issue_s(j + 1);
+                ptx::mbar_wait(p_ready, npv & 1);                       // P_j written, O rescaled
+                if (j == 0 && nitem > 0) ptx::mbar_wait(o_free, (nitem - 1) & 1);   // previous O read out
+                const int st = (int)(npv & 1);
+                ptx::mbar_wait(&v_full[st], (npv >> 1) & 1);
+                ptx::tc_fence_after();
+                ATT_TRACE(npv, 7);
+#pragma unroll
+                for (int kb = 0; kb < 2; ++kb) {
+                    const uint64_t pd = ptx::smem_desc_sw128(ptx::smem_u32(sP + kb * kTile), 0, 1024);
+                    const uint64_t vd = ptx::smem_desc_sw128(ptx::smem_u32(sV + st * kTile + kb * kVBox), 8192, 1024);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        ptx::umma_bf16(tmem + 128, pd + (uint64_t)(kk * 2), vd + (uint64_t)(kk * 128), idesc_o,
+                                       (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+                }
+                ptx::umma_commit(pv_done);
+                ptx::umma_commit(&v_empty[st]);
+                ++npv;
             }
-            ptx::umma_commit(pv_done);
-            ptx::umma_commit(&v_empty[st]);
+            ATT_TRACE(384 + (int)nitem, 1);
+            ++nitem;
         }
       }
       __syncwarp();
@@ -174,106 +336,138 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int quarter = (int)(warp & 3), half = (int)(warp >> 2);
     const int q = quarter * 32 + (int)lane;
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    float m_run = -INFINITY, l_run = 0.f;
     const float sl2 = p.scale_log2;
-    for (int j = 0; j < nk; ++j) {
-        ptx::mbar_wait(s_full, j & 1);
-        ptx::tc_fence_after();
-        float v[64];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            float t[16];
-            ptx::tmem_ld16(trow + (uint32_t)(half * 64 + c * 16), t);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[c * 16 + e] = t[e];
-        }
-        ptx::tc_fence_before();
+    uint32_t ns = 0, npv = 0, nitem = 0;
+    for (int k = (int)blockIdx.x; k < n_items; k += (int)gridDim.x, ++nitem) {
+        ptx::mbar_wait(q_full, nitem & 1);         // the item's (o, L, qt, h) is published
+        const int4 it = info[nitem & 1];
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(s_used);  // the MMA warp may overwrite S now
-        const int kbase = j * 128 + half * 64;    // key index of v[0]
-        float mx = -INFINITY;
-        if (kbase + 64 <= L) {
-#pragma unroll
-            for (int e = 0; e < 64; e += 4) mx = fmaxf(mx, fmaxf(fmaxf(v[e], v[e + 1]), fmaxf(v[e + 2], v[e + 3])));
-        } else {
-#pragma unroll
-            for (int e = 0; e < 64; ++e)
-                if (kbase + e < L) mx = fmaxf(mx, v[e]);
-        }
-        red[half * 128 + q] = mx;
-        ptx::named_bar_sync(1, kSoftmaxThreads);
-        const float m_new = fmaxf(m_run, fmaxf(red[q], red[128 + q]));
-        const float alpha = ptx::ex2_approx((m_run - m_new) * sl2);   // m_run = -inf -> 0
-        const float ms = m_new * sl2;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        if (kbase + 64 <= L) {
-#pragma unroll
-            for (int e = 0; e < 64; ++e) v[e] = ptx::ex2_approx(fmaf(v[e], sl2, -ms));
-        } else {
-#pragma unroll
-            for (int e = 0; e < 64; ++e) v[e] = (kbase + e < L) ? ptx::ex2_approx(fmaf(v[e], sl2, -ms)) : 0.f;
-        }
-#pragma unroll
-        for (int e = 0; e < 64; e += 4) { s0 += v[e]; s1 += v[e + 1]; s2 += v[e + 2]; s3 += v[e + 3]; }
-        l_run = l_run * alpha + ((s0 + s1) + (s2 + s3));
-        m_run = m_new;
-        // P_{j-1} must be consumed (and O final for block j-1) before P / O are touched
-        if (j > 0) {
-            ptx::mbar_wait(pv_done, (j - 1) & 1);
+        if (lane == 0) ptx::mbar_arrive(info_read);
+        const int L = it.y, nk = (L + 127) / 128;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int j = 0; j < nk; ++j) {
+            ptx::mbar_wait(s_full, ns & 1);
             ptx::tc_fence_after();
-        }
-        // P_j: this warp group's 64 keys = one K-major 128-B-swizzled atom column block
-        uint8_t *rowp = sP + half * kTile + q * 128;
+            const int tb = (int)ns;
+            const bool tr = warp == 0 && lane == 0;
+            if (tr) ATT_TRACE(tb, 0);
+            float v[64];
+            {
+                uint32_t r[4][16];                    // four loads in flight, one wait
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            uint32_t w[4];
+                for (int c = 0; c < 4; ++c) ptx::tmem_ld16_nowait(trow + (uint32_t)(half * 64 + c * 16), r[c]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[c * 8 + 2 * e], v[c * 8 + 2 * e + 1]);
-                w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                for (int c = 0; c < 4; ++c) ptx::tmem_wait16(r[c]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[c * 16 + e] = __uint_as_float(r[c][e]);
             }
-            *reinterpret_cast<uint4 *>(rowp + ((c ^ (q & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-        // rescale this row's O half (32 of the 64 output columns) when the running max grew
-        if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(s_used);  // the MMA warp may overwrite S now
+            float *rd = red + (ns & 1) * 256;         // parity buffer: a fast half never overwrites
+            ++ns;                                     // the max its partner has not read yet
+            const int kbase = j * 128 + half * 64;    // key index of v[0]
+            const bool full = kbase + 64 <= L;
+            float mx = -INFINITY;
+            if (full) {
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                float t[16];
-                const uint32_t oa = trow + 128u + (uint32_t)(half * 32 + c * 16);
-                ptx::tmem_ld16(oa, t);
+                for (int e = 0; e < 64; e += 4) mx = fmaxf(mx, fmaxf(fmaxf(v[e], v[e + 1]), fmaxf(v[e + 2], v[e + 3])));
+            } else {
 #pragma unroll
-                for (int e = 0; e < 16; ++e) t[e] *= alpha;
-                tmem_st16(oa, t);
+                for (int e = 0; e < 64; ++e)
+                    if (kbase + e < L) mx = fmaxf(mx, v[e]);
             }
-            tmem_st_wait();
+            if (tr) ATT_TRACE(tb, 1);
+            rd[half * 128 + q] = mx;
+            ptx::named_bar_sync(1, kSoftmaxThreads);
+            if (tr) ATT_TRACE(tb, 2);
+            const float m_new = fmaxf(m_run, fmaxf(rd[q], rd[128 + q]));
+            const float alpha = ptx::ex2_approx((m_run - m_new) * sl2);   // m_run = -inf -> 0
+            const float ms = m_new * sl2;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            if (full) {
+#pragma unroll
+                for (int e = 0; e < 64; ++e) v[e] = ptx::ex2_approx(fmaf(v[e], sl2, -ms));
+            } else {
+#pragma unroll
+                for (int e = 0; e < 64; ++e) v[e] = (kbase + e < L) ? ptx::ex2_approx(fmaf(v[e], sl2, -ms)) : 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 64; e += 4) { s0 += v[e]; s1 += v[e + 1]; s2 += v[e + 2]; s3 += v[e + 3]; }
+            l_run = l_run * alpha + ((s0 + s1) + (s2 + s3));
+            m_run = m_new;
+            if (tr) ATT_TRACE(tb, 3);
+            // P_{j-1} must be consumed (and O final for block j-1) before P / O are touched; at
+            // j = 0 the previous item's epilogue already waited for its last PV
+            if (j > 0) {
+                ptx::mbar_wait(pv_done, npv & 1);
+                ++npv;
+                ptx::tc_fence_after();
+            }
+            if (tr) ATT_TRACE(tb, 4);
+            // P_j: this warp group's 64 keys = one K-major 128-B-swizzled atom column block
+            uint8_t *rowp = sP + half * kTile + q * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    __nv_bfloat162 h2 = __floats2bfloat162_rn(v[c * 8 + 2 * e], v[c * 8 + 2 * e + 1]);
+                    w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                }
+                *reinterpret_cast<uint4 *>(rowp + ((c ^ (q & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            // rescale this row's O half (32 of the 64 output columns) when the running max grew
+            if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    float t[16];
+                    const uint32_t oa = trow + 128u + (uint32_t)(half * 32 + c * 16);
+                    ptx::tmem_ld16(oa, t);
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) t[e] *= alpha;
+                    tmem_st16(oa, t);
+                }
+                tmem_st_wait();
+            }
+            ptx::fence_async_smem();                  // P (generic stores) -> tensor-core reads
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(p_ready);
+            if (tr) ATT_TRACE(tb, 5);
         }
-        ptx::fence_async_smem();                  // P (generic stores) -> tensor-core reads
+        // ---------------- epilogue: O / rowsum
+        redl[half * 128 + q] = l_run;
+        ptx::mbar_wait(pv_done, npv & 1);
+        ++npv;
+        ptx::tc_fence_after();
+        ptx::named_bar_sync(1, kSoftmaxThreads);
+        const float inv = 1.f / (redl[q] + redl[128 + q]);
+        float t0[16], t1[16];                         // every lane loads: tcgen05.ld is warp-collective
+        ptx::tmem_ld16(trow + 128u + (uint32_t)(half * 32), t0);
+        ptx::tmem_ld16(trow + 128u + (uint32_t)(half * 32 + 16), t1);
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(p_ready);
-    }
-    // ---------------- epilogue: O / rowsum
-    redl[half * 128 + q] = l_run;
-    ptx::mbar_wait(pv_done, (nk - 1) & 1);
-    ptx::tc_fence_after();
-    ptx::named_bar_sync(1, kSoftmaxThreads);
-    const float inv = 1.f / (redl[q] + redl[128 + q]);
-    float t0[16], t1[16];                         // every lane loads: tcgen05.ld is warp-collective
-    ptx::tmem_ld16(trow + 128u + (uint32_t)(half * 32), t0);
-    ptx::tmem_ld16(trow + 128u + (uint32_t)(half * 32 + 16), t1);
-    if (q0 + q < L) {
-        __nv_bfloat16 *dst = p.out + (int64_t)(o + q0 + q) * p.ld_out + h * 64 + half * 32;
-        uint32_t w[16];
+        if (lane == 0) ptx::mbar_arrive(o_free);      // the next item's first PV may overwrite O
+        const int q0 = it.z * 128;
+        if (q0 + q < L) {
+            __nv_bfloat16 *dst = p.out + (int64_t)(it.x + q0 + q) * p.ld_out + it.w * 64 + half * 32;
+            uint32_t w[16];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            __nv_bfloat162 a = __floats2bfloat162_rn(t0[2 * e] * inv, t0[2 * e + 1] * inv);
-            __nv_bfloat162 b = __floats2bfloat162_rn(t1[2 * e] * inv, t1[2 * e + 1] * inv);
-            w[e] = *reinterpret_cast<uint32_t *>(&a);
-            w[8 + e] = *reinterpret_cast<uint32_t *>(&b);
+            for (int e = 0; e < 8; ++e) {
+                __nv_bfloat162 a = __floats2bfloat162_rn(t0[2 * e] * inv, t0[2 * e + 1] * inv);
+                __nv_bfloat162 b = __floats2bfloat162_rn(t1[2 * e] * inv, t1[2 * e + 1] * inv);
+                w[e] = *reinterpret_cast<uint32_t *>(&a);
+                w[8 + e] = *reinterpret_cast<uint32_t *>(&b);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                reinterpret_cast<uint4 *>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
         }
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            reinterpret_cast<uint4 *>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+        // redl is rewritten by the next item only after this item's blocks: the named barrier of
+        // the next item's first block orders it after every thread's read above
     }
     }   // softmax warps
     ptx::tc_fence_before();
@@ -291,9 +485,23 @@ size_t attention_smem_bytes(int max_len) {
     return kSmemBytes;
 }
 
+int attention_max_requests() { return kMaxReq; }
+
+int attention_grid(int R, int max_len, int heads) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms = 148;
+    }
+    const int64_t upper = (int64_t)R * ((max_len + 127) / 128) * heads;   // items, if every L_i = max_len
+    const int64_t g = (int64_t)kCtasPerSm * sms;
+    return (int)(upper < g ? upper : g);
+}
+
 cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const int32_t *seq_off,
                                     int R, int max_len, int heads, float scale, __nv_bfloat16 *out, int64_t ld_out,
-                                    cudaStream_t s, CUtensorMap *map_slots) {
+                                    cudaStream_t s, CUtensorMap *map_slots, unsigned long long *trace) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(attention_varlen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -303,12 +511,14 @@ cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &
     }
     AttnParams p;
     p.seq_off = seq_off;
+    p.R = R;
     p.heads = heads;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.out = out;
     p.ld_out = ld_out;
     p.map_slots = map_slots;
-    const dim3 grid((unsigned)((max_len + 127) / 128), (unsigned)heads, (unsigned)R);
+    p.trace = trace;
+    const dim3 grid((unsigned)attention_grid(R, max_len, heads));
     return launch_pdl(attention_varlen_kernel, grid, dim3(kThreads), attention_smem_bytes(max_len), s, tmQK, tmV, p);
 }
 

@@ -48,6 +48,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 }
 
 // ----------------------------------------------------------------- TMA
+// TMA tile prefetch into L2 (no smem destination, no barrier): warms the box for a later load.
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *m, int32_t c0, int32_t c1, int32_t c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
@@ -102,6 +108,23 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Split form: several loads in flight, then one wait.  tmem_wait16 names the registers as
+// in/out operands of the wait, so no use of them can be scheduled above it.
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait16(uint32_t (&r)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+                 :
+                 : "memory");
 }
 
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"):
@@ -183,8 +206,34 @@ __device__ __forceinline__ float erf_as(float x) { return erf_as28(x); }
 #endif
 #ifdef NIMBLE_GELU_ERFF
 __device__ __forceinline__ float gelu_erf(float z) { return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f)); }
-#else
+#elif defined(NIMBLE_GELU_UNFOLDED)
 __device__ __forceinline__ float gelu_erf(float z) { return 0.5f * z * (1.0f + erf_as(z * 0.70710678118654752f)); }
+#else
+// GELU(z) = z Phi(z), Phi(z) = (1 + erf(z / sqrt2)) / 2, with erf from A&S 7.1.28 (the same
+// approximation as erf_as28, |error| <= 5e-7 on GELU) re-associated for the epilogue's issue
+// budget (14 instructions, two MUFU; the epilogue of the GELU GEMM is issue-bound):
+//   * 1/sqrt2 is folded into the coefficients (b_i = a_i 2^(-i/2)),
+//   * the 1/2 of Phi is folded in too: scaling p by 2^(1/16) gives h = p^-16 = (1 - erf) / 2,
+//   * Phi = 1 - h (z >= 0) or h (z < 0), so z Phi = max(z, 0) - |z h| with no select,
+//   * p^-16 = ex2(-16 lg2 p) (lg2/ex2.approx relative error ~2^-22, x16 -> ~4e-6 relative on h).
+__device__ __forceinline__ float gelu_erf(float z) {
+    const float q = fabsf(z);
+    float p = fmaf(5.621299664e-06f, q, 5.105520901e-05f);
+    p = fmaf(p, q, 3.968613701e-05f);
+    p = fmaf(p, q, 3.422739239e-03f);
+    p = fmaf(p, q, 2.207699846e-02f);
+    p = fmaf(p, q, 5.207516304e-02f);
+    p = fmaf(p, q, 1.044273782e+00f);
+#ifdef NIMBLE_GELU_RCP
+    float h = rcp_approx(p);
+    h *= h; h *= h; h *= h; h *= h;                  // 2^-1 (1 + sum a_i x^i)^-16
+#else
+    float h;                                         // p^-16 = 2^(-16 log2 p): 3 instructions, 2 MUFU
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(h) : "f"(p));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(h) : "f"(-16.0f * h));
+#endif
+    return fmaxf(z, 0.0f) - fabsf(z * h);
+}
 #endif
 __device__ __forceinline__ float sigmoidf_(float z) { return 1.0f / (1.0f + expf(-z)); }
 

@@ -3,7 +3,8 @@
 config 2: 2-layer LSTM LM, I = H = 650, batch 1, T in {35, 128, 512}: us/token (hoisted input
           GEMM via dense_dyn + persistent recurrence, all on one stream, CUDA events).
 config 3: BERT-base, batch 1, every L in 1..128: per-request latency (per-L CUDA graph of the
-          12-layer batch-1 path) -> us/token; plus the packed equivalent.
+          12-layer batch-1 path, or one device-extent graph for every L) -> us/token; plus the
+          packed equivalent.
 config 4: Tree-LSTM (300/150) forests of 1 and 32 random trees: us/tree, us/leaf.
 Paper context (other hardware): LSTM 2L Nimble T4 107.4 us/token (300/512); BERT-base
 Nimble T4 95.2 us/token; Tree-LSTM Nimble Intel 40.3 us/token.
@@ -19,7 +20,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2006_03031_b200 import nimble as nb, synth  # noqa: E402
 from paper_2006_03031_b200.bert import BertEncoder, BertPacked  # noqa: E402
 from paper_2006_03031_b200.rnn import LSTMStack, TreeLSTM, TreeSchedule  # noqa: E402
-from paper_2006_03031_b200.serve import GraphCache  # noqa: E402
+from paper_2006_03031_b200.serve import DeviceExtentGraph, GraphCache  # noqa: E402
 
 
 SCHEDULES = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2006_03031_b200",
@@ -73,11 +74,13 @@ def config3(rep):
     cfg = dict(synth.BERT_BASE)
     w = synth.bert_weights_device(cfg, seed=0)
     out = torch.empty((cfg["d"],), dtype=torch.bfloat16, device="cuda")
-    for tag in ("", "_tuned"):
-        if tag:
+    # "": per-L graphs, default rule; "_devextent": ONE graph for every L, extent and residue
+    # dispatch on the device (f4); "_tuned": per-L graphs with the tuned schedules (f3)
+    for tag in ("", "_devextent", "_tuned"):
+        if tag == "_tuned":
             nb.load_dense_schedules(SCHEDULES)
         enc = BertPacked(cfg, w, max_tokens=128)          # batch 1 = packed batch of one request
-        cache = GraphCache(enc)
+        cache = DeviceExtentGraph(enc) if tag == "_devextent" else GraphCache(enc)
         c3 = []
         for L in range(1, 129):
             cache.capture(L)

@@ -23,10 +23,20 @@ out = torch.empty((T, d), device="cuda", dtype=torch.bfloat16)
 for _ in range(3):
     nb.attention_varlen(qkv, off, len(lens), int(lens.max()), H, out)
 torch.cuda.synchronize()
+# CUDA graph of `reps` launches: device time per launch, no host enqueue gaps
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+g = torch.cuda.CUDAGraph()
+with torch.cuda.stream(s):
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(a.reps):
+            nb.attention_varlen(qkv, off, len(lens), int(lens.max()), H, out)
+torch.cuda.current_stream().wait_stream(s)
+g.replay()
+torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-for _ in range(a.reps):
-    nb.attention_varlen(qkv, off, len(lens), int(lens.max()), H, out)
+g.replay()
 e1.record()
 torch.cuda.synchronize()
 t = e0.elapsed_time(e1) / 1e3 / a.reps
