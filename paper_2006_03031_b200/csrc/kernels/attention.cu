@@ -71,6 +71,52 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2) and the 3-input max (FMNMX3): the softmax is
+// issue- and MUFU-bound, so every instruction counts.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+// 2^x for x <= 0 on the FMA pipes (a pair at a time): x = j + f, j = rint(x) by the 1.5 * 2^23
+// magic-number rounding, f in [-1/2, 1/2]; 2^f by a degree-3 minimax polynomial (relative
+// error 7.5e-5, far below the bf16 rounding of P); 2^j added into the exponent field.  x is
+// clamped at -125 so the exponent stays normal (2^-125 is 0 next to a row sum >= 1).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -125.f);
+    x.y = fmaxf(x.y, -125.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f), nmagic = make_float2(-12582912.f, -12582912.f);
+    const float2 t = fadd2(x, magic);
+    const float2 r = fadd2(t, nmagic);                           // rint(x)
+    const float2 f = fadd2(x, make_float2(-r.x, -r.y));
+    float2 q = ffma2(make_float2(0.0551710878f, 0.0551710878f), f, make_float2(0.242611162f, 0.242611162f));
+    q = ffma2(q, f, make_float2(0.693261098f, 0.693261098f));
+    q = ffma2(q, f, make_float2(0.999928072f, 0.999928072f));
+    return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+#ifndef NIMBLE_ATTN_POLY
+#define NIMBLE_ATTN_POLY 2          // pairs out of every 8 whose exp2 runs on the FMA pipes
+#endif
+
 __device__ __forceinline__ int qtiles_of(const int32_t *seq_off, int r) {
     const int L = __ldg(seq_off + r + 1) - __ldg(seq_off + r);
     return (L + 127) / 128;
@@ -372,8 +418,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             const bool full = kbase + 64 <= L;
             float mx = -INFINITY;
             if (full) {
+                float ma = v[0], mb = v[1];
 #pragma unroll
-                for (int e = 0; e < 64; e += 4) mx = fmaxf(mx, fmaxf(fmaxf(v[e], v[e + 1]), fmaxf(v[e + 2], v[e + 3])));
+                for (int e = 2; e < 62; e += 4) {
+                    ma = fmax3(ma, v[e], v[e + 1]);
+                    mb = fmax3(mb, v[e + 2], v[e + 3]);
+                }
+                mx = fmax3(ma, mb, fmaxf(v[62], v[63]));
             } else {
 #pragma unroll
                 for (int e = 0; e < 64; ++e)
@@ -386,17 +437,32 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             const float m_new = fmaxf(m_run, fmaxf(rd[q], rd[128 + q]));
             const float alpha = ptx::ex2_approx((m_run - m_new) * sl2);   // m_run = -inf -> 0
             const float ms = m_new * sl2;
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            float2 sa = make_float2(0.f, 0.f), sb = sa;
             if (full) {
+                const float2 sc = make_float2(sl2, sl2), nm = make_float2(-ms, -ms);
 #pragma unroll
-                for (int e = 0; e < 64; ++e) v[e] = ptx::ex2_approx(fmaf(v[e], sl2, -ms));
+                for (int e = 0; e < 64; e += 2) {
+                    float2 x = ffma2(make_float2(v[e], v[e + 1]), sc, nm);
+                    if (((e >> 1) & 7) < NIMBLE_ATTN_POLY) {
+                        x = exp2_poly2(x);
+                    } else {
+                        x.x = ptx::ex2_approx(x.x);
+                        x.y = ptx::ex2_approx(x.y);
+                    }
+                    v[e] = x.x;
+                    v[e + 1] = x.y;
+                }
             } else {
 #pragma unroll
                 for (int e = 0; e < 64; ++e) v[e] = (kbase + e < L) ? ptx::ex2_approx(fmaf(v[e], sl2, -ms)) : 0.f;
             }
 #pragma unroll
-            for (int e = 0; e < 64; e += 4) { s0 += v[e]; s1 += v[e + 1]; s2 += v[e + 2]; s3 += v[e + 3]; }
-            l_run = l_run * alpha + ((s0 + s1) + (s2 + s3));
+            for (int e = 0; e < 64; e += 4) {
+                sa = fadd2(sa, make_float2(v[e], v[e + 1]));
+                sb = fadd2(sb, make_float2(v[e + 2], v[e + 3]));
+            }
+            sa = fadd2(sa, sb);
+            l_run = l_run * alpha + (sa.x + sa.y);
             m_run = m_new;
             if (tr) ATT_TRACE(tb, 3);
             // P_{j-1} must be consumed (and O final for block j-1) before P / O are touched; at
