@@ -235,6 +235,59 @@ __device__ __forceinline__ float gelu_erf(float z) {
     return fmaxf(z, 0.0f) - fabsf(z * h);
 }
 #endif
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2) and the 3-input max (FMNMX3).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+// gelu_erf on two values at once: the same arithmetic as gelu_erf (same constants, same
+// order per element), with the polynomial and products in FFMA2 / FMUL2.
+__device__ __forceinline__ float2 gelu_erf2(float2 z) {
+    const float2 q = make_float2(fabsf(z.x), fabsf(z.y));
+    float2 p = ffma2(f2(5.621299664e-06f), q, f2(5.105520901e-05f));
+    p = ffma2(p, q, f2(3.968613701e-05f));
+    p = ffma2(p, q, f2(3.422739239e-03f));
+    p = ffma2(p, q, f2(2.207699846e-02f));
+    p = ffma2(p, q, f2(5.207516304e-02f));
+    p = ffma2(p, q, f2(1.044273782e+00f));
+    float2 h;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(h.x) : "f"(p.x));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(h.y) : "f"(p.y));
+    h = fmul2(h, f2(-16.0f));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(h.x) : "f"(h.x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(h.y) : "f"(h.y));
+    const float2 w = fmul2(z, h);
+    return make_float2(fmaxf(z.x, 0.0f) - fabsf(w.x), fmaxf(z.y, 0.0f) - fabsf(w.y));
+}
 __device__ __forceinline__ float sigmoidf_(float z) { return 1.0f / (1.0f + expf(-z)); }
 
 }  // namespace ptx

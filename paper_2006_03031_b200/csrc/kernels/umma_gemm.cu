@@ -367,10 +367,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int c0 = half * 16; c0 < n_this; c0 += 16 * kEpiGroups) {
                         float v[16];
                         ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
+                        if constexpr (EPI == 2) {
+                            // GELU on pairs of token columns (FFMA2 / FMUL2): the epilogue of the
+                            // GELU GEMM is issue-bound, the pairs halve its polynomial work
+#pragma unroll
+                            for (int q = 0; q < 16; q += 2) {
+                                const float2 g = ptx::gelu_erf2(ptx::fadd2(make_float2(v[q], v[q + 1]), ptx::f2(bias_i)));
+                                v[q] = g.x;
+                                v[q + 1] = g.y;
+                            }
+                        }
 #pragma unroll
                         for (int q = 0; q < 16; ++q) {
                             const int o = (c0 + q) * 128 + row_local;
-                            float val = epi_math<EPI>(v[q], p.alpha, bias_i);
+                            float val = EPI == 2 ? v[q] : epi_math<EPI>(v[q], p.alpha, bias_i);
                             if constexpr (EPI == 3) val += __bfloat162float(reinterpret_cast<__nv_bfloat16 *>(stg)[o]);
                             if constexpr (OUT_F32) so[o] = val;
                             else so[o] = __float2bfloat16_rn(val);
