@@ -236,7 +236,7 @@ def main():
         sched_used = os.path.relpath(args.schedules, os.path.dirname(os.path.abspath(__file__)))
     if args.mode == "packed":
         enc = BertPacked(cfg, weights, max_tokens=max(my_tokens, 1))
-        launches_per_step = enc.launches_per_forward()
+        launches_per_step = enc.launches_per_forward(my_tokens)
 
         def run_local(X):
             if len(ids):
@@ -295,7 +295,7 @@ def main():
     roof = None
     if not args.profile and args.mode == "packed" and len(ids):
         trace = []
-        orig = nb.dense_dyn_raw
+        orig, orig_ln = nb.dense_dyn_raw, nb.dense_ln_dyn_raw
 
         def timed(*a):
             e_a = torch.cuda.Event(enable_timing=True)
@@ -304,17 +304,26 @@ def main():
             orig(*a)
             e_b.record()
             trace.append((a[9], a[10], a[11], a[13], e_a, e_b))
-        nb.dense_dyn_raw = timed
+
+        def timed_ln(*a):                          # dense + LayerNorm epilogue (residual read too)
+            e_a = torch.cuda.Event(enable_timing=True)
+            e_b = torch.cuda.Event(enable_timing=True)
+            e_a.record()
+            orig_ln(*a)
+            e_b.record()
+            trace.append((a[12], a[13], a[14], 4, e_a, e_b))
+        nb.dense_dyn_raw, nb.dense_ln_dyn_raw = timed, timed_ln
         try:
             torch.cuda._sleep(int(2e8))            # keep the GPU busy while the host enqueues
             run_local(X_mine)
             torch.cuda.synchronize()
         finally:
-            nb.dense_dyn_raw = orig
+            nb.dense_dyn_raw, nb.dense_ln_dyn_raw = orig, orig_ln
         fl = by = tm = 0.0
         for (M, N, K, epi, a, b) in trace:
             fl += 2.0 * M * N * K
-            by += 2.0 * (M * K + N * K) + 4.0 * N + 2.0 * M * N + (2.0 * M * N if epi == 3 else 0.0)
+            by += 2.0 * (M * K + N * K) + 4.0 * N + 2.0 * M * N + (2.0 * M * N if epi >= 3 else 0.0) + \
+                (8.0 * N if epi == 4 else 0.0)
             tm += a.elapsed_time(b) / 1e3
         n = len(trace)
         t_tc, t_hbm = fl / (peaks["tc_sus"] * 1e12), by / (peaks["hbm"] * 1e9)
@@ -330,7 +339,8 @@ def main():
         except Exception:
             pass
         roof = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit, "frac": ach / pk, "traffic": traffic,
-                "kernel": "nimble::umma_gemm_kernel (dense_dyn bf16: QKV, O, FFN1, FFN2 at M = packed tokens)",
+                "kernel": ("nimble::umma_gemm_kernel (bf16 at M = packed tokens: dense_dyn QKV, FFN1; "
+                           "dense_ln_dyn O+LN1, FFN2+LN2)"),
                 "launches": n, "avg_launch_us": 1e6 * tm / max(n, 1),
                 "algorithmic_flops_per_launch": fl / max(n, 1), "algorithmic_bytes_per_launch": by / max(n, 1),
                 "frac_of_burst_peak": fl / tm / 1e12 / peaks["tc"],
@@ -385,8 +395,9 @@ def main():
                           "requests_per_step": R, "tokens_per_step": int(lens.sum()), "layers": args.layers,
                           "l2": "inputs 35 MB + weights 604 MB/GPU > 126 MB L2 per step; no flush",
                           "parallelism": f"dp-requests{world} (LPT shards, NCCL gather)",
-                          "execution": ("token-packed forward: 7 launches/layer (dense_dyn M=sum L_i x4, "
-                                        "attention_varlen, layernorm x2)" if args.mode == "packed" else
+                          "execution": ((f"token-packed forward: {launches_per_step // args.layers} launches/layer "
+                                         "(dense_dyn QKV, attention_varlen, dense_ln_dyn O+LN1, dense_dyn FFN1, "
+                                         "dense_ln_dyn FFN2+LN2; M = sum L_i)") if args.mode == "packed" else
                                         "per-L CUDA graphs of one-request packed forwards (batch 1)"),
                           "tuned_schedules": sched_used, "setup_s": round(t_setup, 2)},
                "tflops": tflops, "pct_tc_peak": tflops / peaks["tc_sus"],

@@ -147,6 +147,23 @@ int nimble_dense_static(const void *x, int64_t ldx, const void *W, int64_t ldw, 
                         const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
                         int64_t K, int dt, int epi, void *stream);
 
+/* nimble_dense_ln_dyn — dense_dyn with the post-LN BERT sublayer tail fused in:
+ *     y[i] = LayerNorm(x[i] W^T + bias + residual[i]) * gamma + beta,   i < M,
+ * LayerNorm over the N features of each row (biased variance, eps inside the rsqrt;
+ * DESIGN.md reading 10: post-LN, eps = 1e-12 in BERT).  Arguments as nimble_dense_dyn with
+ * dt = NIMBLE_BF16 and the BIAS_RESIDUAL epilogue; gamma, beta: fp32 [N], 16-B aligned.
+ * Where the residue dispatch picks the 2-CTA family (M >= 2048), N = 1024 and K >= 2048
+ * (a main loop long enough to hide the exchange) the LayerNorm runs in the GEMM epilogue: the 8 CTAs holding the four 256-feature quarters of a
+ * 256-token tile exchange per-token (sum, sum of squares) partials through a library
+ * workspace (one such launch in flight per device); the pre-LN sum is rounded to bf16
+ * first, as in the two-launch form.  Elsewhere: nimble_dense_dyn then nimble_layernorm in
+ * place on y (same results up to the variance formula: fused = E[v^2] - mean^2 in fp32,
+ * two-launch = two-pass).  Errors as nimble_dense_dyn; N % 8 != 0 or N > 4096 ->
+ * E_UNSUPPORTED. */
+int nimble_dense_ln_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+                        const void *residual, int64_t ldr, const float *gamma, const float *beta, float eps,
+                        void *y, int64_t ldy, int64_t M, int64_t N, int64_t K, void *stream);
+
 /* nimble_dense_dyn_dev — device-resident extent and dispatch (the "upper bound" shape
  * function of P:269-271 plus on-device dispatch, so one captured CUDA graph serves every
  * extent; P:709-710 hides dispatch behind GPU execution).  bf16 only.  The caller

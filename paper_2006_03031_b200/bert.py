@@ -108,7 +108,9 @@ class BertPacked:
     NEXT-1).  The R requests' tokens are concatenated into X [T x d], T = sum L_i; every
     dense runs once with the symbolic M = T (residue dispatch on T), attention runs once
     per layer over all (request, head) pairs with each request's own L_i
-    (nimble_attention_varlen: no S / P round trip through HBM).  Per layer 7 launches:
+    (nimble_attention_varlen: no S / P round trip through HBM).  With fused_ln the
+    O-projection + LN1 and FFN2 + LN2 pairs are nimble_dense_ln_dyn calls (the library fuses
+    LN2 into the FFN2 epilogue at M >= 2048: 6 launches per layer); unfused, 7 launches:
 
         QKV = X Wqkv^T + bqkv            dense_dyn  (M = T)
         C   = attention_varlen(QKV)      one launch, per-request L_i
@@ -119,10 +121,13 @@ class BertPacked:
         Y   = LN2(O)
     """
 
-    def __init__(self, cfg: dict, weights: list, max_tokens: int, device="cuda"):
+    def __init__(self, cfg: dict, weights: list, max_tokens: int, device="cuda", fused_ln: bool = True):
         self.d, self.H, self.f = cfg["d"], cfg["heads"], cfg["ffn"]
         self.dh = self.d // self.H
         self.max_tokens = max_tokens
+        # fused_ln: O-proj + LN1 and FFN2 + LN2 as nimble_dense_ln_dyn (LayerNorm in the GEMM
+        # epilogue where the dispatch allows; A / O are then not materialised)
+        self.fused_ln = fused_ln
         self.layers = [{k: v.to(device).contiguous() for k, v in w.items()} for w in weights]
         d, f, Tm = self.d, self.f, max_tokens
         bf = dict(dtype=torch.bfloat16, device=device)
@@ -140,8 +145,12 @@ class BertPacked:
     def flops(lens, d=1024, f=4096, layers=24) -> int:
         return int(sum((2 * L * d * (3 * d + d + 2 * f) + 4 * L * L * d) * layers for L in lens))
 
-    def launches_per_forward(self) -> int:
-        return 7 * len(self.layers)
+    def launches_per_forward(self, T: int | None = None) -> int:
+        """Kernel launches of one forward at T packed tokens: 6 per layer where LN2 fuses into the
+        FFN2 epilogue (fused_ln, 2-CTA family M = T >= 2048, d = 1024, K = ffn >= 2048; LN1 after
+        the K = 1024 O-projection stays a launch, the library's rule), else 7."""
+        fused = self.fused_ln and T is not None and T >= 2048 and self.d == 1024 and self.f >= 2048
+        return (6 if fused else 7) * len(self.layers)
 
     def layer(self, x_ptr, out_ptr, T, seq_off_ptr, R, max_len, li, stream):
         d, f, H = self.d, self.f, self.H
@@ -150,6 +159,14 @@ class BertPacked:
                          nb.BF16, nb.EPI_BIAS, stream)
         nb._check(nb._lib.nimble_attention_varlen(p["qkv"], 3 * d, T, seq_off_ptr, R, max_len, H, self.dh,
                                                   1.0 / float(self.dh) ** 0.5, p["ctx"], d, stream))
+        if self.fused_ln:
+            nb.dense_ln_dyn_raw(p["ctx"], d, w["Wo"], d, w["bo"], x_ptr, d, w["g1"], w["be1"], 1e-12, p["H1"], d,
+                                T, d, d, stream)
+            nb.dense_dyn_raw(p["H1"], d, w["W1"], d, w["b1"], None, 0, p["F"], f, T, f, d,
+                             nb.BF16, nb.EPI_BIAS_GELU, stream)
+            nb.dense_ln_dyn_raw(p["F"], f, w["W2"], f, w["b2"], p["H1"], d, w["g2"], w["be2"], 1e-12, out_ptr, d,
+                                T, d, f, stream)
+            return
         nb.dense_dyn_raw(p["ctx"], d, w["Wo"], d, w["bo"], x_ptr, d, p["A"], d, T, d, d,
                          nb.BF16, nb.EPI_BIAS_RESIDUAL, stream)
         nb._check(nb._lib.nimble_layernorm(p["A"], d, w["g1"], w["be1"], 1e-12, p["H1"], d, T, d, stream))

@@ -171,9 +171,51 @@ extern "C" int nimble_last_dispatch(nimble_dispatch *out) {
 }
 
 // ------------------------------------------------------------------ dense_dyn
+// Library workspace of the fused LayerNorm epilogue: per group of 4 CTA pairs, 2 slots of
+// (sum, sum of squares) partials for 256 tokens x 8 CTAs, and 2 self-resetting counters per slot.
+namespace nimble {
+namespace {
+constexpr int kLnMaxGroups = kNumSMs / 8;
+struct LnWorkspace {
+    std::mutex mu;
+    float2 *stats[64] = {};
+    int32_t *cnt[64] = {};
+};
+LnWorkspace g_ln_ws;
+cudaError_t ln_workspace(float2 **stats, int32_t **cnt) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_ln_ws.mu);
+    if (!g_ln_ws.stats[dev]) {
+        if ((e = cudaMalloc(&g_ln_ws.stats[dev], sizeof(float2) * 2 * kLnMaxGroups * 8 * 256)) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&g_ln_ws.cnt[dev], sizeof(int32_t) * 2 * kLnMaxGroups * 2)) != cudaSuccess) return e;
+        if ((e = cudaMemset(g_ln_ws.cnt[dev], 0, sizeof(int32_t) * 2 * kLnMaxGroups * 2)) != cudaSuccess) return e;
+        if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
+    }
+    *stats = g_ln_ws.stats[dev];
+    *cnt = g_ln_ws.cnt[dev];
+    return cudaSuccess;
+}
+bool fused_ln_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("NIMBLE_FUSED_LN");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+struct LnArgs {
+    const float *gamma, *beta;
+    float eps;
+    bool fused;            // out: the LayerNorm ran in the GEMM epilogue
+};
+}  // namespace
+}  // namespace nimble
+
 static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
                       const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
-                      int64_t K, int dt, int epi, void *stream, bool static_twin) {
+                      int64_t K, int dt, int epi, void *stream, bool static_twin, LnArgs *ln = nullptr) {
     // 1. shape function (runtime type-relation check)
     const int64_t xs[2] = {M, K}, ws[2] = {N, K};
     int64_t os[2];
@@ -249,6 +291,24 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     if (L.pair && (L.p.a_batch_mid || L.p.b_batch_mid)) return fail(NIMBLE_E_UNSUPPORTED, "pair mode needs row-major batches");
     plan_pipeline(L, d);
     L.stream = s;
+    if (ln) {
+        // fused only where a group of 4 pairs covers the whole row (family 3, N = 4 x 256) and
+        // the main loop is long enough (K >= 2048) to hide the epilogue's cross-CTA exchange;
+        // at K = 1024 (BERT's O-projection) the fused epilogue costs what the LN launch saves
+        ln->fused = fused_ln_enabled() && L.pair && N == 1024 && K >= 2048 && epi == NIMBLE_EPI_BIAS_RESIDUAL &&
+                    !static_twin;
+        if (ln->fused) {
+            cudaError_t e = ln_workspace(&L.p.ln_stats, &L.p.ln_cnt);
+            if (e != cudaSuccess) return cuda_fail("nimble_dense_ln_dyn workspace", e);
+            const int groups = L.p.tiles_n < kLnMaxGroups ? L.p.tiles_n : kLnMaxGroups;
+            L.p.ln_groups = groups;
+            L.p.ln_gamma = ln->gamma;
+            L.p.ln_beta = ln->beta;
+            L.p.ln_eps = ln->eps;
+            L.grid = dim3((unsigned)(8 * groups), 1, 1);
+            L.epi = 4;
+        }
+    }
     if (static_twin && (epi != NIMBLE_EPI_BIAS || !umma_static_available(M, N, K)))
         return fail(NIMBLE_E_UNSUPPORTED, "nimble_dense_static(bf16): (M, N, K) not compiled in, or epilogue != BIAS");
     cudaError_t e = static_twin ? launch_umma_gemm_static(L, M, N, K) : launch_umma_gemm(L);
@@ -262,6 +322,23 @@ extern "C" int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64
                                 const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
                                 int64_t K, int dt, int epi, void *stream) {
     return dense_impl(x, ldx, W, ldw, bias, residual, ldr, y, ldy, M, N, K, dt, epi, stream, false);
+}
+
+extern "C" int nimble_dense_ln_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+                                   const void *residual, int64_t ldr, const float *gamma, const float *beta, float eps,
+                                   void *y, int64_t ldy, int64_t M, int64_t N, int64_t K, void *stream) {
+    if (!gamma || !beta || !bias || !residual) return fail(NIMBLE_E_NULL, "nimble_dense_ln_dyn: bias, residual, gamma, beta required");
+    if (!aligned16(gamma) || !aligned16(beta)) return fail(NIMBLE_E_ALIGN, "nimble_dense_ln_dyn: gamma / beta 16-B aligned");
+    if (N > 4096 || N % 8) return fail(NIMBLE_E_UNSUPPORTED, "nimble_dense_ln_dyn: N must be a multiple of 8, <= 4096");
+    LnArgs ln{gamma, beta, eps, false};
+    int st = dense_impl(x, ldx, W, ldw, bias, residual, ldr, y, ldy, M, N, K, NIMBLE_BF16, NIMBLE_EPI_BIAS_RESIDUAL,
+                        stream, false, &ln);
+    if (st != NIMBLE_OK || ln.fused) return st;
+    // not fusable at this (M, N): the same two steps as separate launches, LayerNorm in place
+    nimble_dispatch keep = t_last;
+    st = nimble_layernorm(y, ldy, gamma, beta, eps, y, ldy, M, N, stream);
+    t_last = keep;
+    return st;
 }
 
 extern "C" int nimble_dense_static(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,

@@ -45,6 +45,15 @@ struct UmmaParams {
     int32_t var_c;               // variant limit c for the device dispatch
     CUtensorMap *out_slot;       // per-CTA global slots for the extent-patched output map
     nimble_dispatch *rec;        // optional device record of the device dispatch (CTA 0 writes it)
+    // fused LayerNorm epilogue (EPI 4, pair family, rows of exactly 4 x 256 = 1024 features):
+    // y = LN(acc + bias + res) * gamma + beta over each token's 1024 features.  The 8 CTAs of a
+    // group (4 pairs = the 4 feature tiles of one token tile) exchange per-token partial sums
+    // through ln_stats / ln_cnt (library workspace, counters self-resetting).
+    const float *ln_gamma, *ln_beta;
+    float ln_eps;
+    int32_t ln_groups;           // groups of 4 pairs; pairs >= 4 * ln_groups idle
+    float2 *ln_stats;            // [2 * ln_groups][8][256] (sum x, sum x^2) partials
+    int32_t *ln_cnt;             // [2 * ln_groups][2] writers / readers per slot
 };
 
 struct UmmaLaunch {

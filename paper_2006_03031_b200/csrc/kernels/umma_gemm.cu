@@ -115,6 +115,105 @@ __device__ __forceinline__ float epi_math(float acc, float alpha, float bias_i) 
     else return acc + bias_i;      // EPI 1, and 3 before the residual add
 }
 
+// Fused LayerNorm over a 256-token x 1024-feature row block held by the 8 CTAs of a group (EPI 4).
+// This CTA's staging holds bf16 pre-LN sums v = acc + bias + residual for its 128 features
+// (feature-contiguous rows of 256 B, one per token).  Thread e (of 256): feature chunks
+// (e & 7) and (e & 7) + 8 (8 features each, conflict-free 16-B shared loads), tokens
+// (e >> 3) + 32 k, k < 8.
+//   1. partial (sum v, sum v^2) over the 128 features per token -> ln_stats[slot][cta][token]
+//   2. release (fence + counter), wait until the 8 CTAs of the group have written
+//   3. mean = S1 / 1024, var = S2 / 1024 - mean^2 (biased, fp32), y = (v - mean) rsqrt(var + eps)
+//      gamma + beta -> bf16 back into staging (then the usual clipped TMA store)
+// The partials are summed in a fixed butterfly order: the result is deterministic.
+__device__ __forceinline__ void ln_tile(const UmmaParams &p, uint8_t *stg, int n_this, int prank, int fquarter,
+                                        int iter, const float (&gm)[16], const float (&bt)[16], int e, bool leader) {
+    const int cc = e & 7, jt = e >> 3;
+    const int grp = (int)(blockIdx.x / 2) / 4;
+    const int slot = 2 * grp + (iter & 1);
+    const int cta8 = 2 * fquarter + prank;
+    float2 *st = p.ln_stats + (size_t)slot * 8 * 256;
+    int32_t *cnt = p.ln_cnt + 2 * slot;
+    // 1. partial sums
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int j = jt + 32 * k;
+        float s1 = 0.f, s2 = 0.f;
+        if (j < n_this) {
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const uint4 u = *reinterpret_cast<const uint4 *>(stg + j * 256 + (cc + 8 * h2) * 16);
+                const __nv_bfloat162 *hv = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = __bfloat1622float2(hv[q]);
+                    s1 += f.x + f.y;
+                    s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if (cc == 0) __stcg(st + cta8 * 256 + j, make_float2(s1, s2));
+    }
+    __threadfence();
+    ptx::named_bar_sync(1, kEpiThreads);
+    // 2. publish, then wait for the group
+    if (leader) {
+        atomicAdd(cnt, 1);
+        uint32_t spins = 0;
+        while (true) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+            if (v >= 8) break;
+            if (++spins == (1u << 26)) __trap();
+        }
+    }
+    ptx::named_bar_sync(1, kEpiThreads);
+    // 3. statistics and normalisation
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int j = jt + 32 * k;
+        float2 pr = __ldcg(st + cc * 256 + j);                     // lane cc fetches partial cc
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            pr.x += __shfl_xor_sync(0xffffffffu, pr.x, o);
+            pr.y += __shfl_xor_sync(0xffffffffu, pr.y, o);
+        }
+        if (j >= n_this) continue;
+        const float mean = pr.x * (1.f / 1024.f);
+        const float var = fmaxf(fmaf(pr.y, 1.f / 1024.f, -mean * mean), 0.f);
+        const float rs = rsqrtf(var + p.ln_eps);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            uint4 *ptr = reinterpret_cast<uint4 *>(stg + j * 256 + (cc + 8 * h2) * 16);
+            uint4 u = *ptr;
+            __nv_bfloat162 *hv = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(hv[q]);
+                const float a0 = rs * gm[8 * h2 + 2 * q], a1 = rs * gm[8 * h2 + 2 * q + 1];
+                hv[q] = __floats2bfloat162_rn(fmaf(f.x - mean, a0, bt[8 * h2 + 2 * q]),
+                                              fmaf(f.y - mean, a1, bt[8 * h2 + 2 * q + 1]));
+            }
+            *ptr = u;
+        }
+    }
+    // 4. done reading this slot; the group's last reader resets its counters (a fast CTA can
+    //    reuse the slot two tiles later only after every peer has finished this tile)
+    __threadfence();
+    ptx::named_bar_sync(1, kEpiThreads);
+    if (leader) {
+        if (atomicAdd(cnt + 1, 1) == 7) {
+            cnt[0] = 0;
+            cnt[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
 template <int B_MN, int EPI, int OUT_F32, int TRANS, int PAIR = 0, int SM = 0, int SN = 0, int SK = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -154,9 +253,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t prank = PAIR ? ptx::cluster_ctarank() : 0u;
     constexpr int kRowsPerTile = PAIR ? 256 : 128;
     // split: exactly one tile per CTA (cluster along z); else persistent over the tile grid
+    // EPI 4 (fused LayerNorm): pair q = 4 grp + f takes feature tile f of token tiles grp,
+    // grp + G, ... (tile index = 4 * token tile + f with tiles_m = 4), so the four pairs of a
+    // group hold the four 256-feature quarters of the same 256 tokens at the same time.
+    const int pair_q = (int)blockIdx.x / (PAIR ? 2 : 1);
     const int t_first = split ? ((int)(blockIdx.z / p.split) * g.tiles_n + (int)blockIdx.y) * g.tiles_m + (int)blockIdx.x
-                              : (int)blockIdx.x / (PAIR ? 2 : 1);
-    const int t_step = split ? total_tiles : (int)gridDim.x / (PAIR ? 2 : 1);
+                              : (EPI == 4 ? (pair_q < 4 * p.ln_groups ? pair_q : (1 << 30)) : pair_q);
+    const int t_step = split ? total_tiles : (EPI == 4 ? 4 * p.ln_groups : (int)gridDim.x / (PAIR ? 2 : 1));
     const int split_q = split ? (int)(blockIdx.z % p.split) : 0;
     const int kb0 = (int)((int64_t)split_q * g.kb_total / p.split);
     const int kb1 = (int)((int64_t)(split_q + 1) * g.kb_total / p.split);
@@ -332,11 +435,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const CUtensorMap *om = &tmOut;
         if (TRANS && devm && ew == 0 && t_first < total_tiles)
             om = ptx::tmap_patch_extent<1>(&tmOut, smap, p.out_slot + blockIdx.x, (uint32_t)g.rows_b, lane);
-        if (EPI == 3 && TRANS && !split && leader && t_first < total_tiles) {
+        if ((EPI == 3 || EPI == 4) && TRANS && !split && leader && t_first < total_tiles) {
             const TileCoord c = tile_of(g, t_first);
             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
             if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * kRowsPerTile + row_base, c.b, c.n * g.n_full);
             else ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * kRowsPerTile + row_base, c.n * g.n_full, c.b);
+        }
+        // EPI 4: this CTA's 128 features are fixed (feature tile f = t_first % 4): the thread's
+        // two 8-feature chunks of gamma / beta live in registers for the whole kernel
+        float ln_g[16], ln_b[16];
+        int ln_iter = 0;
+        if constexpr (EPI == 4) {
+            const int f0 = (t_first % 4) * 256 + row_base + ((int)(threadIdx.x - 32 * kEpiWarp0) & 7) * 8;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    ln_g[8 * h2 + e] = t_first < total_tiles ? __ldg(p.ln_gamma + f0 + 64 * h2 + e) : 0.f;
+                    ln_b[8 * h2 + e] = t_first < total_tiles ? __ldg(p.ln_beta + f0 + 64 * h2 + e) : 0.f;
+                }
         }
         for (int t = t_first; t < total_tiles; t += t_step) {
             const TileCoord c = tile_of(g, t);
@@ -360,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!split) {
                 if (TRANS) {
                     OutT *so = reinterpret_cast<OutT *>(stg);
-                    if (EPI == 3) {
+                    if (EPI == 3 || EPI == 4) {
                         ptx::mbar_wait(res_bar, res_phase);
                         res_phase ^= 1;
                     }
@@ -381,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int q = 0; q < 16; ++q) {
                             const int o = (c0 + q) * 128 + row_local;
                             float val = EPI == 2 ? v[q] : epi_math<EPI>(v[q], p.alpha, bias_i);
-                            if constexpr (EPI == 3) val += __bfloat162float(reinterpret_cast<__nv_bfloat16 *>(stg)[o]);
+                            if constexpr (EPI == 3 || EPI == 4) val += __bfloat162float(reinterpret_cast<__nv_bfloat16 *>(stg)[o]);
                             if constexpr (OUT_F32) so[o] = val;
                             else so[o] = __float2bfloat16_rn(val);
                         }
@@ -392,6 +509,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (PAIR) ptx::mbar_arrive_cluster(ptx::map_shared_rank(ptx::smem_u32(&tempty[acc]), 0));
                         else ptx::mbar_arrive(&tempty[acc]);
                     }
+                    if constexpr (EPI == 4) {
+                        ptx::named_bar_sync(1, kEpiThreads);          // pre-LN tile complete in staging
+                        ln_tile(p, reinterpret_cast<uint8_t *>(stg), n_this, (int)prank, c.m, ln_iter, ln_g, ln_b,
+                                (int)(threadIdx.x - 32 * kEpiWarp0), leader);
+                        ++ln_iter;
+                    }
                     ptx::fence_async_smem();
                     ptx::named_bar_sync(1, kEpiThreads);
                     if (leader) {
@@ -399,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else ptx::tma_store_3d(om, stg, c.m * kRowsPerTile + row_base, j0, c.b);
                         ptx::tma_store_commit_wait();                 // staging readable again
                         const int tn = t + t_step;
-                        if (EPI == 3 && tn < total_tiles) {
+                        if ((EPI == 3 || EPI == 4) && tn < total_tiles) {
                             const TileCoord cn = tile_of(g, tn);
                             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
                             if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * kRowsPerTile + row_base, cn.b, cn.n * g.n_full);
@@ -625,6 +748,7 @@ cudaError_t launch_umma_gemm(const UmmaLaunch &L) {
             case 0: return launch_t<0, 0, 0, 1, 1>(L, cfg);
             case 1: return launch_t<0, 1, 0, 1, 1>(L, cfg);
             case 2: return launch_t<0, 2, 0, 1, 1>(L, cfg);
+            case 4: return launch_t<0, 4, 0, 1, 1>(L, cfg);
             default: return launch_t<0, 3, 0, 1, 1>(L, cfg);
         }
     }

@@ -68,6 +68,8 @@ _SIGS = {
     "nimble_dense_dyn_dev": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, C.c_int, _vp,
                              _vp],
     "nimble_dense_static": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, C.c_int, C.c_int, _vp],
+    "nimble_dense_ln_dyn": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, C.c_float, _vp, _i64, _i64, _i64, _i64,
+                            _vp],
     "nimble_bmm_dyn": [_vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
                        C.c_float, C.c_int, C.c_int, _vp],
     "nimble_softmax_rows": [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
@@ -269,6 +271,22 @@ def dense_static(x, W, bias, y, epi=EPI_BIAS, residual=None, M=None, stream=None
 def dense_dyn_dev_raw(x_ptr, ldx, W_ptr, ldw, bias_ptr, res_ptr, ldr, y_ptr, ldy, m_ptr, M_max, N, K, epi, stream):
     _check(_lib.nimble_dense_dyn_dev(x_ptr, ldx, W_ptr, ldw, bias_ptr, res_ptr, ldr, y_ptr, ldy, m_ptr, M_max, N, K,
                                      epi, None, stream))
+
+
+def dense_ln_dyn(x, W, bias, residual, gamma, beta, y, eps=1e-12, M=None, stream=None):
+    """y[:M] = LayerNorm(x[:M] W^T + bias + residual[:M]) * gamma + beta (bf16; fused in the GEMM
+    epilogue where the dispatch allows it)."""
+    M = x.shape[0] if M is None else M
+    N, K = W.shape
+    _check(_lib.nimble_dense_ln_dyn(_ptr(x), x.stride(0), _ptr(W), W.stride(0), _ptr(bias), _ptr(residual),
+                                    residual.stride(0), _ptr(gamma), _ptr(beta), eps, _ptr(y), y.stride(0), M, N, K,
+                                    _stream(stream)))
+    return y
+
+
+def dense_ln_dyn_raw(x_ptr, ldx, W_ptr, ldw, bias_ptr, res_ptr, ldr, g_ptr, b_ptr, eps, y_ptr, ldy, M, N, K, stream):
+    _check(_lib.nimble_dense_ln_dyn(x_ptr, ldx, W_ptr, ldw, bias_ptr, res_ptr, ldr, g_ptr, b_ptr, eps, y_ptr, ldy, M,
+                                    N, K, stream))
 
 
 def dense_dyn_raw(x_ptr, ldx, W_ptr, ldw, bias_ptr, res_ptr, ldr, y_ptr, ldy, M, N, K, dt, epi, stream):

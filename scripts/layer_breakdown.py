@@ -2,7 +2,8 @@
 64 requests, L ~ U{1..512}, 24 layers).  The full forward is captured in a CUDA graph and
 timed; then the same forward with one op class left out (its output buffer keeps stale
 data, so only the timing is meaningful) — the difference is that class's in-context time,
-PDL overlap and L2 residency included."""
+PDL overlap and L2 residency included.  "fused_ln" is BertPacked.layer itself (O-proj + LN1
+and FFN2 + LN2 as nimble_dense_ln_dyn: LN2 fuses); "full" is the unfused 7-launch sequence."""
 import json
 import os
 import sys
@@ -43,7 +44,8 @@ def main():
     off = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
     X = synth.device_normal(T, cfg["d"], seed=3)
     res = {"tokens": T}
-    for skip in ((), ("ln",), ("attn",), ("qkv",), ("o",), ("ffn1",), ("ffn2",)):
+    graphs = {}
+    for skip in (("fused",), (), ("ln",), ("attn",), ("qkv",), ("o",), ("ffn1",), ("ffn2",)):
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         g = torch.cuda.CUDAGraph()
@@ -52,27 +54,34 @@ def main():
                 src = X.data_ptr()
                 for li in range(cfg["layers"]):
                     dst = enc.X[li & 1].data_ptr()
-                    layer(enc, src, dst, T, off.data_ptr(), 64, int(lens.max()), li, s.cuda_stream, skip)
+                    if skip == ("fused",):             # BertPacked.layer (nimble_dense_ln_dyn)
+                        enc.layer(src, dst, T, off.data_ptr(), 64, int(lens.max()), li, s.cuda_stream)
+                    else:
+                        layer(enc, src, dst, T, off.data_ptr(), 64, int(lens.max()), li, s.cuda_stream, skip)
                     src = dst
             fwd()
             torch.cuda.synchronize()
             with torch.cuda.graph(g, stream=s):
                 fwd()
         torch.cuda.current_stream().wait_stream(s)
-        for _ in range(3):
-            g.replay()
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(7):
+        key = "fused_ln" if skip == ("fused",) else ("full" if not skip else "without_" + "_".join(skip))
+        graphs[key] = g
+    # interleaved rounds: every variant sees the same mix of power / clock states
+    ts = {k: [] for k in graphs}
+    for g in graphs.values():
+        g.replay()
+    torch.cuda.synchronize()
+    for _ in range(9):
+        for k, g in graphs.items():
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             g.replay()
             b.record()
             torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        ms = float(np.median(ts))
-        res["full" if not skip else "without_" + "_".join(skip)] = ms
-        print(("full" if not skip else "without " + ",".join(skip)), "%.3f ms" % ms, flush=True)
+            ts[k].append(a.elapsed_time(b))
+    for k in graphs:
+        res[k] = float(np.median(ts[k]))
+        print(k, "%.3f ms" % res[k], flush=True)
     full = res["full"]
     print(json.dumps({k: round(full - v, 3) for k, v in res.items() if k.startswith("without")}))
 

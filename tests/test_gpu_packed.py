@@ -74,7 +74,7 @@ def test_packed_bert_large_layer(nb, orc, lens):
     cfg = synth.BERT_LARGE
     w = synth.bert_weights(cfg, seed=0, layers=1)
     T = sum(lens)
-    enc = BertPacked(cfg, w, max_tokens=T + 8)
+    enc = BertPacked(cfg, w, max_tokens=T + 8, fused_ln=False)     # every intermediate materialised
     x = synth.bert_input(T, cfg["d"], seed=900 + T).cuda()
     off = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
     y = enc.forward(x, off, max(lens))
@@ -92,5 +92,31 @@ def test_packed_bert_large_layer(nb, orc, lens):
         assert _err(y[o:o + L], yref) <= 2e-2
         full = orc.bert_layer(dd(x, o, o + L), W, cfg["heads"])
         print(f"packed layer L={L}: free-running err {_err(y[o:o + L], full):.3e}")
+        assert _err(y[o:o + L], full) <= 0.25
+        o += L
+
+
+@pytest.mark.parametrize("lens", [[1, 33, 128, 300], [512, 512, 512, 512, 100, 7]])
+def test_packed_bert_large_layer_fused_ln(nb, orc, lens):
+    """The fused-LN layer (O-proj + LN1, FFN2 + LN2 through nimble_dense_ln_dyn; LN2 runs in the
+    FFN2 epilogue at T >= 2048), teacher-forced per op from the device intermediates."""
+    from paper_2006_03031_b200.bert import BertPacked
+    cfg = synth.BERT_LARGE
+    w = synth.bert_weights(cfg, seed=0, layers=1)
+    T = sum(lens)
+    enc = BertPacked(cfg, w, max_tokens=T + 8)
+    x = synth.bert_input(T, cfg["d"], seed=910 + T).cuda()
+    off = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
+    y = enc.forward(x, off, max(lens))
+    torch.cuda.synchronize()
+    W = {k: v.double().numpy() for k, v in w[0].items()}
+    dd = lambda t, a, b: t[a:b].double().cpu().numpy()
+    o = 0
+    for L in lens:
+        v, _ = orc.dense(dd(enc.ctx, o, o + L), W["Wo"], W["bo"], dd(x, o, o + L), 3)
+        assert _err(enc.H1[o:o + L], orc.layernorm(v, W["g1"], W["be1"])) <= 2e-2
+        v, _ = orc.dense(dd(enc.F, o, o + L), W["W2"], W["b2"], dd(enc.H1, o, o + L), 3)
+        assert _err(y[o:o + L], orc.layernorm(v, W["g2"], W["be2"])) <= 2e-2
+        full = orc.bert_layer(dd(x, o, o + L), W, cfg["heads"])
         assert _err(y[o:o + L], full) <= 0.25
         o += L
