@@ -28,4 +28,12 @@ if [[ $STEPS == *ncu* ]]; then
       python bench.py --profile --steps 1 --warmup 1 > $OUT/ncu_full.log 2>&1; echo "ncu-full rc=$?" >> $OUT/ncu_full.log
   python scripts/gemm_traffic.py $OUT/prof_gemm.ncu-rep > $OUT/gemm_traffic.json
   tail -3 $OUT/ncu_full.log
+  # one attention launch of the bench configuration (layer 5)
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:attention -s 4 -c 1 -o $OUT/prof_attn -f \
+      python bench.py --profile --steps 1 --warmup 1 > $OUT/ncu_attn.log 2>&1; echo "ncu-attn rc=$?" >> $OUT/ncu_attn.log
+  tail -2 $OUT/ncu_attn.log
+fi
+if [[ $STEPS == *configs* ]]; then
+  timeout 900 python scripts/bench_configs.py ${CONFIGS:-2,3,4} > $OUT/configs.log 2>&1; echo "configs rc=$?" >> $OUT/configs.log
+  tail -8 $OUT/configs.log
 fi

@@ -28,10 +28,16 @@ def main(rep, top=12):
     h = src[i]
     rows = src[i + 1:]
     S = h.index("Warp Stall Sampling (All Samples)")
-    tot = sum(int(x[S] or 0) for x in rows if len(x) > S)
+
+    def num(x):                  # the source page repeats header rows per kernel: skip non-numbers
+        try:
+            return int(x[S] or 0) if len(x) > S else 0
+        except ValueError:
+            return 0
+    tot = sum(num(x) for x in rows)
     print(f"  stall samples: {tot}")
     try:
-        for x in sorted(rows, key=lambda x: -int(x[S] or 0))[:top]:
+        for x in sorted(rows, key=lambda x: -num(x))[:top]:
             print(f"    {x[S]:>6} {x[1][:100]}")
     except BrokenPipeError:
         pass
