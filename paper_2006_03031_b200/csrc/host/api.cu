@@ -130,7 +130,8 @@ void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
     L.p.dbg = dbg;
     const int kb_per_split = (L.p.kb_total + L.p.split - 1) / L.p.split;
     const int ob = L.out_f32 ? 4 : 2;
-    int st = kb_per_split < 8 ? kb_per_split : 8;
+    static const int max_st = [] { const char *e = std::getenv("NIMBLE_MAX_STAGES"); return e ? std::atoi(e) : 8; }();
+    int st = kb_per_split < max_st ? kb_per_split : max_st;     // NIMBLE_MAX_STAGES: experiment only
     if (st < 1) st = 1;
     // largest depth that fits next to the epilogue staging
     while (st > 1 && umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair) > 232448) --st;
