@@ -92,6 +92,10 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
     return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
                        __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
 }
+#ifndef NIMBLE_ATTN_LAZY
+#define NIMBLE_ATTN_LAZY 8.0f        // lazy-rescale threshold (log2 units); 0 = rescale on every growth
+#endif
+constexpr float kLazy = NIMBLE_ATTN_LAZY;
 #ifndef NIMBLE_ATTN_POLY
 #define NIMBLE_ATTN_POLY 2          // pairs out of every 8 whose exp2 runs on the FMA pipes
 #endif
@@ -413,8 +417,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             rd[half * 128 + q] = mx;
             ptx::named_bar_sync(1, kSoftmaxThreads);
             if (tr) ATT_TRACE(tb, 2);
-            const float m_new = fmaxf(m_run, fmaxf(rd[q], rd[128 + q]));
-            const float alpha = ptx::ex2_approx((m_run - m_new) * sl2);   // m_run = -inf -> 0
+            // lazy rescaling: the exponent base m_run moves only when the row max grew by more
+            // than 2^kLazy in exp2 units (P then stays <= 2^kLazy, exact in fp32 / bf16 range;
+            // l and O use the same base, so the final O / l is unchanged).  Both key halves of
+            // a row see the same maxima, so they take the same decision.
+            const float m_blk = fmaxf(rd[q], rd[128 + q]);
+            const bool grow = (m_blk - m_run) * sl2 > kLazy;               // m_run = -inf: always
+            const float m_new = grow ? m_blk : m_run;
+            const float alpha = grow ? ptx::ex2_approx((m_run - m_new) * sl2) : 1.f;   // -inf -> 0
             const float ms = m_new * sl2;
             float2 sa = make_float2(0.f, 0.f), sb = sa;
             if (full) {
@@ -465,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 *reinterpret_cast<uint4 *>(rowp + ((c ^ (q & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
             }
             // rescale this row's O half (32 of the 64 output columns) when the running max grew
-            if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {
+            if (j > 0 && __any_sync(0xffffffffu, grow)) {
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     float t[16];

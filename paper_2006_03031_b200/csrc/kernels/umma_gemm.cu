@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         bool first = true;
+        int nkb_p = 0;                                    // debug: k-blocks issued (NIMBLE_DBG & 4)
         // devm: the first tile (t_first < tiles_m) exists for every M >= 1, so its weights can
         // still be requested before the wait; otherwise wait and read M first.
         bool devm_pending = devm;
@@ -368,6 +369,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             for (; kb < kb1; ++kb) {
                 ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+                if ((p.dbg & 4) && trace && cta_lin == 0 && nkb_p < 4096) p.trace[16384 + nkb_p] = clock64();
+                ++nkb_p;
                 if (arms) ptx::mbar_arrive_expect_tx(&full_bar[stage], tx);
                 load_a(stage, kb);
                 load_b(stage, kb);
@@ -384,15 +387,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
+        int nkb_m = 0, ntile_m = 0;                       // debug: k-blocks / tiles consumed (NIMBLE_DBG & 4)
         for (int t = t_first; t < total_tiles; t += t_step) {
             const TileCoord c = tile_of(g, t);
             const int n_this = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
             const uint32_t idesc = ptx::idesc_bf16(PAIR ? 256u : 128u, (uint32_t)n_this, B_MN);
             ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);     // epilogue drained this accumulator
+            if ((p.dbg & 4) && trace && cta_lin == 0 && ntile_m < 256) p.trace[24576 + ntile_m] = clock64();
+            ++ntile_m;
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)(acc * g.n_full);
             for (int kb = kb0; kb < kb1; ++kb) {
                 ptx::mbar_wait(&full_bar[stage], phase);
+                if ((p.dbg & 4) && trace && cta_lin == 0 && nkb_m < 4096) {
+                    p.trace[8192 + nkb_m] = clock64();
+                    if (nkb_m == 0) { p.trace[30000] = clock64(); p.trace[30001] = ptx::globaltimer(); }
+                    p.trace[30002] = clock64();
+                    p.trace[30003] = ptx::globaltimer();
+                }
+                ++nkb_m;
                 ptx::tc_fence_after();
                 if (kb == kb0 && t == t_first) NIMBLE_TRACE(2);
                 const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
