@@ -512,6 +512,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int o = (c0 + q) * 128 + row_local;
                             float val = EPI == 2 ? v[q] : epi_math<EPI>(v[q], p.alpha, bias_i);
                             if constexpr (EPI == 3 || EPI == 4) val += __bfloat162float(reinterpret_cast<__nv_bfloat16 *>(stg)[o]);
+                            // NIMBLE_DBG & 16 (experiment only): drop the output (no staging, no store) to
+                            // measure what the epilogue's shared-memory traffic costs the main loop
+                            if (p.dbg & 16) { if (val == 12345.f) asm volatile("trap;"); continue; }
                             if constexpr (OUT_F32) so[o] = val;
                             else so[o] = __float2bfloat16_rn(val);
                         }
@@ -530,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ptx::fence_async_smem();
                     ptx::named_bar_sync(1, kEpiThreads);
-                    if (leader) {
+                    if (leader && !(p.dbg & 16)) {
                         if (p.out_batch_mid) ptx::tma_store_3d(om, stg, c.m * kRowsPerTile + row_base, c.b, j0);
                         else ptx::tma_store_3d(om, stg, c.m * kRowsPerTile + row_base, j0, c.b);
                         ptx::tma_store_commit_wait();                 // staging readable again
