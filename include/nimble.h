@@ -171,8 +171,9 @@ int nimble_dense_ln_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, 
  * (N, K)); the true extent M is the int32 at M_dev (device memory, 1 <= M <= M_max, read
  * by the kernel after its grid-dependency wait, so an earlier kernel or copy on the stream
  * may write it).  The kernel runs the residue dispatch on the device: family 1 of
- * DISPATCH.md with split_k = 1 and the token tile of the registered schedule (else 128),
- * the variant limit c current at launch.  Writes y rows [0, M) only (the store's tensor
+ * DISPATCH.md with the token tile of the registered schedule (else 128) and the variant
+ * limit c current at launch; split_k is the host rule's (schedule cap, else 8) when M_max
+ * fits one token tile (then it is the same for every M <= M_max), else 1.  Writes y rows [0, M) only (the store's tensor
  * map is re-encoded on the device with extent M; rows [M, M_max) of y are untouched);
  * x rows in [M, M_max) are read but only feed unstored columns.  dispatch_dev: NULL or a
  * device nimble_dispatch that receives the device's dispatch decision.  A device extent

@@ -402,9 +402,13 @@ extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, i
         (epi == NIMBLE_EPI_BIAS_RESIDUAL && (!aligned16(residual) || (ldr * 2) % 16)))
         return fail(NIMBLE_E_ALIGN, "nimble_dense_dyn_dev: TMA needs 16-B aligned x/W/y/residual and ld*2 % 16 == 0");
     int32_t t = 0, cap = 8;
-    dense_schedule(N, K, &t, &cap);                    // tuned token tile (split is always 1 here)
+    dense_schedule(N, K, &t, &cap);                    // tuned token tile / split cap
     nimble_dispatch d;
-    dispatch_umma_t(1, M_max, N, K, &d, t > 0 ? t : 128, 1);   // launch geometry for the bound
+    // split-K needs a launch grid that does not depend on M: allowed when the bound fits ONE
+    // token tile, where the host rule's split (a function of the tile count) is the same for
+    // every M <= M_max; otherwise the device dispatch runs split 1
+    dispatch_umma_t(1, M_max, N, K, &d, t > 0 ? t : 128, cap);
+    if (d.grid[1] != 1) dispatch_umma_t(1, M_max, N, K, &d, t > 0 ? t : 128, 1);   // launch geometry for the bound
     UmmaLaunch L;
     std::memset(&L, 0, sizeof(L));
     L.p.rows_a = (int32_t)N;
@@ -413,7 +417,7 @@ extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, i
     L.p.n_tail = d.r ? d.umma_n_tail : d.umma_n_full;
     L.p.box_n = d.umma_n_full;                         // fixed box: the tail width is decided on device
     L.p.kb_total = (int32_t)((K + 63) / 64);
-    L.p.split = 1;
+    L.p.split = d.split_k;
     L.epi = epi;
     L.transposed = 1;
     L.p.alpha = 1.f;

@@ -82,9 +82,10 @@ __device__ __forceinline__ TileCoord tile_of(const Geo &g, int t) {
     return c;
 }
 
-// Device-side residue dispatch for nimble_dense_dyn_dev (DISPATCH.md family 1 with split 1,
-// the upper-bound form of P:268-271): M is data read after the grid-dependency wait, the
-// rule is the host's, so the recorded dispatch is bit-identical to the oracle's.
+// Device-side residue dispatch for nimble_dense_dyn_dev (DISPATCH.md family 1, the
+// upper-bound form of P:268-271): M is data read after the grid-dependency wait, the rule is
+// the host's, so the recorded dispatch is bit-identical to the oracle's.  The split-K factor
+// is fixed at launch (the host rule's, when the bound fits one token tile; else 1).
 __device__ __forceinline__ void devm_geometry(const UmmaParams &p, Geo &g, int &total_tiles, bool record) {
     const int M = *p.m_dev;
     if (M < 1 || M > p.rows_b) __trap();              // outside [1, M_max]: caller bug, fail loudly
@@ -100,10 +101,11 @@ __device__ __forceinline__ void devm_geometry(const UmmaParams &p, Geo &g, int &
     if (record && p.rec) {
         nimble_dispatch d{};
         d.family = 1; d.tile_t = t; d.granule = 16; d.n_classes = ncls; d.residue_class = cls;
-        d.variant = variant; d.split_k = 1; d.umma_m = 128; d.umma_n_full = t;
+        d.variant = variant; d.split_k = p.split; d.umma_m = 128; d.umma_n_full = t;
         d.umma_n_tail = r ? g.n_tail : 0; d.k = k; d.r = r;
-        d.grid[0] = g.tiles_m; d.grid[1] = g.tiles_n; d.grid[2] = p.batch;
-        d.cluster[0] = d.cluster[1] = d.cluster[2] = 1;
+        d.grid[0] = g.tiles_m; d.grid[1] = g.tiles_n; d.grid[2] = p.batch * p.split;
+        d.cluster[0] = d.cluster[1] = 1;
+        d.cluster[2] = p.split;
         *p.rec = d;
     }
 }
