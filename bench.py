@@ -354,33 +354,50 @@ def main():
         host_in = torch.empty((max(my_tokens, 1), d), dtype=torch.bfloat16, pin_memory=True)
         host_in.copy_(X_mine.cpu())
         host_out = torch.empty((len(ids), d), dtype=torch.bfloat16, pin_memory=True)
-        X_dev = torch.empty_like(X_mine)
+        # double-buffered input staging: step i+1's host->device copy runs on a copy stream
+        # while step i computes (every step's copy is still inside the timed region; step 0's
+        # is exposed).  A buffer is rewritten only after the host saw the step that read it.
+        copy_stream = torch.cuda.Stream()
+        X_bufs = [torch.empty_like(X_mine) for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
 
-        def e2e_step():
-            X_dev.copy_(host_in, non_blocking=True)
-            run_local(X_dev)
+        def issue_copy(i, after=None):
+            with torch.cuda.stream(copy_stream):
+                if after is not None:
+                    copy_stream.wait_event(after)
+                X_bufs[i % 2].copy_(host_in, non_blocking=True)
+                ready[i % 2].record(copy_stream)
+
+        def e2e_step(i, last):
+            torch.cuda.current_stream().wait_event(ready[i % 2])
+            if not last:
+                issue_copy(i + 1)
+            run_local(X_bufs[i % 2])
             host_out.copy_(out, non_blocking=True)
             r = gather_results(ids_t, out, max_count, world, rank)
             torch.cuda.current_stream().synchronize()
             return r
 
-        for _ in range(2):
-            e2e_step()
+        issue_copy(0)
+        for i in range(2):
+            e2e_step(i, i == 1)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         a0 = torch.cuda.Event(enable_timing=True)
         a1 = torch.cuda.Event(enable_timing=True)
         a0.record()
-        for _ in range(args.steps):
-            e2e_step()
+        issue_copy(0, after=a0)                   # the first step's inputs cross PCIe inside the region
+        for i in range(args.steps):
+            e2e_step(i, i == args.steps - 1)
         a1.record()
         torch.cuda.synchronize()
         te = torch.tensor([a0.elapsed_time(a1) / 1e3], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": R * args.steps / float(te.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(my_tokens * d * 2), "d2h_bytes_per_step": int(len(ids) * d * 2)}
+               "h2d_bytes_per_step": int(my_tokens * d * 2), "d2h_bytes_per_step": int(len(ids) * d * 2),
+               "pipelining": "H2D of step i+1 on a copy stream overlaps step i; D2H + host sync every step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
