@@ -210,8 +210,9 @@ int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const void *B, i
  * nondecreasing, seq_off[R] = T.  max_len >= every L_i.  One persistent launch (at
  * most 2 CTAs per SM walking a longest-request-first work list of (query tile, head,
  * request) items built on the device from seq_off); S and P stay on chip (TMEM /
- * smem).  head_dim must be 64, max_len <= 8192 and R <= 1024 (E_UNSUPPORTED
- * otherwise); qkv/out 16-byte aligned with ld*2 % 16 == 0 (E_ALIGN).
+ * smem; more than 1024 requests run as consecutive launches of 1024).  head_dim must be
+ * 64 and max_len <= 8192 (E_UNSUPPORTED otherwise); qkv/out 16-byte aligned with
+ * ld*2 % 16 == 0 (E_ALIGN).
  * ------------------------------------------------------------------------- */
 int nimble_attention_varlen(const void *qkv, int64_t ld_qkv, int64_t T, const int32_t *seq_off, int32_t R,
                             int32_t max_len, int32_t heads, int32_t head_dim, float scale, void *out,

@@ -531,9 +531,7 @@ static int attention_impl(const void *qkv, int64_t ld_qkv, int64_t T, const int3
         return fail(NIMBLE_E_EXTENT, "nimble_attention_varlen: extents must be >= 1");
     if (head_dim != 64) return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen: head_dim must be 64");
     if (max_len > 8192) return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen: max_len > 8192 not built");
-    if (R > attention_max_requests())
-        return fail(NIMBLE_E_UNSUPPORTED, "nimble_attention_varlen: more than " + std::to_string(attention_max_requests()) +
-                                              " requests in one launch");
+
     if (ld_qkv < 3LL * heads * head_dim || ld_out < (int64_t)heads * head_dim)
         return fail(NIMBLE_E_SHAPE, "nimble_attention_varlen: leading dimension too small");
     if (!aligned16(qkv) || !aligned16(out) || (ld_qkv * 2) % 16 || (ld_out * 2) % 16)
@@ -559,9 +557,22 @@ static int attention_impl(const void *qkv, int64_t ld_qkv, int64_t T, const int3
         e = next_slot_block(g_attn_slots, &slots);
         if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen_dev slot ring", e);
     }
-    e = launch_attention_varlen(tmQK, tmV, seq_off, R, max_len, heads, scale, static_cast<__nv_bfloat16 *>(out), ld_out,
-                                static_cast<cudaStream_t>(stream), slots, g_trace);
-    if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen launch", e);
+    // the kernel's work list holds attention_max_requests() requests: longer streams run as
+    // consecutive launches over request chunks (seq_off entries are absolute token offsets, so a
+    // chunk is just a shifted seq_off pointer; the device-extent form reads its chunk's end)
+    const int chunk = attention_max_requests();
+    for (int32_t r0 = 0; r0 < R; r0 += chunk) {
+        const int32_t Rc = R - r0 < chunk ? R - r0 : chunk;
+        CUtensorMap *sl = slots;
+        if (dev && r0 > 0) {
+            e = next_slot_block(g_attn_slots, &sl);
+            if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen_dev slot ring", e);
+        }
+        e = launch_attention_varlen(tmQK, tmV, seq_off + r0, Rc, max_len, heads, scale,
+                                    static_cast<__nv_bfloat16 *>(out), ld_out, static_cast<cudaStream_t>(stream), sl,
+                                    g_trace);
+        if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen launch", e);
+    }
     clear_error();
     return NIMBLE_OK;
 }

@@ -120,3 +120,22 @@ def test_packed_bert_large_layer_fused_ln(nb, orc, lens):
         full = orc.bert_layer(dd(x, o, o + L), W, cfg["heads"])
         assert _err(y[o:o + L], full) <= 0.25
         o += L
+
+
+def test_attention_varlen_more_requests_than_one_work_list(nb, orc):
+    """R = 1300 > 1024: the library runs request chunks as consecutive launches; lengths
+    1..12 (every residue of a tiny tile), checked on a sample of requests across the chunk edge."""
+    H, dh = 2, 64
+    d = H * dh
+    lens = [1 + (i * 7) % 12 for i in range(1300)]
+    T = sum(lens)
+    qkv = synth.normal((T, 3 * d), 1.0, 4242).cuda()
+    off_h = np.concatenate([[0], np.cumsum(lens)])
+    off = torch.tensor(off_h, dtype=torch.int32, device="cuda")
+    out = torch.empty((T, d), dtype=torch.bfloat16, device="cuda")
+    nb.attention_varlen(qkv, off, len(lens), max(lens), H, out, T=T)
+    torch.cuda.synchronize()
+    for i in (0, 5, 1022, 1023, 1024, 1025, 1299):
+        o, L = int(off_h[i]), lens[i]
+        ref = _attn_ref(orc, qkv[o:o + L].double().cpu().numpy(), L, H)
+        assert _err(out[o:o + L], ref) <= 2e-2, (i, L)
