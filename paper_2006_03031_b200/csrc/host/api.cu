@@ -96,7 +96,9 @@ int encode_out(CUtensorMap *m, void *base, bool f32, int64_t rows_i, int64_t row
     cuuint32_t box[3], estr[3] = {1, 1, 1};
     const bool mid = (batch > 1) && (bstride < ld);
     dims[0] = (cuuint64_t)rows_i;
-    box[0] = 128;
+    // bf16 outputs / residuals: 64-feature boxes in the 128-B swizzle layout the kernel's
+    // stmatrix / ldmatrix epilogue stages (two boxes per 128-feature tile); fp32: plain 128
+    box[0] = f32 ? 128 : 64;
     if (mid) {
         dims[1] = (cuuint64_t)batch;  strides[0] = (cuuint64_t)bstride * es; box[1] = 1;
         dims[2] = (cuuint64_t)rows_j; strides[1] = (cuuint64_t)ld * es;      box[2] = (cuuint32_t)box_j;
@@ -107,7 +109,8 @@ int encode_out(CUtensorMap *m, void *base, bool f32, int64_t rows_i, int64_t row
         box[2] = 1;
     }
     CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims,
-                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          f32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(NIMBLE_E_CUDA, "cuTensorMapEncodeTiled(out) failed (code " + std::to_string((int)r) + ")");
     *batch_mid = mid ? 1 : 0;

@@ -117,6 +117,39 @@ __device__ __forceinline__ float epi_math(float acc, float alpha, float bias_i) 
     else return acc + bias_i;      // EPI 1, and 3 before the residual add
 }
 
+// bf16 output staging of the transposed (lane = feature) accumulator: two sub-tiles
+// [tokens][64 features] of 128-B rows in the TMA SWIZZLE_128B layout (16-B chunk c of row j at
+// c ^ (j & 7)), written by stmatrix.trans from the tcgen05.ld.16x256b fragment (thread t: lanes
+// t/4 and t/4 + 8, token columns 2(t%4), 2(t%4)+1): full 128-B shared-memory wavefronts
+// instead of one 64-B STS.16 wavefront per value column.
+__device__ __forceinline__ uint32_t stg_addr(uint32_t stg, int n_stage, int feat, int tok) {
+    const int sub = feat >> 6, cc = (feat >> 3) & 7;
+    return stg + (uint32_t)(sub * n_stage * 128 + tok * 128 + ((cc ^ (tok & 7)) << 4));
+}
+__device__ __forceinline__ void tmem_ld_16x256b_x2(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void stmatrix_x4_trans(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b),
+                 "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t addr, uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(addr)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u));
+}
+
 // Fused LayerNorm over a 256-token x 1024-feature row block held by the 8 CTAs of a group (EPI 4).
 // This CTA's staging holds bf16 pre-LN sums v = acc + bias + residual for its 128 features
 // (feature-contiguous rows of 256 B, one per token).  Thread e (of 256): feature chunks
@@ -127,8 +160,9 @@ __device__ __forceinline__ float epi_math(float acc, float alpha, float bias_i) 
 //   3. mean = S1 / 1024, var = S2 / 1024 - mean^2 (biased, fp32), y = (v - mean) rsqrt(var + eps)
 //      gamma + beta -> bf16 back into staging (then the usual clipped TMA store)
 // The partials are summed in a fixed butterfly order: the result is deterministic.
-__device__ __forceinline__ void ln_tile(const UmmaParams &p, uint8_t *stg, int n_this, int prank, int fquarter,
-                                        int iter, const float (&gm)[16], const float (&bt)[16], int e, bool leader) {
+__device__ __forceinline__ void ln_tile(const UmmaParams &p, uint8_t *stg, int n_stage, int n_this, int prank,
+                                        int fquarter, int iter, const float (&gm)[16], const float (&bt)[16], int e,
+                                        bool leader) {
     const int cc = e & 7, jt = e >> 3;
     const int grp = (int)(blockIdx.x / 2) / 4;
     const int slot = 2 * grp + (iter & 1);
@@ -143,7 +177,7 @@ __device__ __forceinline__ void ln_tile(const UmmaParams &p, uint8_t *stg, int n
         if (j < n_this) {
 #pragma unroll
             for (int h2 = 0; h2 < 2; ++h2) {
-                const uint4 u = *reinterpret_cast<const uint4 *>(stg + j * 256 + (cc + 8 * h2) * 16);
+                const uint4 u = *reinterpret_cast<const uint4 *>(stg + h2 * n_stage * 128 + j * 128 + ((cc ^ (j & 7)) << 4));
                 const __nv_bfloat162 *hv = reinterpret_cast<const __nv_bfloat162 *>(&u);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -190,7 +224,7 @@ __device__ __forceinline__ void ln_tile(const UmmaParams &p, uint8_t *stg, int n
         const float rs = rsqrtf(var + p.ln_eps);
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
-            uint4 *ptr = reinterpret_cast<uint4 *>(stg + j * 256 + (cc + 8 * h2) * 16);
+            uint4 *ptr = reinterpret_cast<uint4 *>(stg + h2 * n_stage * 128 + j * 128 + ((cc ^ (j & 7)) << 4));
             uint4 u = *ptr;
             __nv_bfloat162 *hv = reinterpret_cast<__nv_bfloat162 *>(&u);
 #pragma unroll
@@ -453,8 +487,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if ((EPI == 3 || EPI == 4) && TRANS && !split && leader && t_first < total_tiles) {
             const TileCoord c = tile_of(g, t_first);
             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
-            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * kRowsPerTile + row_base, c.b, c.n * g.n_full);
-            else ptx::tma_load_3d(stg, &tmRes, res_bar, c.m * kRowsPerTile + row_base, c.n * g.n_full, c.b);
+            for (int sb = 0; sb < 2; ++sb)             // two swizzled [tokens][64 features] boxes
+                ptx::tma_load_3d(stg + sb * n_stage * 128, &tmRes, res_bar, c.m * kRowsPerTile + row_base + 64 * sb,
+                                 c.n * g.n_full, c.b);
         }
         // EPI 4: this CTA's 128 features are fixed (feature tile f = t_first % 4): the thread's
         // two 8-feature chunks of gamma / beta live in registers for the whole kernel
@@ -496,29 +531,85 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mbar_wait(res_bar, res_phase);
                         res_phase ^= 1;
                     }
-                    for (int c0 = half * 16; c0 < n_this; c0 += 16 * kEpiGroups) {
-                        float v[16];
-                        ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
-                        if constexpr (EPI == 2) {
-                            // GELU on pairs of token columns (FFMA2 / FMUL2): the epilogue of the
-                            // GELU GEMM is issue-bound, the pairs halve its polynomial work
+                    if constexpr (!OUT_F32) {
+                        // fragment path: per 16 token columns, two 16x256b.x2 loads (TMEM lane rows
+                        // q32 + {0..15} and q32 + {16..31}), math on (feature, token pair) values,
+                        // bf16x2 packs, stmatrix.trans into the swizzled staging (+ ldmatrix.trans
+                        // of the residual in the same fragment)
+                        const uint32_t st_base = ptx::smem_u32(stg);
+                        const int tq = (int)lane >> 2, tc = 2 * ((int)lane & 3);
+                        float bsv[4] = {0.f, 0.f, 0.f, 0.f};  // bias of features q32 + {tq, tq+8, tq+16, tq+24}
+                        if constexpr (EPI >= 1) {
 #pragma unroll
-                            for (int q = 0; q < 16; q += 2) {
-                                const float2 g = ptx::gelu_erf2(ptx::fadd2(make_float2(v[q], v[q + 1]), ptx::f2(bias_i)));
-                                v[q] = g.x;
-                                v[q + 1] = g.y;
+                            for (int h4 = 0; h4 < 4; ++h4) {
+                                const int fi = c.m * kRowsPerTile + row_base + quarter * 32 + tq + 8 * h4;
+                                bsv[h4] = fi < g.rows_a ? __ldg(p.bias + fi) : 0.f;
                             }
                         }
+                        // this thread's stmatrix / ldmatrix row: matrix (lane / 8) of the x4 group, row lane % 8
+                        const int mi = (int)lane >> 3, mr = (int)lane & 7;
+                        for (int c0 = half * 16; c0 < n_this; c0 += 16 * kEpiGroups) {
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) {
-                            const int o = (c0 + q) * 128 + row_local;
-                            float val = EPI == 2 ? v[q] : epi_math<EPI>(v[q], p.alpha, bias_i);
-                            if constexpr (EPI == 3 || EPI == 4) val += __bfloat162float(reinterpret_cast<__nv_bfloat16 *>(stg)[o]);
-                            // NIMBLE_DBG & 16 (experiment only): drop the output (no staging, no store) to
-                            // measure what the epilogue's shared-memory traffic costs the main loop
-                            if (p.dbg & 16) { if (val == 12345.f) asm volatile("trap;"); continue; }
-                            if constexpr (OUT_F32) so[o] = val;
-                            else so[o] = __float2bfloat16_rn(val);
+                            for (int hl = 0; hl < 2; ++hl) {       // TMEM lanes q32 + 16 hl + {0..15}
+                                uint32_t r[8];
+                                tmem_ld_16x256b_x2(tmem_base + ((uint32_t)(quarter * 32 + 16 * hl) << 16) +
+                                                       (uint32_t)(acc * g.n_full + c0), r);
+                                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                                // matrices: 0 = (features +0..7, tokens c0..7), 1 = (+8..15, c0..7),
+                                //           2 = (+0..7, c0+8..15),         3 = (+8..15, c0+8..15)
+                                const int fl0 = quarter * 32 + 16 * hl;      // first feature (CTA-local)
+                                const uint32_t a_me = stg_addr(st_base, n_stage, fl0 + 8 * (mi & 1), c0 + 8 * (mi >> 1) + mr);
+                                float2 x[4];
+#pragma unroll
+                                for (int m = 0; m < 4; ++m)
+                                    x[m] = make_float2(__uint_as_float(r[(m & 1) * 2 + (m >> 1) * 4]),
+                                                       __uint_as_float(r[(m & 1) * 2 + (m >> 1) * 4 + 1]));
+                                float2 rs[4];
+                                if constexpr (EPI == 3 || EPI == 4) {
+                                    uint32_t q0, q1, q2, q3;
+                                    ldmatrix_x4_trans(a_me, q0, q1, q2, q3);
+                                    rs[0] = unpack_bf16(q0); rs[1] = unpack_bf16(q1);
+                                    rs[2] = unpack_bf16(q2); rs[3] = unpack_bf16(q3);
+                                }
+                                uint32_t o[4];
+#pragma unroll
+                                for (int m = 0; m < 4; ++m) {
+                                    const float bb = bsv[2 * hl + (m & 1)];
+                                    float2 y2;
+                                    if constexpr (EPI == 0) y2 = ptx::fmul2(x[m], ptx::f2(p.alpha));
+                                    else if constexpr (EPI == 2) y2 = ptx::gelu_erf2(ptx::fadd2(x[m], ptx::f2(bb)));
+                                    else y2 = ptx::fadd2(x[m], ptx::f2(bb));
+                                    if constexpr (EPI == 3 || EPI == 4) y2 = ptx::fadd2(y2, rs[m]);
+                                    o[m] = pack_bf16(y2.x, y2.y);
+                                }
+                                stmatrix_x4_trans(a_me, o[0], o[1], o[2], o[3]);
+                            }
+                        }
+                    } else {
+                    for (int c0 = half * 16; c0 < n_this; c0 += 16 * kEpiGroups) {
+                            float v[16];
+                            ptx::tmem_ld16(tmem_row + (uint32_t)c0, v);
+                            if constexpr (EPI == 2) {
+                                // GELU on pairs of token columns (FFMA2 / FMUL2): the epilogue of the
+                                // GELU GEMM is issue-bound, the pairs halve its polynomial work
+    #pragma unroll
+                                for (int q = 0; q < 16; q += 2) {
+                                    const float2 g = ptx::gelu_erf2(ptx::fadd2(make_float2(v[q], v[q + 1]), ptx::f2(bias_i)));
+                                    v[q] = g.x;
+                                    v[q + 1] = g.y;
+                                }
+                            }
+    #pragma unroll
+                            for (int q = 0; q < 16; ++q) {
+                                const int o = (c0 + q) * 128 + row_local;
+                                float val = EPI == 2 ? v[q] : epi_math<EPI>(v[q], p.alpha, bias_i);
+                                if constexpr (EPI == 3 || EPI == 4) val += __bfloat162float(reinterpret_cast<__nv_bfloat16 *>(stg)[o]);
+                                // NIMBLE_DBG & 16 (experiment only): drop the output (no staging, no store) to
+                                // measure what the epilogue's shared-memory traffic costs the main loop
+                                if (p.dbg & 16) { if (val == 12345.f) asm volatile("trap;"); continue; }
+                                if constexpr (OUT_F32) so[o] = val;
+                                else so[o] = __float2bfloat16_rn(val);
+                            }
                         }
                     }
                     ptx::tc_fence_before();
@@ -529,22 +620,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if constexpr (EPI == 4) {
                         ptx::named_bar_sync(1, kEpiThreads);          // pre-LN tile complete in staging
-                        ln_tile(p, reinterpret_cast<uint8_t *>(stg), n_this, (int)prank, c.m, ln_iter, ln_g, ln_b,
-                                (int)(threadIdx.x - 32 * kEpiWarp0), leader);
+                        ln_tile(p, reinterpret_cast<uint8_t *>(stg), n_stage, n_this, (int)prank, c.m, ln_iter, ln_g,
+                                ln_b, (int)(threadIdx.x - 32 * kEpiWarp0), leader);
                         ++ln_iter;
                     }
                     ptx::fence_async_smem();
                     ptx::named_bar_sync(1, kEpiThreads);
                     if (leader && !(p.dbg & 16)) {
-                        if (p.out_batch_mid) ptx::tma_store_3d(om, stg, c.m * kRowsPerTile + row_base, c.b, j0);
-                        else ptx::tma_store_3d(om, stg, c.m * kRowsPerTile + row_base, j0, c.b);
+                        if constexpr (OUT_F32) {
+                            if (p.out_batch_mid) ptx::tma_store_3d(om, stg, c.m * kRowsPerTile + row_base, c.b, j0);
+                            else ptx::tma_store_3d(om, stg, c.m * kRowsPerTile + row_base, j0, c.b);
+                        } else {                                  // two swizzled 64-feature boxes
+                            for (int sb = 0; sb < 2; ++sb) {
+                                if (p.out_batch_mid)
+                                    ptx::tma_store_3d(om, stg + sb * n_stage * 128, c.m * kRowsPerTile + row_base + 64 * sb,
+                                                      c.b, j0);
+                                else
+                                    ptx::tma_store_3d(om, stg + sb * n_stage * 128, c.m * kRowsPerTile + row_base + 64 * sb,
+                                                      j0, c.b);
+                            }
+                        }
                         ptx::tma_store_commit_wait();                 // staging readable again
                         const int tn = t + t_step;
                         if ((EPI == 3 || EPI == 4) && tn < total_tiles) {
                             const TileCoord cn = tile_of(g, tn);
                             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
-                            if (p.out_batch_mid) ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * kRowsPerTile + row_base, cn.b, cn.n * g.n_full);
-                            else ptx::tma_load_3d(stg, &tmRes, res_bar, cn.m * kRowsPerTile + row_base, cn.n * g.n_full, cn.b);
+                            for (int sb = 0; sb < 2; ++sb)
+                                ptx::tma_load_3d(stg + sb * n_stage * 128, &tmRes, res_bar,
+                                                 cn.m * kRowsPerTile + row_base + 64 * sb, cn.n * g.n_full, cn.b);
                         }
                     }
                     ptx::named_bar_sync(2, kEpiThreads);
