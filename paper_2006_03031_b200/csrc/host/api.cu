@@ -299,7 +299,9 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
         // fused only where a group of 4 pairs covers the whole row (family 3, N = 4 x 256) and
         // the main loop is long enough (K >= 2048) to hide the epilogue's cross-CTA exchange;
         // at K = 1024 (BERT's O-projection) the fused epilogue costs what the LN launch saves
-        ln->fused = fused_ln_enabled() && L.pair && N == 1024 && K >= 2048 && epi == NIMBLE_EPI_BIAS_RESIDUAL &&
+        const char *mk = std::getenv("NIMBLE_LN_MIN_K");      // experiment knob (default 2048)
+        const int64_t min_k = mk ? std::atoll(mk) : 2048;
+        ln->fused = fused_ln_enabled() && L.pair && N == 1024 && K >= min_k && epi == NIMBLE_EPI_BIAS_RESIDUAL &&
                     !static_twin;
         if (ln->fused) {
             cudaError_t e = ln_workspace(&L.p.ln_stats, &L.p.ln_cnt);

@@ -45,7 +45,14 @@ def main():
     X = synth.device_normal(T, cfg["d"], seed=3)
     res = {"tokens": T}
     graphs = {}
-    for skip in (("fused",), (), ("ln",), ("attn",), ("qkv",), ("o",), ("ffn1",), ("ffn2",)):
+    variants = [("fused",), ("fused_k1024",), (), ("ln",), ("attn",), ("qkv",), ("o",), ("ffn1",), ("ffn2",)]
+    if os.environ.get("BREAKDOWN_SHORT"):
+        variants = variants[:3]
+    for skip in variants:
+        if skip == ("fused_k1024",):                    # LN1 fused into the K = 1024 O-projection too
+            os.environ["NIMBLE_LN_MIN_K"] = "1024"
+        else:
+            os.environ.pop("NIMBLE_LN_MIN_K", None)
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         g = torch.cuda.CUDAGraph()
@@ -54,7 +61,7 @@ def main():
                 src = X.data_ptr()
                 for li in range(cfg["layers"]):
                     dst = enc.X[li & 1].data_ptr()
-                    if skip == ("fused",):             # BertPacked.layer (nimble_dense_ln_dyn)
+                    if skip[0:1] in (("fused",), ("fused_k1024",)):   # BertPacked.layer (nimble_dense_ln_dyn)
                         enc.layer(src, dst, T, off.data_ptr(), 64, int(lens.max()), li, s.cuda_stream)
                     else:
                         layer(enc, src, dst, T, off.data_ptr(), 64, int(lens.max()), li, s.cuda_stream, skip)
@@ -64,7 +71,8 @@ def main():
             with torch.cuda.graph(g, stream=s):
                 fwd()
         torch.cuda.current_stream().wait_stream(s)
-        key = "fused_ln" if skip == ("fused",) else ("full" if not skip else "without_" + "_".join(skip))
+        key = {("fused",): "fused_ln", ("fused_k1024",): "fused_ln_both"}.get(skip) or \
+            ("full" if not skip else "without_" + "_".join(skip))
         graphs[key] = g
     # interleaved rounds: every variant sees the same mix of power / clock states
     ts = {k: [] for k in graphs}
