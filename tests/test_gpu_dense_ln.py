@@ -97,3 +97,25 @@ def test_dense_ln_errors(nb):
         nb._check(nb._lib.nimble_dense_ln_dyn(x.data_ptr(), 1024, W.data_ptr(), 1024, b.data_ptr(), res.data_ptr(),
                                               1024, None, be.data_ptr(), 1e-12, y.data_ptr(), 1024, 64, 1024, 1024,
                                               None))
+
+
+
+@pytest.mark.parametrize("rows", [1184, 5003, 17448])
+def test_layernorm_large_rows_vs_oracle(nb, orc, rows):
+    """LayerNorm at the bench's row counts, out of place and in place (the dense_ln fallback runs
+    it in place): identical bits, and sampled rows (incl. the ragged last block) vs the oracle."""
+    d = 1024
+    X = synth.normal((rows, d), 1.0, 300 + rows).cuda()
+    g = (1.0 + synth.normal((d,), 0.02, 1, torch.float32)).cuda()
+    be = synth.normal((d,), 0.02, 2, torch.float32).cuda()
+    Y = torch.empty_like(X)
+    s = torch.cuda.current_stream().cuda_stream
+    nb._check(nb._lib.nimble_layernorm(X.data_ptr(), d, g.data_ptr(), be.data_ptr(), 1e-12, Y.data_ptr(), d, rows, d, s))
+    Z = X.clone()
+    nb._check(nb._lib.nimble_layernorm(Z.data_ptr(), d, g.data_ptr(), be.data_ptr(), 1e-12, Z.data_ptr(), d, rows, d, s))
+    torch.cuda.synchronize()
+    assert torch.equal(Y, Z)
+    idx = _rows(rows)
+    ref = orc.layernorm(X[idx].double().cpu().numpy(), g.double().cpu().numpy(), be.double().cpu().numpy())
+    got = Y[idx].double().cpu().numpy()
+    assert float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1.0))) <= 2e-2
