@@ -314,27 +314,40 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         const uint64_t qd = ptx::smem_desc_sw128(ptx::smem_u32(sQ), 0, 1024);
         const uint64_t kd = ptx::smem_desc_sw128(ptx::smem_u32(sK), 0, 1024);
         uint32_t ns = 0, npv = 0, nitem = 0;
+        auto issue_s = [&](int j, int nk_item) {
+            if (ns > 0) ptx::mbar_wait(s_used, (ns - 1) & 1);      // softmax holds the previous S
+            ptx::mbar_wait(k_full, ns & 1);
+            ptx::tc_fence_after();
+            ATT_TRACE(ns, 6);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                ptx::umma_bf16(tmem, qd + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idesc_s, kk > 0 ? 1u : 0u);
+            ptx::umma_commit(s_full);
+            ptx::umma_commit(k_empty);
+            if (j == nk_item - 1) ptx::umma_commit(q_empty);
+            ++ns;
+        };
+        int nk = 0;
+        if ((int)blockIdx.x < n_items) {
+            ptx::mbar_wait(q_full, 0);
+            nk = (info[0].y + 127) / 128;
+            issue_s(0, nk);
+        }
         for (int k = (int)blockIdx.x; k < n_items; k += (int)gridDim.x) {
             ATT_TRACE(384 + (int)nitem, 0);
-            ptx::mbar_wait(q_full, nitem & 1);
-            ATT_TRACE(256 + (int)nitem, 7);
-            const int nk = (info[nitem & 1].y + 127) / 128;
-            auto issue_s = [&](int j) {
-                if (ns > 0) ptx::mbar_wait(s_used, (ns - 1) & 1);      // softmax holds the previous S
-                ptx::mbar_wait(k_full, ns & 1);
-                ptx::tc_fence_after();
-                ATT_TRACE(ns, 6);
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    ptx::umma_bf16(tmem, qd + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idesc_s, kk > 0 ? 1u : 0u);
-                ptx::umma_commit(s_full);
-                ptx::umma_commit(k_empty);
-                if (j == nk - 1) ptx::umma_commit(q_empty);
-                ++ns;
-            };
-            issue_s(0);
+            int nk_next = 0;
             for (int j = 0; j < nk; ++j) {
-                if (j + 1 < nk) issue_s(j + 1);
+                if (j + 1 < nk) {
+                    issue_s(j + 1, nk);
+                } else if (k + (int)gridDim.x < n_items) {
+                    // the next item's first S goes to the tensor core BEFORE this item's last PV
+                    // (it only needs the softmax to have pulled the last S into registers), so
+                    // the softmax finds it ready when it finishes this item
+                    ptx::mbar_wait(q_full, (nitem + 1) & 1);
+                    ATT_TRACE(256 + (int)nitem + 1, 7);
+                    nk_next = (info[(nitem + 1) & 1].y + 127) / 128;
+                    issue_s(0, nk_next);
+                }
                 ptx::mbar_wait(p_ready, npv & 1);                       // P_j written, O rescaled
                 if (j == 0 && nitem > 0) ptx::mbar_wait(o_free, (nitem - 1) & 1);   // previous O read out
                 const int st = (int)(npv & 1);
@@ -356,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             }
             ATT_TRACE(384 + (int)nitem, 1);
             ++nitem;
+            nk = nk_next;
         }
       }
       __syncwarp();
