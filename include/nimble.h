@@ -110,7 +110,7 @@ int nimble_dispatch_bmm(int64_t batch, int64_t M, int64_t N, int64_t K, int tran
  * nimble_dispatch_dense and nimble_dense_dyn with M < 2048 (family 3 and the static twin are
  * not tuned).  tile_t in {32, 64, 128, 256} (0 removes the entry), split_max in {1, 2, 4, 8};
  * anything else -> NIMBLE_E_EXTENT.  Process-wide, thread-safe.  get: tile_t = 0 when no
- * schedule is registered (the default t = 128, split_max = 8 applies).
+ * schedule is registered (the default applies: t = 128, split cap 8 if K >= 2048, else 1).
  * ------------------------------------------------------------------------- */
 int nimble_set_dense_schedule(int64_t N, int64_t K, int32_t tile_t, int32_t split_max);
 int nimble_get_dense_schedule(int64_t N, int64_t K, int32_t *tile_t, int32_t *split_max);
@@ -172,8 +172,9 @@ int nimble_dense_ln_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, 
  * by the kernel after its grid-dependency wait, so an earlier kernel or copy on the stream
  * may write it).  The kernel runs the residue dispatch on the device: family 1 of
  * DISPATCH.md with the token tile of the registered schedule (else 128) and the variant
- * limit c current at launch; split_k is the host rule's (schedule cap, else 8) when M_max
- * fits one token tile (then it is the same for every M <= M_max), else 1.  Writes y rows [0, M) only (the store's tensor
+ * limit c current at launch; split_k is the host rule's with the schedule's cap, else the
+ * default cap evaluated at the bound M_max, when M_max fits one token tile (then it is the
+ * same for every M <= M_max), else 1.  Writes y rows [0, M) only (the store's tensor
  * map is re-encoded on the device with extent M; rows [M, M_max) of y are untouched);
  * x rows in [M, M_max) are read but only feed unstored columns.  dispatch_dev: NULL or a
  * device nimble_dispatch that receives the device's dispatch decision.  A device extent

@@ -107,21 +107,27 @@ static int32_t orc_split_cap(int64_t tiles, int64_t K, int32_t cap) {
     return s;
 }
 
-static int32_t orc_split(int64_t tiles, int64_t K) { return orc_split_cap(tiles, K, 8); }
+/* default split cap: split-K only for K >= 2048 (DISPATCH.md: below that the exchange of
+ * fp32 partial tiles costs more than the shorter K loop saves, measured on B200; a cap that
+ * depends on K alone keeps the split a function of the tile grid, so the dynamic-M result
+ * stays bit-identical to pad-then-slice) */
+static int32_t orc_default_cap(int64_t M, int64_t K) { (void)M; return K >= 2048 ? 8 : 1; }
+static int32_t orc_split(int64_t tiles, int64_t M, int64_t K) { return orc_split_cap(tiles, K, orc_default_cap(M, K)); }
 
 #define ORC_MAXEXT 2147483647LL
 
 /* families 1 / 3, UMMA_T: tokens (symbolic M) on the UMMA-N slot, granule 16;
  * t = 128 for M < 2048 (family 1, split-K allowed), t = 256 for M >= 2048 (family 3). */
 /* tile_t / split_max: a tuned schedule for family 1 (DISPATCH.md "Tuned schedules",
- * P:392-406 three-step symbolic tuning picks them); tile_t = 0 -> the default (128, 8). */
+ * P:392-406 three-step symbolic tuning picks them); tile_t = 0 -> the default (128, cap 8 if
+ * K >= 2048, else 1). */
 static int orc_umma_t_sched(int64_t batch, int64_t M, int64_t N, int64_t K, int c, int32_t tile_t,
                             int32_t split_max, orc_dispatch *d) {
     memset(d, 0, sizeof(*d));
     int wide = (M >= 2048);
     int32_t t = wide ? 256 : (tile_t > 0 ? tile_t : 128);
     /* split-K exchanges two fp32 [128 x t] buffers through smem: only t <= 128 fits */
-    int32_t cap = (!wide && tile_t > 0) ? (t <= 128 ? split_max : 1) : 8;
+    int32_t cap = (!wide && tile_t > 0) ? (t <= 128 ? split_max : 1) : orc_default_cap(M, K);
     d->family = wide ? 3 : 1; d->tile_t = t; d->granule = 16; d->n_classes = t / 16 + 1;
     d->k = M / t; d->r = M % t;                      /* x = t k + r */
     d->residue_class = (int32_t)orc_ceil_div(d->r, 16);
@@ -191,7 +197,7 @@ int orc_dispatch_bmm(int64_t batch, int64_t M, int64_t N, int64_t K, int trans_b
     d->umma_n_full = (N >= 256) ? 256 : (int32_t)(16 * orc_ceil_div(N, 16));
     d->umma_n_tail = (int32_t)(16 * orc_ceil_div(N - 256 * (nN - 1), 16));
     int64_t mt = d->k + (d->r > 0);
-    d->split_k = orc_split(mt * nN * batch, K);
+    d->split_k = orc_split(mt * nN * batch, M, K);
     d->grid[0] = (int32_t)mt; d->grid[1] = (int32_t)nN; d->grid[2] = (int32_t)(batch * d->split_k);
     d->cluster[0] = 1; d->cluster[1] = 1; d->cluster[2] = d->split_k;
     return ORC_OK;

@@ -412,7 +412,7 @@ extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, i
     // split-K needs a launch grid that does not depend on M: allowed when the bound fits ONE
     // token tile, where the host rule's split (a function of the tile count) is the same for
     // every M <= M_max; otherwise the device dispatch runs split 1
-    dispatch_umma_t(1, M_max, N, K, &d, t > 0 ? t : 128, cap);
+    dispatch_umma_t(1, M_max, N, K, &d, t, cap);        // t = 0: the default rule (t = 128, K-dependent cap)
     if (d.grid[1] != 1) dispatch_umma_t(1, M_max, N, K, &d, t > 0 ? t : 128, 1);   // launch geometry for the bound
     UmmaLaunch L;
     std::memset(&L, 0, sizeof(L));

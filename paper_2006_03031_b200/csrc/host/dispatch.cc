@@ -50,6 +50,14 @@ int32_t choose_split(int64_t ctas, int64_t K, int32_t cap = 8) {
     return s;
 }
 
+// The default split cap: split-K only for K >= 2048.  Below that the DSMEM exchange of the
+// fp32 partial tiles costs more than the shorter K loop saves at M >= 64 (measured on B200:
+// profiles/r01_gemm_sweep.json, P:392-406 tuning data in profiles/r01_symbolic_tuning.json;
+// at M <= 16 the split would still win — the tuned schedules cover that).  A cap depending on
+// K alone keeps the split a function of the tile grid, so dynamic M stays bit-identical to
+// pad-then-slice.  Tuned schedules carry their own cap.
+int32_t default_split_cap(int64_t M, int64_t K) { (void)M; return K >= 2048 ? 8 : 1; }
+
 void split_residue(const ResidueFamily &f, int64_t x, nimble_dispatch *d) {
     d->family = f.id;
     d->tile_t = f.t;
@@ -87,7 +95,7 @@ int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, 
     const ResidueFamily f3x{kUMMA_T256.id, f3_tile, 16, f3_tile / 16 + 1};
     const ResidueFamily &f = wide ? (f3_tile > 0 ? f3x : kUMMA_T256) : (tile_t > 0 ? tuned : kUMMA_T);
     // split-K parks and receives fp32 [128 x t] slices in smem: only t <= 128 fits 227 KB
-    const int32_t cap = (!wide && tile_t > 0) ? (tile_t <= 128 ? split_max : 1) : 8;
+    const int32_t cap = (!wide && tile_t > 0) ? (tile_t <= 128 ? split_max : 1) : default_split_cap(M_tokens, K);
     split_residue(f, M_tokens, d);
     d->residue_class = static_cast<int32_t>(cdiv(d->r, f.granule));
     d->variant = select_variant(f, d->residue_class);
@@ -120,7 +128,7 @@ int dispatch_umma_d(int64_t batch, int64_t M, int64_t N, int64_t K, nimble_dispa
     d->umma_n_full = static_cast<int32_t>(N >= 256 ? 256 : 16 * cdiv(N, 16));
     d->umma_n_tail = static_cast<int32_t>(16 * cdiv(N - 256 * (n_tiles - 1), 16));
     const int64_t m_tiles = d->k + (d->r ? 1 : 0);
-    d->split_k = choose_split(m_tiles * n_tiles * batch, K);
+    d->split_k = choose_split(m_tiles * n_tiles * batch, K, default_split_cap(M, K));
     d->grid[0] = static_cast<int32_t>(m_tiles);
     d->grid[1] = static_cast<int32_t>(n_tiles);
     d->grid[2] = static_cast<int32_t>(batch * d->split_k);

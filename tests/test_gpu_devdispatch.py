@@ -206,19 +206,25 @@ def test_bert_forward_dev_and_one_graph_bitwise(nb):
 @pytest.mark.parametrize("N,K", [(768, 3072), (2304, 768), (1024, 4096)])
 def test_dense_dyn_dev_split_k_within_one_tile(nb, orc, N, K):
     """M_max <= 128 fits one token tile: the device dispatch keeps the host rule's split-K (the
-    same for every M <= M_max), the record equals the oracle's with split cap 8, and outputs
-    equal the host-extent launch bit for bit (same tiles, same fixed-order split reduction)."""
+    same for every M <= M_max; the default cap evaluated at the bound), the record equals the
+    oracle's rule with that (t, cap), and outputs equal the host-extent launch with the same
+    schedule bit for bit (same tiles, same fixed-order split reduction)."""
     M_max = 128
     W, b, x = _setup(N, K, M_max, 71)
     Wd, bd, xd = W.cuda(), b.cuda(), x.cuda()
+    cap = 8 if K >= 2048 else 1            # the default rule's split cap, evaluated at the bound
     for M in (1, 7, 16, 33, 100, 127, 128):
         rec = torch.zeros(nb.DISPATCH_BYTES, dtype=torch.uint8, device="cuda")
         y_dev = torch.empty((M_max, N), dtype=torch.bfloat16, device="cuda")
         nb.dense_dyn_dev(xd, Wd, bd, y_dev, torch.tensor([M], dtype=torch.int32, device="cuda"), M_max, record=rec)
-        y_host = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
-        nb.dense_dyn(xd[:M], Wd, bd, y_host)
+        nb.set_dense_schedule(N, K, 128, cap)               # the host path with the same (t, cap)
+        try:
+            y_host = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+            nb.dense_dyn(xd[:M], Wd, bd, y_host)
+        finally:
+            nb.set_dense_schedule(N, K, 0, 1)
         torch.cuda.synchronize()
         drec = nb.dispatch_from_bytes(rec)
-        assert drec == orc.dispatch_dense(M, N, K, 1, 0, 128, 8)[1], M
-        assert drec["split_k"] > 1 or N * K < 1
+        assert drec == orc.dispatch_dense(M, N, K, 1, 0, 128, cap)[1], M
+        assert (drec["split_k"] > 1) == (K >= 2048)
         assert torch.equal(y_dev[:M], y_host), M
