@@ -85,15 +85,11 @@ int dispatch_simt8(int64_t M, int64_t N, nimble_dispatch *d) {
 int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, nimble_dispatch *d,
                     int32_t tile_t, int32_t split_max) {
     *d = nimble_dispatch{};
-    // experiment-only overrides (break oracle parity): family-3 threshold and token tile
-    static const int64_t f3_from = [] { const char *e = std::getenv("NIMBLE_F3_FROM"); return e ? std::atoll(e) : kWideTileFrom; }();
-    static const int32_t f3_tile = [] { const char *e = std::getenv("NIMBLE_F3_TILE"); return e ? std::atoi(e) : 0; }();
-    const bool wide = M_tokens >= f3_from;
+    const bool wide = M_tokens >= kWideTileFrom;
     // a tuned schedule replaces family 1's token tile t (residue classes
     // t/16 + 1) and caps its split-K; family 3 (M >= 2048) is not tuned.
     const ResidueFamily tuned{kUMMA_T.id, tile_t, 16, tile_t / 16 + 1};
-    const ResidueFamily f3x{kUMMA_T256.id, f3_tile, 16, f3_tile / 16 + 1};
-    const ResidueFamily &f = wide ? (f3_tile > 0 ? f3x : kUMMA_T256) : (tile_t > 0 ? tuned : kUMMA_T);
+    const ResidueFamily &f = wide ? kUMMA_T256 : (tile_t > 0 ? tuned : kUMMA_T);
     // split-K parks and receives fp32 [128 x t] slices in smem: only t <= 128 fits 227 KB
     const int32_t cap = (!wide && tile_t > 0) ? (tile_t <= 128 ? split_max : 1) : default_split_cap(M_tokens, K);
     split_residue(f, M_tokens, d);

@@ -1,5 +1,7 @@
-"""Family-3 token-tile probe: dense_dyn TFLOP/s per (shape, M) under the current env overrides
-(NIMBLE_F3_FROM / NIMBLE_F3_TILE, experiment only).  CUDA-graph timing, weights past L2."""
+"""dense_dyn TFLOP/s per (shape, M) (CUDA-graph timing, weights past L2), tagged with PROBE_TAG.
+The family-3 tile / threshold overrides this probe was written for (NIMBLE_F3_TILE / _FROM)
+were removed after the sweep in profiles/r01_gemm_m_sweep.json; experiment knobs that remain:
+NIMBLE_MAX_STAGES, NIMBLE_DBG bits."""
 import json
 import os
 import sys
