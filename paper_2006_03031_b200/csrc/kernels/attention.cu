@@ -13,15 +13,20 @@
 // prefetch happen once per CTA, and the producer runs ahead into the next item (its Q and
 // first K/V blocks load while the current item finishes).
 // Per item, online softmax over 128-key blocks, 320 threads:
-//   warp 8 lane 0  TMA producer: Q tile, then per key block K_j [128 x 64] (single buffer) and
-//                  V_j (MN-major, two 64-key boxes, 2-stage ring).
+//   warp 8 lane 0  TMA producer and the only role that decodes the work list: publishes each
+//                  item's (offset, L, q-tile, head) in a 2-slot smem ring released by the Q
+//                  barrier; Q tile, then per key block K_j [128 x 64] (single buffer) and V_j
+//                  (MN-major, two 64-key boxes, 2-stage ring).
 //   warp 9 lane 0  MMA issuer: S = Q K_j^T into TMEM cols [0,128) as soon as the previous S
-//                  has been read; O += P_j V_j into TMEM cols [128,192) once P_j is written.
+//                  has been read (the next item's first S before this item's last PV);
+//                  O += P_j V_j into TMEM cols [128,192) once P_j is written.
 //   warps 0-7      softmax: row q = TMEM lane 32*(w%4)+lane, key half (w/4) of the block held
-//                  in registers; running max / sum; unnormalised P_j written as bf16 straight
-//                  into the UMMA K-major swizzled smem layout; O rescaled in TMEM when the
-//                  running max grows; epilogue O / rowsum -> bf16.
-// TMEM 256 columns and ~107 KB smem per CTA: two CTAs share an SM.  Keys >= L_i get P = 0;
+//                  in registers; running max / sum in FFMA2 / FADD2 / FMNMX3, exp2 on MUFU
+//                  and (2 of 8 pairs) on the FMA pipes; unnormalised P_j written as bf16
+//                  straight into the UMMA K-major swizzled smem layout; O rescaled in TMEM
+//                  only when a row max grew by more than 2^8 (lazy rescaling); epilogue
+//                  O / rowsum -> bf16.
+// TMEM 256 columns and ~113 KB smem per CTA: two CTAs share an SM.  Keys >= L_i get P = 0;
 // query rows >= L_i are computed but never stored.
 #include <cstdint>
 
