@@ -15,10 +15,14 @@
 //   warp 2         TMEM allocation / deallocation.
 //   warps 4..      epilogue: warp w reads TMEM lane quarter (w % 4), 16-column chunks
 //                  round-robin over the column groups; compile-time epilogue
-//                  (alpha | bias | bias+GELU | bias+residual, residual tile TMA-loaded into
-//                  the staging buffer); the transposed output tile is staged in smem and
-//                  written by ONE TMA store that clips rows beyond the symbolic extent.
-//                  The epilogue of tile i overlaps the MMAs of tile i+1 (persistent CTAs).
+//                  (alpha | bias | bias+GELU | bias+residual | bias+residual+LayerNorm).
+//                  bf16 outputs: tcgen05.ld.16x256b fragments -> stmatrix.trans into two
+//                  [tokens][64 features] sub-tiles in the 128-B TMA swizzle (the residual is
+//                  TMA-loaded into the same layout and read with ldmatrix.trans); two TMA
+//                  stores clip rows beyond the symbolic extent.  fp32 outputs (bmm scores):
+//                  32x32b loads and one plain TMA store.  The epilogue of tile i overlaps the
+//                  MMAs of tile i+1 (persistent CTAs, double-buffered TMEM accumulators).
+//                  LayerNorm (EPI 4): 8-CTA groups exchange per-token partial sums (ln_tile).
 // split > 1 (small M, weight-streaming regime): the K slices of one tile form a cluster
 // along z.  Each CTA parks its fp32 partial in smem and bulk-copies (cp.async.bulk over
 // DSMEM) slice q to CTA q, which sums the slices in rank order (deterministic, no
