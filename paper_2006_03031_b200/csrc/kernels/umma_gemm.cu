@@ -499,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // two 8-feature chunks of gamma / beta live in registers for the whole kernel
         float ln_g[16], ln_b[16];
         int ln_iter = 0;
+        int ep_tile = 0;                                    // debug: tiles drained (NIMBLE_DBG & 4)
         if constexpr (EPI == 4) {
             const int f0 = (t_first % 4) * 256 + row_base + ((int)(threadIdx.x - 32 * kEpiWarp0) & 7) * 8;
 #pragma unroll
@@ -526,6 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             if (leader && t == t_first) NIMBLE_TRACE(3);
+            const bool ktr = (p.dbg & 4) && trace && cta_lin == 0 && leader && ep_tile < 512;
+            if (ktr) p.trace[32768 + ep_tile * 4 + 0] = clock64();   // accumulator ready
             const uint32_t tmem_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * g.n_full);
 
             if (!split) {
@@ -618,6 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ptx::tc_fence_before();
                     __syncwarp();
+                    if (ktr) p.trace[32768 + ep_tile * 4 + 1] = clock64();   // TMEM read, staged
                     if (lane == 0) {                                 // TMEM may be overwritten now
                         if (PAIR) ptx::mbar_arrive_cluster(ptx::map_shared_rank(ptx::smem_u32(&tempty[acc]), 0));
                         else ptx::mbar_arrive(&tempty[acc]);
@@ -645,6 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                         ptx::tma_store_commit_wait();                 // staging readable again
+                        if (ktr) p.trace[32768 + ep_tile * 4 + 2] = clock64();   // store drained
                         const int tn = t + t_step;
                         if ((EPI == 3 || EPI == 4) && tn < total_tiles) {
                             const TileCoord cn = tile_of(g, tn);
@@ -741,6 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
+            ++ep_tile;
         }
     }
 

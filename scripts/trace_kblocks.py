@@ -21,7 +21,7 @@ for shp in (sys.argv[1] if len(sys.argv) > 1 else "17448x3072x1024,17448x1024x40
     for _ in range(3):
         nb.dense_dyn(x, W, b, y)
     torch.cuda.synchronize()
-    buf = torch.zeros(32768, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(32768 + 4 * 512, dtype=torch.int64, device="cuda")
     nb._lib.nimble_debug_trace(buf.data_ptr())
     nb.dense_dyn(x, W, b, y)
     torch.cuda.synchronize()
@@ -64,6 +64,17 @@ for shp in (sys.argv[1] if len(sys.argv) > 1 else "17448x3072x1024,17448x1024x40
           " end med %.2f max %.2f" % ((ph[ok, 0].max() - t0) / 1e3, (np.median(ph[ok, 1]) - t0) / 1e3,
                                      (np.median(ph[ok, 2]) - t0) / 1e3, (ph[ok, 2].max() - t0) / 1e3,
                                      (np.median(ph[ok, 6]) - t0) / 1e3, (ph[ok, 6].max() - t0) / 1e3))
+    ep = t[32768:32768 + 4 * 512].reshape(-1, 4)
+    ep = ep[ep[:, 0] > 0]
+    if len(ep) > 1:
+        print("  epilogue per tile (clk): acc ready -> staged median %.0f; staged -> store drained %.0f;"
+              " acc-ready to acc-ready %.0f; MMA tile (full 0 -> full 0) %.0f"
+              % (np.median(ep[:, 1] - ep[:, 0]), np.median(ep[:, 2] - ep[:, 1]), np.median(np.diff(ep[:, 0])),
+                 np.median(np.diff(full[::kb])) if len(full) > kb else -1))
+        # does the MMA wait for the accumulator? tile i's acc-free vs epilogue of tile i-2 staged
+        lag = [tiles[i] - ep[i - 2, 1] for i in range(2, min(len(tiles), len(ep) + 2))]
+        print("  MMA acc-free minus epilogue(i-2) staged (clk, >0 = MMA could proceed only after it): median %.0f"
+              % np.median(lag))
     clk = t[30002] - t[30000]
     ns = t[30003] - t[30001]
     print("  CTA 0 SM clock over its k-blocks: %.0f MHz (%.0f clk in %.1f us)" % (1e3 * clk / max(ns, 1), clk, ns / 1e3))
