@@ -295,3 +295,19 @@ def test_bf16_large_m_cta_pairs(nb, orc, M):
     y = _dense_gpu(nb, xi, Wi, bi, nb.EPI_BIAS)
     ref, _ = orc.dense(xi.double().numpy(), Wi.double().numpy(), bi.numpy(), None, 1)
     assert np.array_equal(y.double().cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("M,N", [(77, 200), (300, 72), (2100, 520), (2049, 264)])
+def test_bf16_partial_feature_boxes(nb, orc, M, N):
+    """N not a multiple of the 64-feature swizzled store box (nor of 128 / 256): the epilogue's
+    last store / residual box is clipped by TMA, every epilogue kind, families 1 and 3."""
+    K = 192
+    W = synth.normal((N, K), 0.05, 500 + N)
+    b = synth.normal((N,), 0.1, 501 + N, torch.float32)
+    x = synth.normal((M, K), 1.0, 502 + M)
+    for epi in (nb.EPI_BIAS, nb.EPI_BIAS_GELU, nb.EPI_BIAS_RESIDUAL):
+        res = synth.normal((M, N), 1.0, 503 + M) if epi == nb.EPI_BIAS_RESIDUAL else None
+        y = _dense_gpu(nb, x, W, b, epi, res)
+        ref, D = orc.dense(x.double().numpy(), W.double().numpy(), b.numpy(),
+                           None if res is None else res.double().numpy(), epi)
+        assert _err(y, ref, D) <= TOL_BF16, (M, N, epi)
