@@ -137,9 +137,11 @@ void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
     int st = kb_per_split < max_st ? kb_per_split : max_st;     // NIMBLE_MAX_STAGES: experiment only
     if (st < 1) st = 1;
     // largest depth that fits next to the epilogue staging
-    while (st > 1 && umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair) > 232448) --st;
+    while (st > 1 && umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair, L.p.half_stg) >
+                         232448)
+        --st;
     L.p.stages = st;
-    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair);
+    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair, L.p.half_stg);
     L.p.tiles_m = L.pair ? (L.p.rows_a + 255) / 256 : d.grid[0];   // pairs own 256-row tiles
     L.p.tiles_n = d.grid[1];
     L.p.batch = d.grid[2] / d.split_k;
@@ -201,6 +203,13 @@ cudaError_t ln_workspace(float2 **stats, int32_t **cnt) {
     *stats = g_ln_ws.stats[dev];
     *cnt = g_ln_ws.cnt[dev];
     return cudaSuccess;
+}
+bool half_staging_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("NIMBLE_HALF_STG");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 bool fused_ln_enabled() {
     static const bool on = [] {
@@ -282,12 +291,27 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     L.p.a_static = pdl_enabled() ? 1 : 0;   // weights: fetched before the PDL grid-dependency wait
     L.pair = (d.family == 3) ? 1 : 0;       // large M: 2-CTA pairs, each CTA loads half of B
     const int box_b = L.pair ? L.p.box_n / 2 : L.p.box_n;
+    // LayerNorm fusion (nimble_dense_ln_dyn): fused only where a group of 4 pairs covers the
+    // whole row (family 3, N = 4 x 256) and the main loop is long enough (K >= 2048) to hide the
+    // epilogue's cross-CTA exchange; at K = 1024 (BERT's O-projection) the fused epilogue
+    // costs what the LN launch saves
+    bool ln_fused = false;
+    if (ln) {
+        const char *mk = std::getenv("NIMBLE_LN_MIN_K");      // experiment knob (default 2048)
+        const int64_t min_k = mk ? std::atoll(mk) : 2048;
+        ln_fused = fused_ln_enabled() && L.pair && N == 1024 && K >= min_k && epi == NIMBLE_EPI_BIAS_RESIDUAL &&
+                   !static_twin;
+    }
+    // the 2-CTA family stages its bf16 output in 128-token halves (a 6th pipeline stage fits);
+    // the fused LayerNorm needs the whole tile in shared memory
+    L.p.half_stg = (L.pair && !ln_fused && half_staging_enabled()) ? 1 : 0;
+    const int out_box = L.p.half_stg ? L.p.box_n / 2 : L.p.box_n;
     if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
     if ((st = encode_operand(&L.tmB, x, K, M, ldx, 1, 0, box_b, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
-    if ((st = encode_out(&L.tmOut, y, false, N, M, ldy, 1, 0, L.p.box_n, &L.p.out_batch_mid)) != NIMBLE_OK) return st;
+    if ((st = encode_out(&L.tmOut, y, false, N, M, ldy, 1, 0, out_box, &L.p.out_batch_mid)) != NIMBLE_OK) return st;
     if (epi == NIMBLE_EPI_BIAS_RESIDUAL) {
         int mid = 0;
-        if ((st = encode_out(&L.tmRes, const_cast<void *>(residual), false, N, M, ldr, 1, 0, L.p.box_n, &mid)) != NIMBLE_OK) return st;
+        if ((st = encode_out(&L.tmRes, const_cast<void *>(residual), false, N, M, ldr, 1, 0, out_box, &mid)) != NIMBLE_OK) return st;
     } else {
         L.tmRes = L.tmOut;
     }
@@ -296,13 +320,7 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     plan_pipeline(L, d);
     L.stream = s;
     if (ln) {
-        // fused only where a group of 4 pairs covers the whole row (family 3, N = 4 x 256) and
-        // the main loop is long enough (K >= 2048) to hide the epilogue's cross-CTA exchange;
-        // at K = 1024 (BERT's O-projection) the fused epilogue costs what the LN launch saves
-        const char *mk = std::getenv("NIMBLE_LN_MIN_K");      // experiment knob (default 2048)
-        const int64_t min_k = mk ? std::atoll(mk) : 2048;
-        ln->fused = fused_ln_enabled() && L.pair && N == 1024 && K >= min_k && epi == NIMBLE_EPI_BIAS_RESIDUAL &&
-                    !static_twin;
+        ln->fused = ln_fused;
         if (ln->fused) {
             cudaError_t e = ln_workspace(&L.p.ln_stats, &L.p.ln_cnt);
             if (e != cudaSuccess) return cuda_fail("nimble_dense_ln_dyn workspace", e);

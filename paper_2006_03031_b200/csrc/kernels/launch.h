@@ -54,6 +54,9 @@ struct UmmaParams {
     int32_t ln_groups;           // groups of 4 pairs; pairs >= 4 * ln_groups idle
     float2 *ln_stats;            // [2 * ln_groups][8][256] (sum x, sum x^2) partials
     int32_t *ln_cnt;             // [2 * ln_groups][2] writers / readers per slot
+    // half staging (2-CTA family, bf16, EPI <= 3): the epilogue stages and stores the tile in two
+    // 128-token halves through a 32 KB buffer, which leaves room for a 6th pipeline stage
+    int32_t half_stg;
 };
 
 struct UmmaLaunch {
@@ -69,7 +72,8 @@ struct UmmaLaunch {
 cudaError_t launch_umma_gemm(const UmmaLaunch &L);
 bool umma_static_available(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_umma_gemm_static(const UmmaLaunch &L, int64_t M, int64_t N, int64_t K);
-size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed, int pair);
+size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed, int pair,
+                       int half_stg = 0);
 // Programmatic dependent launch (griddepcontrol) on every libnimble launch that supports it.
 bool pdl_enabled();
 

@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
                      const UmmaParams p) {
     using OutT = typename std::conditional<OUT_F32, float, __nv_bfloat16>::type;
+    constexpr bool HALF_OK = PAIR && !OUT_F32 && EPI <= 3 && !B_MN;   // half staging supported
     Geo g = make_geo<SM, SN, SK>(p);
     const bool devm = p.m_dev != nullptr;          // extent on the device (dense_dyn_dev)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -275,7 +276,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int n_stage = PAIR ? 2 * g.box_n : g.box_n;
     const int part_bytes = split ? 128 * n_stage * 4 : 0;
     const int region0 = ring_bytes > part_bytes ? ring_bytes : part_bytes;
-    const int stg_bytes = split ? 128 * n_stage * 4 : (TRANS ? 128 * n_stage * (int)sizeof(OutT) : 0);
+    const int stg_tok = p.half_stg ? n_stage / 2 : n_stage;   // tokens per staging buffer
+    const int stg_bytes = split ? 128 * n_stage * 4 : (TRANS ? 128 * stg_tok * (int)sizeof(OutT) : 0);
     uint8_t *stg = smem + region0;                 // epilogue staging / split-K receive buffer
     uint64_t *full_bar = reinterpret_cast<uint64_t *>(stg + stg_bytes);
     uint64_t *empty_bar = full_bar + p.stages;
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int half = ew >> 2;                            // column group 0..kEpiGroups-1
         const int row_local = quarter * 32 + (int)lane;
         const bool leader = (ew == 0 && lane == 0);
-        const int res_bytes = 128 * n_stage * 2;
+        const int res_bytes = 128 * stg_tok * 2;
         const int row_base = (int)prank * 128;
         int acc = 0;
         uint32_t acc_phase = 0, res_phase = 0;
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const TileCoord c = tile_of(g, t_first);
             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
             for (int sb = 0; sb < 2; ++sb)             // two swizzled [tokens][64 features] boxes
-                ptx::tma_load_3d(stg + sb * n_stage * 128, &tmRes, res_bar, c.m * kRowsPerTile + row_base + 64 * sb,
+                ptx::tma_load_3d(stg + sb * stg_tok * 128, &tmRes, res_bar, c.m * kRowsPerTile + row_base + 64 * sb,
                                  c.n * g.n_full, c.b);
         }
         // EPI 4: this CTA's 128 features are fixed (feature tile f = t_first % 4): the thread's
@@ -532,7 +534,95 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t tmem_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * g.n_full);
 
             if (!split) {
-                if (TRANS) {
+                if (TRANS && HALF_OK && p.half_stg) {
+                    // ---- half staging: two 128-token halves through one 32 KB swizzled buffer
+                    const uint32_t st_base = ptx::smem_u32(stg);
+                    const int tq = (int)lane >> 2;
+                    float bsv[4] = {0.f, 0.f, 0.f, 0.f};
+                    if constexpr (EPI >= 1) {
+#pragma unroll
+                        for (int h4 = 0; h4 < 4; ++h4) {
+                            const int fi = c.m * kRowsPerTile + row_base + quarter * 32 + tq + 8 * h4;
+                            bsv[h4] = fi < g.rows_a ? __ldg(p.bias + fi) : 0.f;
+                        }
+                    }
+                    const int mi = (int)lane >> 3, mr = (int)lane & 7;
+                    const int nh = (n_this + stg_tok - 1) / stg_tok;
+                    for (int hh = 0; hh < nh; ++hh) {
+                        const int col0 = hh * stg_tok, col1 = min(n_this, col0 + stg_tok);
+                        if (EPI == 3) {
+                            ptx::mbar_wait(res_bar, res_phase);
+                            res_phase ^= 1;
+                        }
+                        for (int c0 = col0 + half * 16; c0 < col1; c0 += 16 * kEpiGroups) {
+#pragma unroll
+                            for (int hl = 0; hl < 2; ++hl) {
+                                uint32_t r[8];
+                                tmem_ld_16x256b_x2(tmem_base + ((uint32_t)(quarter * 32 + 16 * hl) << 16) +
+                                                       (uint32_t)(acc * g.n_full + c0), r);
+                                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                                const int fl0 = quarter * 32 + 16 * hl;
+                                const uint32_t a_me =
+                                    stg_addr(st_base, stg_tok, fl0 + 8 * (mi & 1), c0 - col0 + 8 * (mi >> 1) + mr);
+                                float2 x[4];
+#pragma unroll
+                                for (int m = 0; m < 4; ++m)
+                                    x[m] = make_float2(__uint_as_float(r[(m & 1) * 2 + (m >> 1) * 4]),
+                                                       __uint_as_float(r[(m & 1) * 2 + (m >> 1) * 4 + 1]));
+                                float2 rs[4];
+                                if constexpr (EPI == 3) {
+                                    uint32_t q0, q1, q2, q3;
+                                    ldmatrix_x4_trans(a_me, q0, q1, q2, q3);
+                                    rs[0] = unpack_bf16(q0); rs[1] = unpack_bf16(q1);
+                                    rs[2] = unpack_bf16(q2); rs[3] = unpack_bf16(q3);
+                                }
+                                uint32_t o[4];
+#pragma unroll
+                                for (int m = 0; m < 4; ++m) {
+                                    const float bb = bsv[2 * hl + (m & 1)];
+                                    float2 y2;
+                                    if constexpr (EPI == 0) y2 = ptx::fmul2(x[m], ptx::f2(p.alpha));
+                                    else if constexpr (EPI == 2) y2 = ptx::gelu_erf2(ptx::fadd2(x[m], ptx::f2(bb)));
+                                    else y2 = ptx::fadd2(x[m], ptx::f2(bb));
+                                    if constexpr (EPI == 3) y2 = ptx::fadd2(y2, rs[m]);
+                                    o[m] = pack_bf16(y2.x, y2.y);
+                                }
+                                stmatrix_x4_trans(a_me, o[0], o[1], o[2], o[3]);
+                            }
+                        }
+                        if (hh == nh - 1) {                      // last TMEM read of this tile
+                            ptx::tc_fence_before();
+                            __syncwarp();
+                            if (ktr) p.trace[32768 + ep_tile * 4 + 1] = clock64();
+                            if (lane == 0) ptx::mbar_arrive_cluster(ptx::map_shared_rank(ptx::smem_u32(&tempty[acc]), 0));
+                        }
+                        ptx::fence_async_smem();
+                        ptx::named_bar_sync(1, kEpiThreads);
+                        if (leader && !(p.dbg & 16)) {
+                            for (int sb = 0; sb < 2; ++sb)
+                                ptx::tma_store_3d(om, stg + sb * stg_tok * 128, c.m * kRowsPerTile + row_base + 64 * sb,
+                                                  j0 + col0, c.b);
+                            ptx::tma_store_commit_wait();             // staging readable again
+                            if (EPI == 3) {                           // next residual half
+                                const int tn = t + t_step;
+                                if (hh + 1 < nh) {
+                                    ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
+                                    for (int sb = 0; sb < 2; ++sb)
+                                        ptx::tma_load_3d(stg + sb * stg_tok * 128, &tmRes, res_bar,
+                                                         c.m * kRowsPerTile + row_base + 64 * sb, j0 + col1, c.b);
+                                } else if (tn < total_tiles) {
+                                    const TileCoord cn = tile_of(g, tn);
+                                    ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
+                                    for (int sb = 0; sb < 2; ++sb)
+                                        ptx::tma_load_3d(stg + sb * stg_tok * 128, &tmRes, res_bar,
+                                                         cn.m * kRowsPerTile + row_base + 64 * sb, cn.n * g.n_full, cn.b);
+                                }
+                            }
+                        }
+                        ptx::named_bar_sync(2, kEpiThreads);
+                    }
+                    if (ktr) p.trace[32768 + ep_tile * 4 + 2] = clock64();
+                } else if (TRANS) {
                     OutT *so = reinterpret_cast<OutT *>(stg);
                     if (EPI == 3 || EPI == 4) {
                         ptx::mbar_wait(res_bar, res_phase);
@@ -796,11 +886,13 @@ int umma_max_stages(int box_n, int b_mn_major) {
     return (kSmemLimit - 1024 - kTailBytes) / stage;
 }
 
-size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed, int pair) {
+size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed, int pair,
+                       int half_stg) {
     const size_t ring = (size_t)stages * (kABytes + b_stage_bytes(box_n, b_mn_major));
     const int n_stage = pair ? 2 * box_n : box_n;
     const size_t part = split > 1 ? (size_t)128 * n_stage * 4 : 0;
-    const size_t stg = split > 1 ? (size_t)128 * n_stage * 4 : (transposed ? (size_t)128 * n_stage * out_bytes : 0);
+    const size_t stg = split > 1 ? (size_t)128 * n_stage * 4
+                                 : (transposed ? (size_t)128 * (half_stg ? n_stage / 2 : n_stage) * out_bytes : 0);
     return 1024 /* alignment slack */ + (ring > part ? ring : part) + stg + kTailBytes;
 }
 
