@@ -49,7 +49,7 @@ constexpr int kMaxQT = 64;                // query tiles per request (max_len <=
 constexpr int kRedBytes = 4 * 256 * 4;    // [2 parity][2 halves][128] row max + [2][128] row sums
 // rounded to 1 KiB: the barrier block after it holds the 128-B-aligned maps being patched
 constexpr int kListBytes = (2 * kMaxReq * 4 + kMaxReq * 2 + 2 * (kMaxQT + 1) * 4 + 1023) / 1024 * 1024;
-constexpr int kSmemBytes = 1024 + 6 * kTile + kRedBytes + kListBytes + 512;
+constexpr int kSmemBytes = 1024 + 6 * kTile + kRedBytes + kListBytes + 512;   // + barriers, 2 map scratches
 constexpr int kCtasPerSm = 2;
 
 struct AttnParams {
@@ -59,7 +59,8 @@ struct AttnParams {
     float scale_log2;         // scale * log2(e)
     __nv_bfloat16 *out;
     int64_t ld_out;
-    CUtensorMap *map_slots;   // device token count: 2 per-CTA slots for the extent-patched maps
+    CUtensorMap *map_slots;   // patch_T: 2 per-CTA slots for the extent-patched Q/K and V maps
+    int32_t patch_T;          // device token count: re-encode the Q/K and V maps with T = seq_off[R]
     unsigned long long *trace;   // debug (nimble_debug_trace): CTA 0 per-block clock64 stamps
 };
 
@@ -165,7 +166,7 @@ struct ItemIter {
 
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     attention_varlen_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
-                            const AttnParams p) {
+                            const __grid_constant__ CUtensorMap tmO, const AttnParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *sQ = smem;
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     // publishes copies of both maps with the token extent patched to T (rows past T then
     // zero-fill exactly as with a host-encoded T).
     const CUtensorMap *mQK = &tmQK, *mV = &tmV;
-    if (p.map_slots && warp == 8) {
+    if (p.patch_T && warp == 8) {
         const uint32_t T = (uint32_t)__ldg(p.seq_off + R);
         CUtensorMap *slot = p.map_slots + 2 * (size_t)blockIdx.x;
         mQK = ptx::tmap_patch_extent<2>(&tmQK, smaps, slot, T, lane);
@@ -387,7 +388,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const float sl2 = p.scale_log2;
     uint32_t ns = 0, npv = 0, nitem = 0;
     for (int k = (int)blockIdx.x; k < n_items; k += (int)gridDim.x, ++nitem) {
+        if (warp == 0 && lane == 0) ATT_TRACE(448 + (int)nitem, 0);
         ptx::mbar_wait(q_full, nitem & 1);         // the item's (o, L, qt, h) is published
+        if (warp == 0 && lane == 0) ATT_TRACE(448 + (int)nitem, 1);
         const int4 it = info[nitem & 1];
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(info_read);
@@ -434,6 +437,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             }
             if (tr) ATT_TRACE(tb, 1);
             rd[half * 128 + q] = mx;
+            // the previous item's O tile left sP through a TMA store issued by thread 0: it must
+            // have finished reading before anyone writes P_j (after this barrier)
+            if (j == 0 && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             ptx::named_bar_sync(1, kSoftmaxThreads);
             if (tr) ATT_TRACE(tb, 2);
             // lazy rescaling: the exponent base m_run moves only when the row max grew by more
@@ -514,10 +520,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         }
         // ---------------- epilogue: O / rowsum
         redl[half * 128 + q] = l_run;
+        if (warp == 0 && lane == 0) ATT_TRACE(448 + (int)nitem, 2);
         ptx::mbar_wait(pv_done, npv & 1);
+        if (warp == 0 && lane == 0) ATT_TRACE(448 + (int)nitem, 3);
         ++npv;
         ptx::tc_fence_after();
         ptx::named_bar_sync(1, kSoftmaxThreads);
+        if (warp == 0 && lane == 0) ATT_TRACE(448 + (int)nitem, 4);
         const float inv = 1.f / (redl[q] + redl[128 + q]);
         float t0[16], t1[16];                         // every lane loads: tcgen05.ld is warp-collective
         ptx::tmem_ld16(trow + 128u + (uint32_t)(half * 32), t0);
@@ -525,17 +534,37 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(o_free);      // the next item's first PV may overwrite O
+        if (warp == 0 && lane == 0) ATT_TRACE(448 + (int)nitem, 5);
         const int q0 = it.z * 128;
-        if (q0 + q < L) {
-            __nv_bfloat16 *dst = p.out + (int64_t)(it.x + q0 + q) * p.ld_out + it.w * 64 + half * 32;
-            uint32_t w[16];
+        uint32_t w[16];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                __nv_bfloat162 a = __floats2bfloat162_rn(t0[2 * e] * inv, t0[2 * e + 1] * inv);
-                __nv_bfloat162 b = __floats2bfloat162_rn(t1[2 * e] * inv, t1[2 * e + 1] * inv);
-                w[e] = *reinterpret_cast<uint32_t *>(&a);
-                w[8 + e] = *reinterpret_cast<uint32_t *>(&b);
+        for (int e = 0; e < 8; ++e) {
+            __nv_bfloat162 a = __floats2bfloat162_rn(t0[2 * e] * inv, t0[2 * e + 1] * inv);
+            __nv_bfloat162 b = __floats2bfloat162_rn(t1[2 * e] * inv, t1[2 * e + 1] * inv);
+            w[e] = *reinterpret_cast<uint32_t *>(&a);
+            w[8 + e] = *reinterpret_cast<uint32_t *>(&b);
+        }
+        if (q0 + 128 <= L) {
+            // full query tile: stage the O tile in the (now idle) P buffer in the 128-B swizzle
+            // and let ONE asynchronous TMA store write it — the softmax warps go straight on to
+            // the next item instead of waiting out 64 B of global stores per row (measured: the
+            // output stores cost 10 us of a 76 us layer).  Partial tiles keep plain stores: a TMA
+            // box cannot clip at the request boundary L_i (an output map re-encoded per partial
+            // tile with extent o + L_i measured no faster).
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int c = half * 4 + e;                 // 16-B chunk of the 128-B row
+                *reinterpret_cast<uint4 *>(sP + q * 128 + ((c ^ (q & 7)) << 4)) =
+                    make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
             }
+            ptx::fence_async_smem();
+            ptx::named_bar_sync(1, kSoftmaxThreads);
+            if (threadIdx.x == 0) {
+                ptx::tma_store_2d(&tmO, sP, it.w * 64, it.x + q0);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        } else if (q0 + q < L) {
+            __nv_bfloat16 *dst = p.out + (int64_t)(it.x + q0 + q) * p.ld_out + it.w * 64 + half * 32;
 #pragma unroll
             for (int e = 0; e < 4; ++e)
                 reinterpret_cast<uint4 *>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
@@ -543,6 +572,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         // redl is rewritten by the next item only after this item's blocks: the named barrier of
         // the next item's first block orders it after every thread's read above
     }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // sP read out
     }   // softmax warps
     ptx::tc_fence_before();
     __syncthreads();
@@ -573,9 +603,11 @@ int attention_grid(int R, int max_len, int heads) {
     return (int)(upper < g ? upper : g);
 }
 
-cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const int32_t *seq_off,
+cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const CUtensorMap &tmO,
+                                    const int32_t *seq_off,
                                     int R, int max_len, int heads, float scale, __nv_bfloat16 *out, int64_t ld_out,
-                                    cudaStream_t s, CUtensorMap *map_slots, unsigned long long *trace) {
+                                    cudaStream_t s, CUtensorMap *map_slots, bool patch_T,
+                                    unsigned long long *trace) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(attention_varlen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -591,9 +623,11 @@ cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &
     p.out = out;
     p.ld_out = ld_out;
     p.map_slots = map_slots;
+    p.patch_T = patch_T ? 1 : 0;
     p.trace = trace;
     const dim3 grid((unsigned)attention_grid(R, max_len, heads));
-    return launch_pdl(attention_varlen_kernel, grid, dim3(kThreads), attention_smem_bytes(max_len), s, tmQK, tmV, p);
+    return launch_pdl(attention_varlen_kernel, grid, dim3(kThreads), attention_smem_bytes(max_len), s, tmQK, tmV, tmO,
+                      p);
 }
 
 }  // namespace nimble

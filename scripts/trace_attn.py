@@ -27,7 +27,8 @@ torch.cuda.synchronize()
 nb._lib.nimble_debug_trace(None)
 t = buf.cpu().numpy().reshape(-1, 8).astype(np.float64)
 pr = t[256:384]
-mm = t[384:]
+mm = t[384:448]
+sm = t[448:512]
 t = t[:256]
 n = int((t[:, 0] > 0).sum())
 t = t[:n]
@@ -47,6 +48,9 @@ print(" MMA at Q wait:", " ".join("%d" % (v - t0) for v in mm[:, 0] if v > 0))
 print(" MMA saw Q:", " ".join("%d" % (v - t0) for v in pr[:, 7] if v > 0))
 print(" K issued:", " ".join("%d" % (v - t0) for v in pr[:, 4] if v > 0))
 print(" V issued:", " ".join("%d" % (v - t0) for v in pr[:, 5] if v > 0))
+print(" softmax per item: [before q_full, after q_full, epi start, pv_done seen, rowsum xchg, o_free]:")
+for i in range(min(6, int((sm[:, 0] > 0).sum()))):
+    print("   item %d:" % i, " ".join("%d" % (v - t0) for v in sm[i, :6]))
 d = np.diff(t[:, 0])
 print("S-ready to S-ready median %.0f clk; phases (median clk): ld+max %.0f, xchg %.0f, exp %.0f, pvwait %.0f, P %.0f"
       % (np.median(d), *[np.median(t[:, i + 1] - t[:, i]) for i in range(5)]))
