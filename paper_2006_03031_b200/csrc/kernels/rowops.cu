@@ -1,6 +1,8 @@
 // Row ops around bmm_dyn in a BERT encoder layer: softmax over the dynamic
 // sequence length L and LayerNorm (the paper is silent on both; DESIGN.md
 // readings 9-10).  Memory-bound; 16-B vector loads where the layout allows.
+#include <cstdlib>
+
 #include "launch.h"
 #include "ptx.cuh"
 
@@ -133,6 +135,98 @@ __global__ void __launch_bounds__(256) layernorm_warp_kernel(const __nv_bfloat16
     }
 }
 
+// d = 1024 (BERT-large) at many rows: one wave of 12-warp CTAs (one per SM), each warp
+// normalising `rpw` consecutive rows with gamma / beta held in registers (loaded once per warp
+// instead of once per row: 8 KB of L1 traffic per row saved) and the next row's 16-B loads
+// issued before the current row's arithmetic.  Per row the arithmetic is exactly
+// layernorm_warp_kernel<4>'s (same order), so both agree bit for bit.
+constexpr int kLnWarps = 12;
+__global__ void __launch_bounds__(32 * kLnWarps, 1) layernorm_rows_kernel(const __nv_bfloat16 *__restrict__ X,
+                                                                         int64_t ldx, const float *__restrict__ g,
+                                                                         const float *__restrict__ be, float eps,
+                                                                         __nv_bfloat16 *__restrict__ Y, int64_t ldy,
+                                                                         int64_t rows, int32_t rpw,
+                                                                         const int32_t *__restrict__ rows_dev) {
+    constexpr int CH = 4, d = 1024;
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    if (rows_dev) {
+        const int32_t r = *rows_dev;
+        if (r < 1 || r > rows) __trap();
+        rows = r;
+    }
+    const int64_t row0 = ((int64_t)blockIdx.x * kLnWarps + (threadIdx.x >> 5)) * rpw;
+    if (row0 >= rows) return;
+    const int lane = threadIdx.x & 31;
+    float gg[CH * 8], bb[CH * 8];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+        const int j = (lane + 32 * q) * 8;
+        const float4 g0 = *reinterpret_cast<const float4 *>(g + j), g1 = *reinterpret_cast<const float4 *>(g + j + 4);
+        const float4 b0 = *reinterpret_cast<const float4 *>(be + j), b1 = *reinterpret_cast<const float4 *>(be + j + 4);
+        gg[8 * q + 0] = g0.x; gg[8 * q + 1] = g0.y; gg[8 * q + 2] = g0.z; gg[8 * q + 3] = g0.w;
+        gg[8 * q + 4] = g1.x; gg[8 * q + 5] = g1.y; gg[8 * q + 6] = g1.z; gg[8 * q + 7] = g1.w;
+        bb[8 * q + 0] = b0.x; bb[8 * q + 1] = b0.y; bb[8 * q + 2] = b0.z; bb[8 * q + 3] = b0.w;
+        bb[8 * q + 4] = b1.x; bb[8 * q + 5] = b1.y; bb[8 * q + 6] = b1.z; bb[8 * q + 7] = b1.w;
+    }
+    uint4 cur[CH], nxt[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) cur[q] = *reinterpret_cast<const uint4 *>(X + row0 * ldx + (lane + 32 * q) * 8);
+#pragma unroll 1
+    for (int r = 0; r < rpw; ++r) {
+        const int64_t row = row0 + r;
+        if (row >= rows) break;
+        const bool more = r + 1 < rpw && row + 1 < rows;
+        if (more) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) nxt[q] = *reinterpret_cast<const uint4 *>(X + (row + 1) * ldx + (lane + 32 * q) * 8);
+        }
+        // the row stays packed (bf16) in cur[]: values are re-expanded per pass (fewer registers)
+        float sum = 0.f;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&cur[q]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                sum += f.x;
+                sum += f.y;
+            }
+        }
+        const float mean = warp_sum(sum) / (float)d;
+        float ss = 0.f;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&cur[q]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                const float t0 = f.x - mean, t1 = f.y - mean;
+                ss += t0 * t0;
+                ss += t1 * t1;
+            }
+        }
+        const float inv = rsqrtf(warp_sum(ss) / (float)d + eps);
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&cur[q]);
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                __nv_bfloat162 h2 = __floats2bfloat162_rn((f.x - mean) * inv * gg[8 * q + 2 * e] + bb[8 * q + 2 * e],
+                                                          (f.y - mean) * inv * gg[8 * q + 2 * e + 1] + bb[8 * q + 2 * e + 1]);
+                w[e] = *reinterpret_cast<uint32_t *>(&h2);
+            }
+            *reinterpret_cast<uint4 *>(Y + row * ldy + (lane + 32 * q) * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        if (more) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) cur[q] = nxt[q];
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_softmax_rows(const float *S, int64_t ldS, int64_t strideS, __nv_bfloat16 *P, int64_t ldP,
@@ -147,6 +241,14 @@ cudaError_t launch_layernorm(const __nv_bfloat16 *X, int64_t ldx, const float *g
                              __nv_bfloat16 *Y, int64_t ldy, int64_t rows, int64_t d, cudaStream_t s,
                              const int32_t *rows_dev) {
     if (d > 4096 || d % 8) return cudaErrorInvalidValue;
+    static const bool rows_off = [] { const char *e = std::getenv("NIMBLE_LN_ROWS"); return e && e[0] == '0'; }();
+    if (d == 1024 && rows >= 4 * kLnWarps * 148 && !rows_off) {   // >= 4 rows per warp amortise gamma / beta
+        const int64_t warps = (int64_t)kLnWarps * 148;
+        const int32_t rpw = (int32_t)((rows + warps - 1) / warps);
+        const int64_t ctas = ((rows + rpw - 1) / rpw + kLnWarps - 1) / kLnWarps;
+        return launch_pdl(layernorm_rows_kernel, dim3((unsigned)ctas), dim3(32 * kLnWarps), 0, s, X, ldx, g, b, eps, Y,
+                          ldy, rows, rpw, rows_dev);
+    }
     const dim3 grid((unsigned)((rows + 7) / 8)), block(256);
     if (d <= 1024)
         return launch_pdl(layernorm_warp_kernel<4>, grid, block, 0, s, X, ldx, g, b, eps, Y, ldy, rows, (int)d, rows_dev);
