@@ -576,13 +576,15 @@ static int attention_impl(const void *qkv, int64_t ld_qkv, int64_t T, const int3
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     // output [T x ld_out] bf16: 2-D view {heads * 64 columns, T rows}, box {64, 128} in the
     // 128-B swizzle the kernel stages full query tiles in (one TMA store per full tile)
-    CUtensorMap tmO;
-    if (r == CUDA_SUCCESS) {
+    // (+ the same view with 64 / 32 / 16 / 8-row boxes for the valid rows of partial tiles)
+    CUtensorMap tmO, tmOp[4];
+    for (int b = -1; b < 4 && r == CUDA_SUCCESS; ++b) {
         cuuint64_t odims[2] = {(cuuint64_t)heads * 64, (cuuint64_t)T};
         cuuint64_t ostr[1] = {(cuuint64_t)ld_out * 2};
-        cuuint32_t obox[2] = {64, 128}, oestr[2] = {1, 1};
-        r = g_encode(&tmO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, odims, ostr, obox, oestr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        cuuint32_t obox[2] = {64, b < 0 ? 128u : (64u >> b)}, oestr[2] = {1, 1};
+        r = g_encode(b < 0 ? &tmO : &tmOp[b], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, odims, ostr, obox, oestr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) return fail(NIMBLE_E_CUDA, "cuTensorMapEncodeTiled(attention) failed (code " + std::to_string((int)r) + ")");
     // per-CTA tensor-map slots: the device-extent form patches its Q/K and V maps (extent T)
@@ -602,7 +604,7 @@ static int attention_impl(const void *qkv, int64_t ld_qkv, int64_t T, const int3
             e = next_slot_block(g_attn_slots, &sl);
             if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen_dev slot ring", e);
         }
-        e = launch_attention_varlen(tmQK, tmV, tmO, seq_off + r0, Rc, max_len, heads, scale,
+        e = launch_attention_varlen(tmQK, tmV, tmO, tmOp, seq_off + r0, Rc, max_len, heads, scale,
                                     static_cast<__nv_bfloat16 *>(out), ld_out, static_cast<cudaStream_t>(stream), sl,
                                     dev, g_trace);
         if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen launch", e);

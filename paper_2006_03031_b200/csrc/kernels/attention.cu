@@ -52,6 +52,13 @@ constexpr int kListBytes = (2 * kMaxReq * 4 + kMaxReq * 2 + 2 * (kMaxQT + 1) * 4
 constexpr int kSmemBytes = 1024 + 6 * kTile + kRedBytes + kListBytes + 512;   // + barriers, 2 map scratches
 constexpr int kCtasPerSm = 2;
 
+// TMA maps of the output with boxes of 64, 32, 16 and 8 rows: a partial query tile's valid
+// rows leave as a 64/32/16/8-row decomposition (starting rows stay multiples of 8, so every
+// box starts on a 1 KB swizzle atom of the staging); only the last < 8 rows use plain stores.
+struct OutMaps {
+    CUtensorMap box[4];
+};
+
 struct AttnParams {
     const int32_t *seq_off;   // [R + 1] prefix sums of request lengths (device)
     int32_t R;
@@ -166,7 +173,8 @@ struct ItemIter {
 
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     attention_varlen_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
-                            const __grid_constant__ CUtensorMap tmO, const AttnParams p) {
+                            const __grid_constant__ CUtensorMap tmO, const __grid_constant__ OutMaps tmOp,
+                            const AttnParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *sQ = smem;
@@ -544,30 +552,46 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             w[e] = *reinterpret_cast<uint32_t *>(&a);
             w[8 + e] = *reinterpret_cast<uint32_t *>(&b);
         }
-        if (q0 + 128 <= L) {
-            // full query tile: stage the O tile in the (now idle) P buffer in the 128-B swizzle
-            // and let ONE asynchronous TMA store write it — the softmax warps go straight on to
-            // the next item instead of waiting out 64 B of global stores per row (measured: the
-            // output stores cost 10 us of a 76 us layer).  Partial tiles keep plain stores: a TMA
-            // box cannot clip at the request boundary L_i (an output map re-encoded per partial
-            // tile with extent o + L_i measured no faster).
+        // stage the normalised O tile in the (now idle) P buffer in the 128-B swizzle and let
+        // asynchronous TMA stores write it — the softmax warps go straight on to the next item
+        // instead of waiting out 64 B of global stores per row (measured: the per-row output
+        // stores cost 10 us of a 76 us layer).  A full tile is one 128-row store; a partial
+        // tile's n = L - q0 valid rows leave as 64/32/16/8-row boxes (a TMA box cannot clip at
+        // the request boundary L_i) plus plain stores for the last n % 8 rows.
+        const int nv = min(128, L - q0);                    // valid rows of this query tile
+        const int n8 = nv & ~7;                             // rows covered by TMA boxes
+        if (q < n8) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int c = half * 4 + e;                 // 16-B chunk of the 128-B row
                 *reinterpret_cast<uint4 *>(sP + q * 128 + ((c ^ (q & 7)) << 4)) =
                     make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
             }
-            ptx::fence_async_smem();
-            ptx::named_bar_sync(1, kSoftmaxThreads);
-            if (threadIdx.x == 0) {
-                ptx::tma_store_2d(&tmO, sP, it.w * 64, it.x + q0);
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-        } else if (q0 + q < L) {
+        } else if (q < nv) {
             __nv_bfloat16 *dst = p.out + (int64_t)(it.x + q0 + q) * p.ld_out + it.w * 64 + half * 32;
 #pragma unroll
             for (int e = 0; e < 4; ++e)
                 reinterpret_cast<uint4 *>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+        }
+        if (n8 > 0) {
+            ptx::fence_async_smem();
+            ptx::named_bar_sync(1, kSoftmaxThreads);
+            if (threadIdx.x == 0) {
+                if (n8 == 128) {
+                    ptx::tma_store_2d(&tmO, sP, it.w * 64, it.x + q0);
+                } else {
+                    int r0 = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {            // box rows 64, 32, 16, 8
+                        const int br = 64 >> b;
+                        if (n8 & br) {
+                            ptx::tma_store_2d(&tmOp.box[b], sP + r0 * 128, it.w * 64, it.x + q0 + r0);
+                            r0 += br;
+                        }
+                    }
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
         }
         // redl is rewritten by the next item only after this item's blocks: the named barrier of
         // the next item's first block orders it after every thread's read above
@@ -604,7 +628,7 @@ int attention_grid(int R, int max_len, int heads) {
 }
 
 cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const CUtensorMap &tmO,
-                                    const int32_t *seq_off,
+                                    const CUtensorMap *tmOparts, const int32_t *seq_off,
                                     int R, int max_len, int heads, float scale, __nv_bfloat16 *out, int64_t ld_out,
                                     cudaStream_t s, CUtensorMap *map_slots, bool patch_T,
                                     unsigned long long *trace) {
@@ -626,8 +650,10 @@ cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &
     p.patch_T = patch_T ? 1 : 0;
     p.trace = trace;
     const dim3 grid((unsigned)attention_grid(R, max_len, heads));
+    OutMaps op;
+    for (int b = 0; b < 4; ++b) op.box[b] = tmOparts[b];
     return launch_pdl(attention_varlen_kernel, grid, dim3(kThreads), attention_smem_bytes(max_len), s, tmQK, tmV, tmO,
-                      p);
+                      op, p);
 }
 
 }  // namespace nimble

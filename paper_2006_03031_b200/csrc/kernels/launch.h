@@ -113,7 +113,7 @@ size_t attention_smem_bytes(int max_len);
 int attention_max_requests();                     // R bound of one launch (work list in smem)
 int attention_grid(int R, int max_len, int heads);   // persistent CTAs: <= 2 per SM
 cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const CUtensorMap &tmO,
-                                    const int32_t *seq_off,
+                                    const CUtensorMap *tmOparts, const int32_t *seq_off,
                                     int R, int max_len, int heads, float scale, __nv_bfloat16 *out, int64_t ld_out,
                                     cudaStream_t s, CUtensorMap *map_slots, bool patch_T,
                                     unsigned long long *trace = nullptr);
