@@ -31,6 +31,14 @@
  *    no floating-point atomics).
  *  - Thread safety: all entry points are re-entrant; nimble_set_variant_limit is
  *    process-global and must be set before concurrent use.
+ *  - Programmatic dependent launch (PDL, on unless NIMBLE_PDL=0): every kernel lets the
+ *    next kernel on its stream start its prologue early, and the GEMMs (dense_dyn,
+ *    dense_dyn_dev, dense_ln_dyn, dense_static) TMA-load the WEIGHT operand W of their
+ *    first tiles BEFORE waiting for the preceding kernel (its bias, residual and x are
+ *    read after the wait).  W must therefore not be written by the immediately preceding
+ *    work on the same stream: weights are static per model (P:386-387 tiles the
+ *    symbolic extent only).  Passing a just-computed activation as W needs NIMBLE_PDL=0
+ *    or an event / other kernel in between.  bmm_dyn and attention wait before every load.
  */
 #ifndef NIMBLE_H_
 #define NIMBLE_H_
@@ -155,8 +163,13 @@ int nimble_dense_static(const void *x, int64_t ldx, const void *W, int64_t ldw, 
  * Where the residue dispatch picks the 2-CTA family (M >= 2048), N = 1024 and K >= 2048
  * (a main loop long enough to hide the exchange) the LayerNorm runs in the GEMM epilogue: the 8 CTAs holding the four 256-feature quarters of a
  * 256-token tile exchange per-token (sum, sum of squares) partials through a library
- * workspace (one such launch in flight per device); the pre-LN sum is rounded to bf16
- * first, as in the two-launch form.  Elsewhere: nimble_dense_dyn then nimble_layernorm in
+ * workspace owned by the calling STREAM (a pool of 16 per device: launches on different
+ * streams never share counters; two CUDA graphs captured on the same stream share one and
+ * must not replay concurrently; more than 16 streams share slots round-robin).  The groups
+ * spin on each other, so the group count is capped by the co-resident CTA pairs the
+ * occupancy API reports (the two-launch form when none; also when the device's workspace
+ * pool would first be allocated inside a graph capture).  The pre-LN sum is rounded to
+ * bf16 first, as in the two-launch form.  Elsewhere: nimble_dense_dyn then nimble_layernorm in
  * place on y (same results up to the variance formula: fused = E[v^2] - mean^2 in fp32,
  * two-launch = two-pass).  Errors as nimble_dense_dyn; N % 8 != 0 or N > 4096 ->
  * E_UNSUPPORTED. */
@@ -200,6 +213,17 @@ int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const void *B, i
                    int64_t batch, int64_t M, int64_t N, int64_t K, float alpha, int in_dt,
                    int out_dt, void *stream);
 
+/* nimble_bmm_static — measurement baseline for bmm_dyn: the same kernel source with
+ * (M, N, K) compile-time constants (fig:sym-codegen P:696-703), for the attention-score form
+ * only (trans_b = 0, fp32 output, alpha epilogue): (M, N, K) in {(128,128,64), (512,512,64),
+ * (513,513,64), (2048,2048,64), (2049,2049,64)}; batch, strides and leading dims at run time.
+ * Same arguments and dispatch record as nimble_bmm_dyn; other shapes / forms ->
+ * NIMBLE_E_UNSUPPORTED. */
+int nimble_bmm_static(const void *A, int64_t lda, int64_t strideA, const void *B, int64_t ldb,
+                      int64_t strideB, int trans_b, void *C, int64_t ldc, int64_t strideC,
+                      int64_t batch, int64_t M, int64_t N, int64_t K, float alpha, int in_dt,
+                      int out_dt, void *stream);
+
 /* ---------------------------------------------------------------------------
  * nimble_attention_varlen — fused attention over token-packed variable-length
  * requests: for request i = 0..R-1 (tokens
@@ -213,7 +237,10 @@ int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const void *B, i
  * request) items built on the device from seq_off); S and P stay on chip (TMEM /
  * smem; more than 1024 requests run as consecutive launches of 1024).  head_dim must be
  * 64 and max_len <= 8192 (E_UNSUPPORTED otherwise); qkv/out 16-byte aligned with
- * ld*2 % 16 == 0 (E_ALIGN).
+ * ld*2 % 16 == 0 (E_ALIGN).  seq_off is device data the host never reads: the kernel
+ * validates it (seq_off[0] >= 0, nondecreasing, every L_i <= max_len, seq_off[R] <= T) and
+ * traps (a sticky launch failure at the next synchronisation) instead of reading or
+ * writing out of bounds.
  * ------------------------------------------------------------------------- */
 int nimble_attention_varlen(const void *qkv, int64_t ld_qkv, int64_t T, const int32_t *seq_off, int32_t R,
                             int32_t max_len, int32_t heads, int32_t head_dim, float scale, void *out,

@@ -9,6 +9,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../kernels/launch.h"
 #include "internal.h"
@@ -145,13 +147,15 @@ void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
     L.p.tiles_m = L.pair ? (L.p.rows_a + 255) / 256 : d.grid[0];   // pairs own 256-row tiles
     L.p.tiles_n = d.grid[1];
     L.p.batch = d.grid[2] / d.split_k;
+    static const bool l2pf_on = [] { const char *e = std::getenv("NIMBLE_L2PF"); return !(e && e[0] == '0'); }();
+    const int64_t tiles = (int64_t)L.p.tiles_m * L.p.tiles_n * L.p.batch;
+    const int64_t slots = L.pair ? kNumSMs / 2 : kNumSMs;
     if (L.p.split > 1) {
         L.grid = dim3(d.grid[0], d.grid[1], d.grid[2]);
     } else {
-        const int64_t tiles = (int64_t)L.p.tiles_m * L.p.tiles_n * L.p.batch;
-        const int64_t slots = L.pair ? kNumSMs / 2 : kNumSMs;
         L.grid = dim3((unsigned)((tiles < slots ? tiles : slots) * (L.pair ? 2 : 1)), 1, 1);
     }
+    L.p.l2pf = (l2pf_on && tiles <= slots) ? 1 : 0;      // one wave: every CTA owns <= 1 tile
 }
 
 }  // namespace
@@ -179,29 +183,48 @@ extern "C" int nimble_last_dispatch(nimble_dispatch *out) {
 // ------------------------------------------------------------------ dense_dyn
 // Library workspace of the fused LayerNorm epilogue: per group of 4 CTA pairs, 2 slots of
 // (sum, sum of squares) partials for 256 tokens x 8 CTAs, and 2 self-resetting counters per slot.
+// One workspace per STREAM (a pool of kLnSlots per device, allocated together on the first fused
+// launch of the device, so a stream first seen during graph capture needs no allocation): two
+// streams running dense_ln_dyn concurrently never share counters.  More than kLnSlots distinct
+// streams share slots round-robin (documented in include/nimble.h).
 namespace nimble {
 namespace {
 constexpr int kLnMaxGroups = kNumSMs / 8;
+constexpr int kLnSlots = 16;
+constexpr size_t kLnStatsElems = (size_t)2 * kLnMaxGroups * 8 * 256;
+constexpr size_t kLnCntElems = (size_t)2 * kLnMaxGroups * 2;
 struct LnWorkspace {
     std::mutex mu;
     float2 *stats[64] = {};
     int32_t *cnt[64] = {};
+    std::vector<std::pair<cudaStream_t, int>> owner[64];   // stream -> slot
 };
 LnWorkspace g_ln_ws;
-cudaError_t ln_workspace(float2 **stats, int32_t **cnt) {
+cudaError_t ln_workspace(cudaStream_t stream, float2 **stats, int32_t **cnt) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     std::lock_guard<std::mutex> lk(g_ln_ws.mu);
     if (!g_ln_ws.stats[dev]) {
-        if ((e = cudaMalloc(&g_ln_ws.stats[dev], sizeof(float2) * 2 * kLnMaxGroups * 8 * 256)) != cudaSuccess) return e;
-        if ((e = cudaMalloc(&g_ln_ws.cnt[dev], sizeof(int32_t) * 2 * kLnMaxGroups * 2)) != cudaSuccess) return e;
-        if ((e = cudaMemset(g_ln_ws.cnt[dev], 0, sizeof(int32_t) * 2 * kLnMaxGroups * 2)) != cudaSuccess) return e;
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+            return cudaErrorStreamCaptureUnsupported;        // caller falls back to the two-launch form
+        if ((e = cudaMalloc(&g_ln_ws.stats[dev], sizeof(float2) * kLnStatsElems * kLnSlots)) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&g_ln_ws.cnt[dev], sizeof(int32_t) * kLnCntElems * kLnSlots)) != cudaSuccess) return e;
+        if ((e = cudaMemset(g_ln_ws.cnt[dev], 0, sizeof(int32_t) * kLnCntElems * kLnSlots)) != cudaSuccess) return e;
         if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
     }
-    *stats = g_ln_ws.stats[dev];
-    *cnt = g_ln_ws.cnt[dev];
+    auto &own = g_ln_ws.owner[dev];
+    int slot = -1;
+    for (const auto &o : own)
+        if (o.first == stream) slot = o.second;
+    if (slot < 0) {
+        slot = (int)(own.size() % kLnSlots);
+        own.emplace_back(stream, slot);
+    }
+    *stats = g_ln_ws.stats[dev] + (size_t)slot * kLnStatsElems;
+    *cnt = g_ln_ws.cnt[dev] + (size_t)slot * kLnCntElems;
     return cudaSuccess;
 }
 bool half_staging_enabled() {
@@ -316,15 +339,24 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
         L.tmRes = L.tmOut;
     }
     L.p.box_n = box_b;
-    if (L.pair && (L.p.a_batch_mid || L.p.b_batch_mid)) return fail(NIMBLE_E_UNSUPPORTED, "pair mode needs row-major batches");
+    if (L.pair && (L.p.a_batch_mid || L.p.b_batch_mid || L.p.out_batch_mid))
+        return fail(NIMBLE_E_UNSUPPORTED, "nimble_dense_dyn: dense operands are single-batch (internal error)");
     plan_pipeline(L, d);
     L.stream = s;
     if (ln) {
+        // the 8 CTAs of a group spin on each other: every group must be co-resident, so the
+        // group count is capped by the occupancy API's count of co-resident CTA pairs (fewer
+        // SMs under MPS / green contexts shrink it; none left -> the two-launch form)
+        const int max_groups = ln_fused ? umma_ln_max_groups(L.smem_bytes) : 0;
+        if (max_groups < 1) ln_fused = false;
+        if (ln_fused && ln_workspace(s, &L.p.ln_stats, &L.p.ln_cnt) != cudaSuccess) {
+            cudaGetLastError();
+            ln_fused = false;                                   // e.g. first use inside a capture
+        }
         ln->fused = ln_fused;
         if (ln->fused) {
-            cudaError_t e = ln_workspace(&L.p.ln_stats, &L.p.ln_cnt);
-            if (e != cudaSuccess) return cuda_fail("nimble_dense_ln_dyn workspace", e);
-            const int groups = L.p.tiles_n < kLnMaxGroups ? L.p.tiles_n : kLnMaxGroups;
+            int groups = L.p.tiles_n < kLnMaxGroups ? L.p.tiles_n : kLnMaxGroups;
+            if (groups > max_groups) groups = max_groups;
             L.p.ln_groups = groups;
             L.p.ln_gamma = ln->gamma;
             L.p.ln_beta = ln->beta;
@@ -473,9 +505,10 @@ extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, i
 }
 
 // ------------------------------------------------------------------ bmm_dyn
-extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const void *B, int64_t ldb,
-                              int64_t strideB, int trans_b, void *Cout, int64_t ldc, int64_t strideC, int64_t batch,
-                              int64_t M, int64_t N, int64_t K, float alpha, int in_dt, int out_dt, void *stream) {
+static int bmm_impl(const void *A, int64_t lda, int64_t strideA, const void *B, int64_t ldb,
+                    int64_t strideB, int trans_b, void *Cout, int64_t ldc, int64_t strideC, int64_t batch,
+                    int64_t M, int64_t N, int64_t K, float alpha, int in_dt, int out_dt, void *stream,
+                    bool static_twin) {
     if (!ext_ok(batch) || !ext_ok(M) || !ext_ok(N) || !ext_ok(K))
         return fail(NIMBLE_E_EXTENT, "nimble_bmm_dyn: extents must be in [1, 2^31-1]");
     const int64_t as[3] = {batch, M, K};
@@ -538,11 +571,27 @@ extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const
     }
     plan_pipeline(L, d);
     L.stream = s;
-    cudaError_t e = launch_umma_gemm(L);
+    if (static_twin && (trans_b || out_dt != NIMBLE_F32 || !umma_static_bmm_available(M, N, K)))
+        return fail(NIMBLE_E_UNSUPPORTED, "nimble_bmm_static: (M, N, K) not compiled in, or trans_b / bf16 output");
+    cudaError_t e = static_twin ? launch_umma_gemm_static(L, M, N, K) : launch_umma_gemm(L);
     if (e != cudaSuccess) return cuda_fail("nimble_bmm_dyn launch", e);
     record_dispatch(d);
     clear_error();
     return NIMBLE_OK;
+}
+
+extern "C" int nimble_bmm_dyn(const void *A, int64_t lda, int64_t strideA, const void *B, int64_t ldb,
+                              int64_t strideB, int trans_b, void *Cout, int64_t ldc, int64_t strideC, int64_t batch,
+                              int64_t M, int64_t N, int64_t K, float alpha, int in_dt, int out_dt, void *stream) {
+    return bmm_impl(A, lda, strideA, B, ldb, strideB, trans_b, Cout, ldc, strideC, batch, M, N, K, alpha, in_dt,
+                    out_dt, stream, false);
+}
+
+extern "C" int nimble_bmm_static(const void *A, int64_t lda, int64_t strideA, const void *B, int64_t ldb,
+                                 int64_t strideB, int trans_b, void *Cout, int64_t ldc, int64_t strideC, int64_t batch,
+                                 int64_t M, int64_t N, int64_t K, float alpha, int in_dt, int out_dt, void *stream) {
+    return bmm_impl(A, lda, strideA, B, ldb, strideB, trans_b, Cout, ldc, strideC, batch, M, N, K, alpha, in_dt,
+                    out_dt, stream, true);
 }
 
 // ------------------------------------------------------------------ varlen attention
@@ -605,7 +654,7 @@ static int attention_impl(const void *qkv, int64_t ld_qkv, int64_t T, const int3
             if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen_dev slot ring", e);
         }
         e = launch_attention_varlen(tmQK, tmV, tmO, tmOp, seq_off + r0, Rc, max_len, heads, scale,
-                                    static_cast<__nv_bfloat16 *>(out), ld_out, static_cast<cudaStream_t>(stream), sl,
+                                    static_cast<__nv_bfloat16 *>(out), ld_out, T, static_cast<cudaStream_t>(stream), sl,
                                     dev, g_trace);
         if (e != cudaSuccess) return cuda_fail("nimble_attention_varlen launch", e);
     }

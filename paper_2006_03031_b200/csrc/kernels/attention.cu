@@ -68,6 +68,8 @@ struct AttnParams {
     int64_t ld_out;
     CUtensorMap *map_slots;   // patch_T: 2 per-CTA slots for the extent-patched Q/K and V maps
     int32_t patch_T;          // device token count: re-encode the Q/K and V maps with T = seq_off[R]
+    int32_t T_max;            // bound on seq_off[R] (the tensor maps' / output's row extent)
+    int32_t max_len;          // bound on every L_i
     unsigned long long *trace;   // debug (nimble_debug_trace): CTA 0 per-block clock64 stamps
 };
 
@@ -225,6 +227,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     ptx::pdl_wait();                              // QKV and seq_off come from earlier work
     ptx::pdl_trigger();
     __syncthreads();
+    // ---- seq_off is device data: a non-monotone prefix, an L_i above max_len or a total above
+    //      the row extent the maps were encoded for would send TMA / row stores out of bounds
+    for (int r = threadIdx.x; r < R; r += kThreads) {
+        const int a = __ldg(p.seq_off + r), b = __ldg(p.seq_off + r + 1);
+        if (a < 0 || b < a || b - a > p.max_len || b > p.T_max) __trap();
+    }
     // ---- work list (identical in every CTA): counting sort of the requests by query tiles, descending
     for (int r = threadIdx.x; r < R; r += kThreads) atomicAdd(&cnt[min(qtiles_of(p.seq_off, r), kMaxQT)], 1);
     __syncthreads();
@@ -630,7 +638,7 @@ int attention_grid(int R, int max_len, int heads) {
 cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const CUtensorMap &tmO,
                                     const CUtensorMap *tmOparts, const int32_t *seq_off,
                                     int R, int max_len, int heads, float scale, __nv_bfloat16 *out, int64_t ld_out,
-                                    cudaStream_t s, CUtensorMap *map_slots, bool patch_T,
+                                    int64_t T_max, cudaStream_t s, CUtensorMap *map_slots, bool patch_T,
                                     unsigned long long *trace) {
     static bool attr = false;
     if (!attr) {
@@ -648,6 +656,8 @@ cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &
     p.ld_out = ld_out;
     p.map_slots = map_slots;
     p.patch_T = patch_T ? 1 : 0;
+    p.T_max = (int32_t)T_max;
+    p.max_len = max_len;
     p.trace = trace;
     const dim3 grid((unsigned)attention_grid(R, max_len, heads));
     OutMaps op;

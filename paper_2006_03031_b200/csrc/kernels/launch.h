@@ -57,6 +57,10 @@ struct UmmaParams {
     // half staging (2-CTA family, bf16, EPI <= 3): the epilogue stages and stores the tile in two
     // 128-token halves through a 32 KB buffer, which leaves room for a 6th pipeline stage
     int32_t half_stg;
+    // one-wave launches (every CTA owns at most one tile): prefetch the first tile's remaining
+    // k-blocks of both operands into L2 at kernel start (weights before the PDL wait), so the
+    // DRAM fetch of a cold weight slab runs at full parallelism instead of ring-depth bound
+    int32_t l2pf;
 };
 
 struct UmmaLaunch {
@@ -71,6 +75,8 @@ struct UmmaLaunch {
 
 cudaError_t launch_umma_gemm(const UmmaLaunch &L);
 bool umma_static_available(int64_t M, int64_t N, int64_t K);
+bool umma_static_bmm_available(int64_t M, int64_t N, int64_t K);
+int umma_ln_max_groups(size_t smem_bytes);   // co-resident 4-pair groups for the fused-LN GEMM
 cudaError_t launch_umma_gemm_static(const UmmaLaunch &L, int64_t M, int64_t N, int64_t K);
 size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed, int pair,
                        int half_stg = 0);
@@ -115,7 +121,7 @@ int attention_grid(int R, int max_len, int heads);   // persistent CTAs: <= 2 pe
 cudaError_t launch_attention_varlen(const CUtensorMap &tmQK, const CUtensorMap &tmV, const CUtensorMap &tmO,
                                     const CUtensorMap *tmOparts, const int32_t *seq_off,
                                     int R, int max_len, int heads, float scale, __nv_bfloat16 *out, int64_t ld_out,
-                                    cudaStream_t s, CUtensorMap *map_slots, bool patch_T,
+                                    int64_t T_max, cudaStream_t s, CUtensorMap *map_slots, bool patch_T,
                                     unsigned long long *trace = nullptr);
 
 cudaError_t launch_softmax_rows(const float *S, int64_t ldS, int64_t strideS, __nv_bfloat16 *P, int64_t ldP,

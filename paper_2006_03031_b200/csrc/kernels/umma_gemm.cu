@@ -61,14 +61,17 @@ __host__ __device__ inline int pow2_cols(int n) { return n <= 32 ? 32 : n <= 64 
 struct Geo {
     int rows_a, rows_b, n_full, n_tail, tiles_m, tiles_n, box_n, kb_total;
 };
-template <int SM, int SN, int SK>
+template <int SM, int SN, int SK, int PAIR>
 __device__ __forceinline__ Geo make_geo(const UmmaParams &p) {
     if constexpr (SM > 0) {
+        // the DISPATCH.md rule at compile time: family 1 (t = 128) below 2048, else family 3
+        // (t = 256, CTA pairs: 256-row weight tiles, each CTA loads half of the token box)
         constexpr int t = SM < 2048 ? 128 : 256;
         constexpr int r = SM % t;
         constexpr int tiles_n = SM / t + (r ? 1 : 0);
         constexpr int n_tail = r ? 16 * ((r + 15) / 16) : t;
-        return Geo{SN, SM, t, n_tail, (SN + 127) / 128, tiles_n, tiles_n == 1 ? n_tail : t, (SK + 63) / 64};
+        constexpr int box = (tiles_n == 1 ? n_tail : t) / (PAIR ? 2 : 1);
+        return Geo{SN, SM, t, n_tail, PAIR ? (SN + 255) / 256 : (SN + 127) / 128, tiles_n, box, (SK + 63) / 64};
     } else {
         return Geo{p.rows_a, p.rows_b, p.n_full, p.n_tail, p.tiles_m, p.tiles_n, p.box_n, p.kb_total};
     }
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const UmmaParams p) {
     using OutT = typename std::conditional<OUT_F32, float, __nv_bfloat16>::type;
     constexpr bool HALF_OK = PAIR && !OUT_F32 && EPI <= 3 && !B_MN;   // half staging supported
-    Geo g = make_geo<SM, SN, SK>(p);
+    Geo g = make_geo<SM, SN, SK, PAIR>(p);
     const bool devm = p.m_dev != nullptr;          // extent on the device (dense_dyn_dev)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the 128-B swizzle atoms.  Offset the __shared__ array itself (no
@@ -367,8 +370,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             auto load_a = [&](int st, int kb) {
                 uint8_t *sa = smem + st * stage_bytes;
                 const int32_t kc = kb * kBlockK;
-                if (PAIR) ptx::tma_load_3d_pair(sa, &tmA, &full_bar[st], kc, a_row, ab);
-                else if (p.a_batch_mid) ptx::tma_load_3d(sa, &tmA, &full_bar[st], kc, ab, a_row);
+                // heads interleaved inside a row (QKV views): batch is the middle tensor-map dim
+                if (PAIR) {
+                    if (p.a_batch_mid) ptx::tma_load_3d_pair(sa, &tmA, &full_bar[st], kc, ab, a_row);
+                    else ptx::tma_load_3d_pair(sa, &tmA, &full_bar[st], kc, a_row, ab);
+                } else if (p.a_batch_mid) ptx::tma_load_3d(sa, &tmA, &full_bar[st], kc, ab, a_row);
                 else ptx::tma_load_3d(sa, &tmA, &full_bar[st], kc, a_row, ab);
             };
             auto load_b = [&](int st, int kb) {
@@ -381,10 +387,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[st], b_row + 64 * q, kc, bb);
                     }
                 } else {
-                    if (PAIR) ptx::tma_load_3d_pair(sb, &tmB, &full_bar[st], kc, b_row, bb);
-                    else if (p.b_batch_mid) ptx::tma_load_3d(sb, &tmB, &full_bar[st], kc, bb, b_row);
+                    if (PAIR) {
+                        if (p.b_batch_mid) ptx::tma_load_3d_pair(sb, &tmB, &full_bar[st], kc, bb, b_row);
+                        else ptx::tma_load_3d_pair(sb, &tmB, &full_bar[st], kc, b_row, bb);
+                    } else if (p.b_batch_mid) ptx::tma_load_3d(sb, &tmB, &full_bar[st], kc, bb, b_row);
                     else ptx::tma_load_3d(sb, &tmB, &full_bar[st], kc, b_row, bb);
                 }
+            };
+            // L2 prefetch of k-block kb (same boxes as the loads, no smem, no barrier)
+            auto pf_a = [&](int kb) {
+                const int32_t kc = kb * kBlockK;
+                if (p.a_batch_mid) ptx::tma_prefetch_3d(&tmA, kc, ab, a_row);
+                else ptx::tma_prefetch_3d(&tmA, kc, a_row, ab);
+            };
+            auto pf_b = [&](int kb) {
+                const int32_t kc = kb * kBlockK;
+                if (p.b_batch_mid) ptx::tma_prefetch_3d(&tmB, kc, bb, b_row);
+                else ptx::tma_prefetch_3d(&tmB, kc, b_row, bb);
             };
             int kb = kb0;
             if (first) {
@@ -395,6 +414,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (arms) ptx::mbar_arrive_expect_tx(&full_bar[s], tx);
                     if (p.a_static) load_a(s, kb0 + s);
                 }
+                const bool l2pf = p.l2pf && !B_MN && !devm;
+                if (l2pf && p.a_static)
+                    for (int q = kb0 + npre; q < kb1; ++q) pf_a(q);
                 ptx::pdl_wait();
                 if (devm_pending) {
                     devm_geometry(p, g, total_tiles, blockIdx.x == 0);
@@ -403,6 +425,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int s = 0; s < npre; ++s) {
                     if (!p.a_static) load_a(s, kb0 + s);
                     load_b(s, kb0 + s);
+                }
+                if (l2pf) {
+                    for (int q = kb0 + npre; q < kb1; ++q) {
+                        if (!p.a_static) pf_a(q);
+                        pf_b(q);
+                    }
                 }
                 kb = kb0 + npre;
                 stage = npre % p.stages;
@@ -873,6 +901,9 @@ cudaError_t launch_t(const UmmaLaunch &L, cudaLaunchConfig_t &cfg) {
     X(512, 1024, 4096) X(513, 1024, 4096) X(527, 1024, 4096) X(2048, 1024, 4096) X(2049, 1024, 4096)   \
     X(8192, 1024, 4096) X(128, 2304, 768) X(128, 768, 768) X(128, 3072, 768) X(128, 768, 3072)
 
+// bmm scores (trans_b = 0, fp32 out, alpha): (M, N, K) = (L, L, 64), heads at run time
+#define NIMBLE_STATIC_BMM_SHAPES(X) X(128, 128, 64) X(512, 512, 64) X(513, 513, 64) X(2048, 2048, 64) X(2049, 2049, 64)
+
 bool pdl_enabled() {
     static const bool on = [] {
         const char *e = std::getenv("NIMBLE_PDL");
@@ -896,9 +927,45 @@ size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out
     return 1024 /* alignment slack */ + (ring > part ? ring : part) + stg + kTailBytes;
 }
 
+// Co-resident groups of 4 CTA pairs for the fused-LayerNorm kernel (EPI 4) at this smem size:
+// the occupancy API's count of simultaneously active 2-CTA clusters, divided by 4.
+int umma_ln_max_groups(size_t smem_bytes) {
+    static size_t cached_smem = 0;
+    static int cached = -1;
+    if (cached >= 0 && cached_smem == smem_bytes) return cached;
+    auto fn = umma_gemm_kernel<0, 4, 0, 1, 1>;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit) != cudaSuccess) return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(148, 1, 1);        // one persistent CTA per SM (B200: 148 SMs)
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = 2;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cached_smem = smem_bytes;
+    cached = n / 4;
+    return cached;
+}
+
 bool umma_static_available(int64_t M, int64_t N, int64_t K) {
 #define NIMBLE_X(m, n, k) if (M == m && N == n && K == k) return true;
     NIMBLE_STATIC_GEMM_SHAPES(NIMBLE_X)
+#undef NIMBLE_X
+    return false;
+}
+
+bool umma_static_bmm_available(int64_t M, int64_t N, int64_t K) {
+#define NIMBLE_X(m, n, k) if (M == m && N == n && K == k) return true;
+    NIMBLE_STATIC_BMM_SHAPES(NIMBLE_X)
 #undef NIMBLE_X
     return false;
 }
@@ -930,6 +997,16 @@ cudaError_t launch_umma_gemm_static(const UmmaLaunch &L, int64_t M, int64_t N, i
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute attr[2];
     fill_cfg(L, cfg, attr);
+    if (L.out_f32) {                                 // bmm scores twin (alpha epilogue, fp32 out)
+#define NIMBLE_X(m, n, k) \
+    if (M == m && N == n && K == k) {                                                  \
+        if (L.pair) return launch_t<0, 0, 1, 1, 1, m, n, k>(L, cfg);                     \
+        return launch_t<0, 0, 1, 1, 0, m, n, k>(L, cfg);                                 \
+    }
+        NIMBLE_STATIC_BMM_SHAPES(NIMBLE_X)
+#undef NIMBLE_X
+        return cudaErrorInvalidValue;
+    }
 #define NIMBLE_X(m, n, k) \
     if (M == m && N == n && K == k) {                                                  \
         if (L.pair) return launch_t<0, 1, 0, 1, 1, m, n, k>(L, cfg);                     \

@@ -72,6 +72,8 @@ _SIGS = {
                             _vp],
     "nimble_bmm_dyn": [_vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
                        C.c_float, C.c_int, C.c_int, _vp],
+    "nimble_bmm_static": [_vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
+                          C.c_float, C.c_int, C.c_int, _vp],
     "nimble_softmax_rows": [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
     "nimble_layernorm": [_vp, _i64, _vp, _vp, C.c_float, _vp, _i64, _i64, _i64, _vp],
     "nimble_lstm_seq": [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp],
@@ -304,6 +306,19 @@ def bmm_dyn(A, lda, strideA, B, ldb, strideB, trans_b, Cout, ldc, strideC, batch
         out_dt = _dt(Cout)
     _check(_lib.nimble_bmm_dyn(a, lda, strideA, b, ldb, strideB, int(trans_b), c, ldc, strideC, batch, M, N, K,
                                float(alpha), BF16, out_dt, _stream(stream)))
+    return Cout
+
+
+def bmm_static(A, lda, strideA, B, ldb, strideB, trans_b, Cout, ldc, strideC, batch, M, N, K, alpha=1.0,
+               out_dt=None, stream=None):
+    """The static-shape twin of bmm_dyn (measurement baseline; compiled score shapes only)."""
+    a = A if isinstance(A, int) else _ptr(A)
+    b = B if isinstance(B, int) else _ptr(B)
+    c = Cout if isinstance(Cout, int) else _ptr(Cout)
+    if out_dt is None:
+        out_dt = _dt(Cout)
+    _check(_lib.nimble_bmm_static(a, lda, strideA, b, ldb, strideB, int(trans_b), c, ldc, strideC, batch, M, N, K,
+                                  float(alpha), BF16, out_dt, _stream(stream)))
     return Cout
 
 

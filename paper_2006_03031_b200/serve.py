@@ -122,27 +122,48 @@ def run_requests(cache: GraphCache, ids, lens, X_all: torch.Tensor, offsets, out
         cache.run(X_all[o:o + L], L, out[i])
 
 
+class ResultGather:
+    """The one collective of the request-sharded stream (§8(e)): every step, each rank's
+    (request id, [CLS]) rows are gathered to rank 0 into preallocated buffers, with no host
+    synchronisation (the ids are padded to max_count with -1; nothing is compacted on the
+    hot path).  `result()` — called once, after the timed region — drops the padding and
+    orders rank 0's rows by request id."""
+
+    def __init__(self, max_count: int, d: int, world: int, rank: int, device, dtype=torch.bfloat16):
+        self.world, self.rank, self.max_count = world, rank, max_count
+        self.ids_pad = torch.full((max_count,), -1, dtype=torch.int64, device=device)
+        self.cls_pad = torch.zeros((max_count, d), dtype=dtype, device=device)
+        if world > 1 and rank == 0:
+            self.all_ids = [torch.empty_like(self.ids_pad) for _ in range(world)]
+            self.all_cls = [torch.empty_like(self.cls_pad) for _ in range(world)]
+        else:
+            self.all_ids = [self.ids_pad] if world == 1 else None
+            self.all_cls = [self.cls_pad] if world == 1 else None
+
+    def step(self, ids_local: torch.Tensor, cls_local: torch.Tensor):
+        n = ids_local.shape[0]
+        if n:
+            self.ids_pad[:n].copy_(ids_local, non_blocking=True)
+            self.cls_pad[:n].copy_(cls_local, non_blocking=True)
+        if self.world > 1:
+            dist.gather(self.ids_pad, self.all_ids, dst=0)
+            dist.gather(self.cls_pad, self.all_cls, dst=0)
+
+    def result(self):
+        """(ids, cls) sorted by id on rank 0 (padding dropped); (None, None) elsewhere."""
+        if self.rank != 0:
+            return None, None
+        ids = torch.cat(self.all_ids)
+        cls = torch.cat(self.all_cls)
+        keep = ids >= 0
+        ids, cls = ids[keep], cls[keep]
+        order = torch.argsort(ids)
+        return ids[order], cls[order]
+
+
 def gather_results(ids_local: torch.Tensor, cls_local: torch.Tensor, max_count: int, world: int, rank: int):
-    """Gather (ids, [CLS]) from every rank to rank 0; returns (ids, cls) sorted by id on rank 0,
-    (None, None) elsewhere.  Shards are padded to max_count (id -1 marks padding)."""
-    d = cls_local.shape[1]
-    n = ids_local.shape[0]
-    ids_pad = torch.full((max_count,), -1, dtype=torch.int64, device=cls_local.device)
-    cls_pad = torch.zeros((max_count, d), dtype=cls_local.dtype, device=cls_local.device)
-    ids_pad[:n] = ids_local
-    cls_pad[:n] = cls_local
-    if world == 1:
-        all_ids, all_cls = [ids_pad], [cls_pad]
-    else:
-        all_ids = [torch.empty_like(ids_pad) for _ in range(world)] if rank == 0 else None
-        all_cls = [torch.empty_like(cls_pad) for _ in range(world)] if rank == 0 else None
-        dist.gather(ids_pad, all_ids, dst=0)
-        dist.gather(cls_pad, all_cls, dst=0)
-    if rank != 0:
-        return None, None
-    ids = torch.cat(all_ids)
-    cls = torch.cat(all_cls)
-    keep = ids >= 0
-    ids, cls = ids[keep], cls[keep]
-    order = torch.argsort(ids)
-    return ids[order], cls[order]
+    """One-shot form of ResultGather: gather (ids, [CLS]) from every rank to rank 0; returns
+    (ids, cls) sorted by id on rank 0, (None, None) elsewhere."""
+    g = ResultGather(max_count, cls_local.shape[1], world, rank, cls_local.device, cls_local.dtype)
+    g.step(ids_local, cls_local)
+    return g.result()

@@ -14,8 +14,18 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2006_03031_b200 import nimble as nb  # noqa: E402
 
-PEAK_TC = 1632.9e12
-PEAK_HBM = 6546.2e9
+def _peaks():
+    """Roofline denominators from the driver-written MEASURED_PEAKS.json (burst bf16, copy HBM)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    try:
+        with open(os.path.join(root, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk["bf16_tflops"] * 1e12, pk["hbm_gbs"] * 1e9
+    except Exception:                      # the profiling guide's fallback figures
+        return 1590e12, 6650e9
+
+
+PEAK_TC, PEAK_HBM = _peaks()
 
 
 def time_graph(fn, reps=20, iters=5):
@@ -66,6 +76,10 @@ def main():
     ap.add_argument("--shapes", default="large")
     ap.add_argument("--Ms", default="1,16,64,128,200,256,300,384,512,1024,2048,4096,8192")
     ap.add_argument("--out", default="gpurun_out/gemm_sweep.jsonl")
+    ap.add_argument("--hot", action="store_true", help="one weight copy (L2-resident weights)")
+    ap.add_argument("--tag", default="")
+    ap.add_argument("--residues", default="",
+                    help="M0 list: sweep M = M0 + delta for delta in 0,1,8,16,17,63,64,65,127 (SURVEY 8(d))")
     args = ap.parse_args()
     shapes = {"large": [(3072, 1024), (1024, 1024), (4096, 1024), (1024, 4096)],
               "base": [(2304, 768), (768, 768), (3072, 768), (768, 3072)]}[args.shapes]
@@ -73,9 +87,15 @@ def main():
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "a") as f:
         for (N, K), epi in zip(shapes, epis):
-            copies = max(2, int(2 * 126e6 / (N * K * 2)) + 1)
-            for M in [int(m) for m in args.Ms.split(",")]:
+            copies = 1 if args.hot else max(2, int(2 * 126e6 / (N * K * 2)) + 1)
+            Ms = [int(m) for m in args.Ms.split(",")]
+            if args.residues:
+                Ms = [m0 + dl for m0 in (int(v) for v in args.residues.split(","))
+                      for dl in (0, 1, 8, 16, 17, 63, 64, 65, 127)]
+            for M in Ms:
                 r = dense_point(M, N, K, epi, copies)
+                r["tag"] = args.tag
+                r["weights"] = "hot" if args.hot else "cold"
                 print(json.dumps(r), flush=True)
                 f.write(json.dumps(r) + "\n")
 

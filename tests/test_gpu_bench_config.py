@@ -12,6 +12,7 @@ import pytest
 import torch
 
 from paper_2006_03031_b200 import synth
+from parity import gate_bf16
 
 pytestmark = pytest.mark.gpu
 
@@ -58,7 +59,7 @@ def test_bench_config_layer_sampled(nb, orc):
     for i in sorted(pick):
         o, L = int(off_h[i]), int(lens[i])
         ref, D = orc.dense(rows(x, o, o + L), W["Wqkv"], W["bqkv"], None, 1)
-        assert np.max(np.abs(rows(enc.qkv, o, o + L) - ref) / D) <= 2e-2, ("qkv", i, L)
+        gate_bf16(rows(enc.qkv, o, o + L), ref, D, ("bench qkv", i, L))
         qkv = rows(enc.qkv, o, o + L)
         att = np.empty((L, d))
         for h in range(H):
@@ -66,10 +67,10 @@ def test_bench_config_layer_sampled(nb, orc):
             sc, _ = orc.bmm(q[None], k[None], 0, 0.125)
             c2, _ = orc.bmm(orc.softmax_rows(sc[0])[None], v[None], 1)
             att[:, 64 * h:64 * h + 64] = c2[0]
-        assert _err(enc.ctx[o:o + L], att) <= 2e-2, ("attention", i, L)
+        gate_bf16(enc.ctx[o:o + L], att, what=("bench attention", i, L))
         v1, _ = orc.dense(rows(enc.ctx, o, o + L), W["Wo"], W["bo"], rows(x, o, o + L), 3)
-        assert _err(enc.H1[o:o + L], orc.layernorm(v1, W["g1"], W["be1"])) <= 2e-2, ("o-proj+ln1", i, L)
+        gate_bf16(enc.H1[o:o + L], orc.layernorm(v1, W["g1"], W["be1"]), what=("bench o-proj+ln1", i, L))
         ref, D = orc.dense(rows(enc.H1, o, o + L), W["W1"], W["b1"], None, 2)
-        assert np.max(np.abs(rows(enc.F, o, o + L) - ref) / D) <= 2e-2, ("ffn1+gelu", i, L)
+        gate_bf16(rows(enc.F, o, o + L), ref, D, ("bench ffn1+gelu", i, L))
         v2, _ = orc.dense(rows(enc.F, o, o + L), W["W2"], W["b2"], rows(enc.H1, o, o + L), 3)
-        assert _err(out[o:o + L], orc.layernorm(v2, W["g2"], W["be2"])) <= 2e-2, ("ffn2+ln2 fused", i, L)
+        gate_bf16(out[o:o + L], orc.layernorm(v2, W["g2"], W["be2"]), what=("bench ffn2+ln2 fused", i, L))

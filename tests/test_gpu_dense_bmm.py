@@ -11,6 +11,7 @@ import pytest
 import torch
 
 from paper_2006_03031_b200 import synth
+from parity import gate, gate_bf16, gate_f32
 
 pytestmark = pytest.mark.gpu
 TOL_F32, TOL_BF16 = 1e-4, 2e-2
@@ -53,7 +54,7 @@ def test_config1_fp32_every_residue(nb, orc):
             res = synth.uniform((M, 128), -1, 1, 77 + M) if epi == nb.EPI_BIAS_RESIDUAL else None
             y = _dense_gpu(nb, x, W, b, epi, res)
             ref, D = orc.dense(x.numpy(), W.numpy(), b.numpy(), None if res is None else res.numpy(), epi)
-            assert _err(y, ref, D) <= TOL_F32, (M, epi)
+            gate_f32(y, ref, D, ("config1", M, epi))
             assert nb.last_dispatch() == orc.dispatch_dense(M, 128, 128, 0)[1]
 
 
@@ -84,7 +85,7 @@ def test_fp32_general_shapes(nb, orc):
         b = synth.normal((N,), 0.1, 13, torch.float32)
         y = _dense_gpu(nb, x, W, b, nb.EPI_BIAS)
         ref, D = orc.dense(x.numpy(), W.numpy(), b.numpy(), None, 1)
-        assert _err(y, ref, D) <= TOL_F32, (M, N, K)
+        gate_f32(y, ref, D, ("fp32", M, N, K))
 
 
 # ------------------------------------------------------------------ bf16 tcgen05 dense
@@ -103,8 +104,7 @@ def test_bf16_dense_vs_oracle(nb, orc, N, K):
             y = _dense_gpu(nb, x, W, b, epi, res)
             ref, D = orc.dense(x.double().numpy(), W.double().numpy(), b.numpy(),
                                None if res is None else res.double().numpy(), epi)
-            e = _err(y, ref, D)
-            assert e <= TOL_BF16, (N, K, M, epi, e)
+            gate_bf16(y, ref, D, ("bf16 dense", N, K, M, epi))
             assert nb.last_dispatch() == orc.dispatch_dense(M, N, K, 1)[1]
 
 
@@ -125,8 +125,7 @@ def test_bf16_tuned_schedule_vs_oracle(nb, orc, tile_t, split_max):
                 y = _dense_gpu(nb, x, W, b, epi, res)
                 ref, D = orc.dense(x.double().numpy(), W.double().numpy(), b.numpy(),
                                    None if res is None else res.double().numpy(), epi)
-                e = _err(y, ref, D)
-                assert e <= TOL_BF16, (tile_t, split_max, M, epi, e)
+                gate_bf16(y, ref, D, ("tuned", tile_t, split_max, M, epi))
                 assert nb.last_dispatch() == orc.dispatch_dense(M, N, K, 1, 0, tile_t, split_max)[1]
     finally:
         nb.set_dense_schedule(N, K, 0, 8)
@@ -159,7 +158,7 @@ def test_bf16_variant_limit_same_result(nb, orc):
                 assert nb.last_dispatch() == orc.dispatch_dense(M, N, K, 1, c)[1]
             finally:
                 nb.set_variant_limit(0)
-            assert _err(y, ref, D) <= TOL_BF16
+            gate_bf16(y, ref, D, ("variant limit", M, c))
             if base is None:
                 base = y
             assert torch.equal(y, base), (M, c)         # residue variants compute the same function
@@ -213,7 +212,7 @@ def test_bmm_scores_and_context_vs_oracle(nb, orc, L):
     v = qkv[:, 2 * d:].double().cpu().numpy().reshape(L, H, dh).transpose(1, 0, 2)
     ref, D = orc.bmm(q, k, 0, 0.125)
     Sg = S[:, :, :L].double().cpu().numpy()
-    assert np.max(np.abs(Sg - ref) / np.maximum(D, 1e-30)) <= TOL_BF16
+    gate(Sg, ref, D, TOL_BF16, ("bmm scores fp32 out", L))
     assert torch.all(S[:, :, 4 * ((L + 3) // 4):] == 7.0)     # TMA may fill the row's last 16-B segment
     # context: C_h = P_h V_h with V_h MN-major (trans_b = 1), P bf16 [H x L x ldP]
     ldP = 8 * ((L + 7) // 8)
@@ -226,7 +225,7 @@ def test_bmm_scores_and_context_vs_oracle(nb, orc, L):
     Pn = P[:, :, :L].double().cpu().numpy()
     refc, Dc = orc.bmm(Pn, v, 1, 1.0)
     cg = ctx.double().cpu().numpy().reshape(L, H, dh).transpose(1, 0, 2)
-    assert np.max(np.abs(cg - refc) / np.maximum(Dc, 1e-30)) <= TOL_BF16
+    gate_bf16(cg, refc, Dc, ("bmm context", L))
 
 
 def test_bmm_integer_exact(nb, orc):
@@ -288,7 +287,7 @@ def test_bf16_large_m_cta_pairs(nb, orc, M):
         assert d == orc.dispatch_dense(M, N, K, 1)[1] and d["cluster"] == (2, 1, 1)
         ref, D = orc.dense(x.double().numpy(), W.double().numpy(), b.numpy(),
                            None if res is None else res.double().numpy(), epi)
-        assert _err(y, ref, D) <= TOL_BF16, (M, epi)
+        gate_bf16(y, ref, D, ("family 3", M, epi))
     xi = synth.ternary((M, K), 95 + M, torch.bfloat16, max_nonzero_per_row=200)
     Wi = synth.ternary((N, K), 96, torch.bfloat16)
     bi = synth.ternary((N,), 97, torch.float32)
@@ -310,4 +309,4 @@ def test_bf16_partial_feature_boxes(nb, orc, M, N):
         y = _dense_gpu(nb, x, W, b, epi, res)
         ref, D = orc.dense(x.double().numpy(), W.double().numpy(), b.numpy(),
                            None if res is None else res.double().numpy(), epi)
-        assert _err(y, ref, D) <= TOL_BF16, (M, N, epi)
+        gate_bf16(y, ref, D, ("partial feature boxes", M, N, epi))

@@ -9,6 +9,7 @@ import pytest
 import torch
 
 from paper_2006_03031_b200 import synth
+from parity import gate_bf16
 
 pytestmark = pytest.mark.gpu
 
@@ -52,8 +53,7 @@ def test_dense_ln_vs_oracle(nb, orc, M, N, K):
     v, _ = orc.dense(d64(x[rows]), d64(W), d64(b), d64(res[rows]), 3)
     ref = orc.layernorm(v, d64(g), d64(be))
     got = d64(y[rows])
-    err = float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1.0)))
-    assert err <= 2e-2, (M, N, K, err)
+    gate_bf16(got, ref, what=("dense_ln", M, N, K))
 
 
 def test_dense_ln_fused_matches_two_launch_form(nb):
@@ -118,4 +118,4 @@ def test_layernorm_large_rows_vs_oracle(nb, orc, rows):
     idx = _rows(rows)
     ref = orc.layernorm(X[idx].double().cpu().numpy(), g.double().cpu().numpy(), be.double().cpu().numpy())
     got = Y[idx].double().cpu().numpy()
-    assert float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1.0))) <= 2e-2
+    gate_bf16(got, ref, what=("layernorm rows", rows))
