@@ -86,6 +86,27 @@ int encode_operand(CUtensorMap *m, const void *base, int64_t inner, int64_t rows
     return NIMBLE_OK;
 }
 
+// K-blocked operand view for two-k-block pipeline stages (batch 1, K % 64 == 0):
+// dims {64 (k within a block), rows, K / 64 (k-block)}, strides {ld, 64 elements};
+// box {64, box_rows, 2}: one TMA moves two consecutive swizzled 64-wide k-blocks.
+int encode_operand_kb(CUtensorMap *m, const void *base, int64_t K, int64_t rows, int64_t ld, int box_rows) {
+    cudaError_t e = get_encoder();
+    if (e != cudaSuccess) return cuda_fail("cuTensorMapEncodeTiled lookup", e);
+    cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(K / 64)};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 2, 128};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 2}, estr[3] = {1, 1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(NIMBLE_E_CUDA, "cuTensorMapEncodeTiled(k-blocked) failed (code " + std::to_string((int)r) + ")");
+    return NIMBLE_OK;
+}
+
+bool kblock2_enabled() {
+    static const bool on = [] { const char *e = std::getenv("NIMBLE_KD"); return !(e && e[0] == '1'); }();
+    return on;
+}
+
 // Output tile map for the transposed epilogue: out[b*bstride + j*ld + i], i < rows_i (inner),
 // j < rows_j; box {128 i, box_j j, 1}, no swizzle.  TMA clips the box at the tensor bounds, so
 // rows beyond the symbolic extent are never written.
@@ -133,21 +154,23 @@ void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
     L.p.trace = g_trace;
     static const int dbg = [] { const char *e = std::getenv("NIMBLE_DBG"); return e ? std::atoi(e) : 0; }();
     L.p.dbg = dbg;
+    if (L.p.kd < 1) L.p.kd = 1;
     const int kb_per_split = (L.p.kb_total + L.p.split - 1) / L.p.split;
+    const int st_per_split = (kb_per_split + L.p.kd - 1) / L.p.kd;        // pipeline stages of kd k-blocks
     const int ob = L.out_f32 ? 4 : 2;
     static const int max_st = [] { const char *e = std::getenv("NIMBLE_MAX_STAGES"); return e ? std::atoi(e) : 8; }();
-    int st = kb_per_split < max_st ? kb_per_split : max_st;     // NIMBLE_MAX_STAGES: experiment only
+    int st = st_per_split < max_st ? st_per_split : max_st;     // NIMBLE_MAX_STAGES: experiment only
     if (st < 1) st = 1;
     // largest depth that fits next to the epilogue staging
-    while (st > 1 && umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair, L.p.half_stg) >
-                         232448)
+    while (st > 1 && umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair, L.p.half_stg,
+                                     L.p.kd) > 232448)
         --st;
     L.p.stages = st;
-    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair, L.p.half_stg);
+    L.smem_bytes = umma_smem_bytes(L.p.box_n, L.b_mn_major, st, L.p.split, ob, L.transposed, L.pair, L.p.half_stg,
+                                   L.p.kd);
     L.p.tiles_m = L.pair ? (L.p.rows_a + 255) / 256 : d.grid[0];   // pairs own 256-row tiles
     L.p.tiles_n = d.grid[1];
     L.p.batch = d.grid[2] / d.split_k;
-    static const bool l2pf_on = [] { const char *e = std::getenv("NIMBLE_L2PF"); return !(e && e[0] == '0'); }();
     const int64_t tiles = (int64_t)L.p.tiles_m * L.p.tiles_n * L.p.batch;
     const int64_t slots = L.pair ? kNumSMs / 2 : kNumSMs;
     if (L.p.split > 1) {
@@ -155,7 +178,6 @@ void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
     } else {
         L.grid = dim3((unsigned)((tiles < slots ? tiles : slots) * (L.pair ? 2 : 1)), 1, 1);
     }
-    L.p.l2pf = (l2pf_on && tiles <= slots) ? 1 : 0;      // one wave: every CTA owns <= 1 tile
 }
 
 }  // namespace
@@ -329,8 +351,15 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     // the fused LayerNorm needs the whole tile in shared memory
     L.p.half_stg = (L.pair && !ln_fused && half_staging_enabled()) ? 1 : 0;
     const int out_box = L.p.half_stg ? L.p.box_n / 2 : L.p.box_n;
-    if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
-    if ((st = encode_operand(&L.tmB, x, K, M, ldx, 1, 0, box_b, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+    // two k-blocks per pipeline stage where the operands tile K exactly (every BERT shape)
+    L.p.kd = (kblock2_enabled() && K % 64 == 0 && K >= 128) ? 2 : 1;
+    if (L.p.kd == 2) {
+        if ((st = encode_operand_kb(&L.tmA, W, K, N, ldw, 128)) != NIMBLE_OK) return st;
+        if ((st = encode_operand_kb(&L.tmB, x, K, M, ldx, box_b)) != NIMBLE_OK) return st;
+    } else {
+        if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
+        if ((st = encode_operand(&L.tmB, x, K, M, ldx, 1, 0, box_b, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+    }
     if ((st = encode_out(&L.tmOut, y, false, N, M, ldy, 1, 0, out_box, &L.p.out_batch_mid)) != NIMBLE_OK) return st;
     if (epi == NIMBLE_EPI_BIAS_RESIDUAL) {
         int mid = 0;
@@ -485,8 +514,14 @@ extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, i
     L.p.m_dev = M_dev;
     L.p.var_c = variant_limit();
     L.p.rec = dispatch_dev;
-    if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
-    if ((st = encode_operand(&L.tmB, x, K, M_max, ldx, 1, 0, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+    L.p.kd = (kblock2_enabled() && K % 64 == 0 && K >= 128) ? 2 : 1;
+    if (L.p.kd == 2) {
+        if ((st = encode_operand_kb(&L.tmA, W, K, N, ldw, 128)) != NIMBLE_OK) return st;
+        if ((st = encode_operand_kb(&L.tmB, x, K, M_max, ldx, L.p.box_n)) != NIMBLE_OK) return st;
+    } else {
+        if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
+        if ((st = encode_operand(&L.tmB, x, K, M_max, ldx, 1, 0, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;
+    }
     if ((st = encode_out(&L.tmOut, y, false, N, M_max, ldy, 1, 0, L.p.box_n, &L.p.out_batch_mid)) != NIMBLE_OK) return st;
     if (epi == NIMBLE_EPI_BIAS_RESIDUAL) {
         int mid = 0;

@@ -57,10 +57,9 @@ struct UmmaParams {
     // half staging (2-CTA family, bf16, EPI <= 3): the epilogue stages and stores the tile in two
     // 128-token halves through a 32 KB buffer, which leaves room for a 6th pipeline stage
     int32_t half_stg;
-    // one-wave launches (every CTA owns at most one tile): prefetch the first tile's remaining
-    // k-blocks of both operands into L2 at kernel start (weights before the PDL wait), so the
-    // DRAM fetch of a cold weight slab runs at full parallelism instead of ring-depth bound
-    int32_t l2pf;
+    // k-blocks of 64 per pipeline stage: 2 where the operands are viewed as {64 k, rows, k-block}
+    // (batch 1, K % 64 == 0; tensor maps tmA / tmB encoded that way), else 1
+    int32_t kd;
 };
 
 struct UmmaLaunch {
@@ -79,7 +78,7 @@ bool umma_static_bmm_available(int64_t M, int64_t N, int64_t K);
 int umma_ln_max_groups(size_t smem_bytes);   // co-resident 4-pair groups for the fused-LN GEMM
 cudaError_t launch_umma_gemm_static(const UmmaLaunch &L, int64_t M, int64_t N, int64_t K);
 size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed, int pair,
-                       int half_stg = 0);
+                       int half_stg, int kd);
 // Programmatic dependent launch (griddepcontrol) on every libnimble launch that supports it.
 bool pdl_enabled();
 
@@ -100,7 +99,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
-int umma_max_stages(int box_n, int b_mn_major);
+int umma_max_stages(int box_n, int b_mn_major, int kd);
 
 // fp32 SIMT8 dense (family 0)
 struct Simt8Params {

@@ -272,8 +272,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // not generic ST/LD through the LSU).
     uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const bool split = p.split > 1;
-    const int b_bytes = b_stage_bytes(g.box_n, B_MN);
-    const int stage_bytes = kABytes + b_bytes;
+    const int kd = p.kd;                           // k-blocks of 64 per pipeline stage (1 or 2)
+    const int b_bytes = b_stage_bytes(g.box_n, B_MN);   // per k-block
+    const int stage_bytes = kd * (kABytes + b_bytes);
     const int ring_bytes = p.stages * stage_bytes;
     // PAIR: each CTA of the pair holds half of the B rows (box_n); output tiles are 2x box_n wide
     const int n_stage = PAIR ? 2 * g.box_n : g.box_n;
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (TRANS) ptx::prefetch_tmap(&tmOut);
         if (EPI == 3 && TRANS) ptx::prefetch_tmap(&tmRes);
         for (int s = 0; s < p.stages; ++s) {
-            ptx::mbar_init(&full_bar[s], 1);
+            ptx::mbar_init(&full_bar[s], 2);               // the A and the B producer warp each arrive once
             ptx::mbar_init(&empty_bar[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -344,22 +345,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::pdl_trigger();                            // the next kernel's prologue may start now
     if (threadIdx.x == 0) NIMBLE_TRACE(1);
 
-    if (warp == 0 && lane == 0) {
-        // ================= TMA producer
-        const uint32_t tx = (PAIR ? 2u : 1u) * (kABytes + b_bytes);    // PAIR: rank 0 expects both halves
+    if ((warp == 0 || warp == 3) && lane == 0) {
+        // ================= TMA producers: warp 0 streams A (weights), warp 3 streams B (tokens).
+        // One warp keeps only about one TMA stage in flight (measured: scripts/exp/tma_ingest.cu,
+        // ~1k clk per stage per issuing warp), so the two operands are issued from two warps and a
+        // stage covers kd = 2 k-blocks (64 KB for the 2-CTA tile) where the layout allows.
+        const bool isA = (warp == 0);
+        const uint32_t tx = (PAIR ? 2u : 1u) * (uint32_t)(kd * (isA ? kABytes : b_bytes));   // PAIR: rank 0 expects both halves
         const bool arms = !PAIR || prank == 0;                          // who arms the full barriers
         int stage = 0;
         uint32_t phase = 0;
-        bool first = true;
+        int nload = 0;                                    // stages issued by this warp
         int nkb_p = 0;                                    // debug: k-blocks issued (NIMBLE_DBG & 4)
-        // devm: the first tile (t_first < tiles_m) exists for every M >= 1, so its weights can
-        // still be requested before the wait; otherwise wait and read M first.
-        bool devm_pending = devm;
-        if (devm && !(p.a_static && t_first < g.tiles_m)) {
-            ptx::pdl_wait();
-            devm_geometry(p, g, total_tiles, blockIdx.x == 0);
-            devm_pending = false;
-        }
+        // the weights (A, static) may be requested before the grid-dependency wait; tokens (B) and
+        // a non-static A after it.  devm: the first tile (t_first < tiles_m) exists for every
+        // M >= 1, so its weights can still be requested before M is read.
+        bool waited = false;
+        auto ensure_wait = [&]() {
+            if (!waited) {
+                ptx::pdl_wait();
+                if (devm) devm_geometry(p, g, total_tiles, isA && blockIdx.x == 0);
+                waited = true;
+            }
+        };
+        if (!isA || !p.a_static || (devm && t_first >= g.tiles_m)) ensure_wait();
         for (int t = t_first; t < total_tiles; t += t_step) {
             const TileCoord c = tile_of(g, t);
             const int n_this_p = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
@@ -367,85 +376,46 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int32_t b_row = c.n * g.n_full + (PAIR ? (int)prank * (n_this_p / 2) : 0);
             const int32_t ab = p.a_bcast ? 0 : c.b;
             const int32_t bb = p.b_bcast ? 0 : c.b;
-            auto load_a = [&](int st, int kb) {
-                uint8_t *sa = smem + st * stage_bytes;
-                const int32_t kc = kb * kBlockK;
-                // heads interleaved inside a row (QKV views): batch is the middle tensor-map dim
-                if (PAIR) {
-                    if (p.a_batch_mid) ptx::tma_load_3d_pair(sa, &tmA, &full_bar[st], kc, ab, a_row);
-                    else ptx::tma_load_3d_pair(sa, &tmA, &full_bar[st], kc, a_row, ab);
-                } else if (p.a_batch_mid) ptx::tma_load_3d(sa, &tmA, &full_bar[st], kc, ab, a_row);
-                else ptx::tma_load_3d(sa, &tmA, &full_bar[st], kc, a_row, ab);
-            };
-            auto load_b = [&](int st, int kb) {
-                uint8_t *sb = smem + st * stage_bytes + kABytes;
-                const int32_t kc = kb * kBlockK;
-                if (B_MN) {
-                    const int chunks = (g.box_n + 63) / 64;
-                    for (int q = 0; q < chunks; ++q) {
-                        if (p.b_batch_mid) ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[st], b_row + 64 * q, bb, kc);
-                        else ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[st], b_row + 64 * q, kc, bb);
-                    }
-                } else {
-                    if (PAIR) {
-                        if (p.b_batch_mid) ptx::tma_load_3d_pair(sb, &tmB, &full_bar[st], kc, bb, b_row);
-                        else ptx::tma_load_3d_pair(sb, &tmB, &full_bar[st], kc, b_row, bb);
-                    } else if (p.b_batch_mid) ptx::tma_load_3d(sb, &tmB, &full_bar[st], kc, bb, b_row);
-                    else ptx::tma_load_3d(sb, &tmB, &full_bar[st], kc, b_row, bb);
+            for (int kb = kb0; kb < kb1; kb += kd) {
+                if (nload >= p.stages) {
+                    ensure_wait();          // a ring's worth of early weights at most, then the dependencies
+                    ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
                 }
-            };
-            // L2 prefetch of k-block kb (same boxes as the loads, no smem, no barrier)
-            auto pf_a = [&](int kb) {
-                const int32_t kc = kb * kBlockK;
-                if (p.a_batch_mid) ptx::tma_prefetch_3d(&tmA, kc, ab, a_row);
-                else ptx::tma_prefetch_3d(&tmA, kc, a_row, ab);
-            };
-            auto pf_b = [&](int kb) {
-                const int32_t kc = kb * kBlockK;
-                if (p.b_batch_mid) ptx::tma_prefetch_3d(&tmB, kc, bb, b_row);
-                else ptx::tma_prefetch_3d(&tmB, kc, b_row, bb);
-            };
-            int kb = kb0;
-            if (first) {
-                // ring is empty: the first `stages` blocks need no empty-wait; static weights
-                // are requested before the grid-dependency wait
-                const int npre = min(p.stages, kb1 - kb0);
-                for (int s = 0; s < npre; ++s) {
-                    if (arms) ptx::mbar_arrive_expect_tx(&full_bar[s], tx);
-                    if (p.a_static) load_a(s, kb0 + s);
-                }
-                const bool l2pf = p.l2pf && !B_MN && !devm;
-                if (l2pf && p.a_static)
-                    for (int q = kb0 + npre; q < kb1; ++q) pf_a(q);
-                ptx::pdl_wait();
-                if (devm_pending) {
-                    devm_geometry(p, g, total_tiles, blockIdx.x == 0);
-                    devm_pending = false;
-                }
-                for (int s = 0; s < npre; ++s) {
-                    if (!p.a_static) load_a(s, kb0 + s);
-                    load_b(s, kb0 + s);
-                }
-                if (l2pf) {
-                    for (int q = kb0 + npre; q < kb1; ++q) {
-                        if (!p.a_static) pf_a(q);
-                        pf_b(q);
-                    }
-                }
-                kb = kb0 + npre;
-                stage = npre % p.stages;
-                phase = (npre == p.stages) ? 1u : 0u;
-                first = false;
-            }
-            for (; kb < kb1; ++kb) {
-                ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-                if ((p.dbg & 4) && trace && cta_lin == 0 && nkb_p < 4096) p.trace[16384 + nkb_p] = clock64();
+                if (isA && (p.dbg & 4) && trace && cta_lin == 0 && nkb_p < 4096) p.trace[16384 + nkb_p] = clock64();
                 ++nkb_p;
                 if (arms) ptx::mbar_arrive_expect_tx(&full_bar[stage], tx);
-                load_a(stage, kb);
-                load_b(stage, kb);
+                const int32_t kc = kb * kBlockK;
+                uint8_t *sa = smem + stage * stage_bytes;
+                if (isA) {
+                    if (kd == 2) {          // {64 k, rows, k-block} view: two 16 KB swizzled blocks
+                        if (PAIR) ptx::tma_load_3d_pair(sa, &tmA, &full_bar[stage], 0, a_row, kb);
+                        else ptx::tma_load_3d(sa, &tmA, &full_bar[stage], 0, a_row, kb);
+                    } else if (PAIR) {      // heads interleaved inside a row (QKV views): batch mid
+                        if (p.a_batch_mid) ptx::tma_load_3d_pair(sa, &tmA, &full_bar[stage], kc, ab, a_row);
+                        else ptx::tma_load_3d_pair(sa, &tmA, &full_bar[stage], kc, a_row, ab);
+                    } else if (p.a_batch_mid) ptx::tma_load_3d(sa, &tmA, &full_bar[stage], kc, ab, a_row);
+                    else ptx::tma_load_3d(sa, &tmA, &full_bar[stage], kc, a_row, ab);
+                } else {
+                    uint8_t *sb = sa + kd * kABytes;
+                    if (B_MN) {
+                        const int chunks = (g.box_n + 63) / 64;
+                        for (int q = 0; q < chunks; ++q) {
+                            if (p.b_batch_mid) ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[stage], b_row + 64 * q, bb, kc);
+                            else ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[stage], b_row + 64 * q, kc, bb);
+                        }
+                    } else if (kd == 2) {
+                        if (PAIR) ptx::tma_load_3d_pair(sb, &tmB, &full_bar[stage], 0, b_row, kb);
+                        else ptx::tma_load_3d(sb, &tmB, &full_bar[stage], 0, b_row, kb);
+                    } else if (PAIR) {
+                        if (p.b_batch_mid) ptx::tma_load_3d_pair(sb, &tmB, &full_bar[stage], kc, bb, b_row);
+                        else ptx::tma_load_3d_pair(sb, &tmB, &full_bar[stage], kc, b_row, bb);
+                    } else if (p.b_batch_mid) ptx::tma_load_3d(sb, &tmB, &full_bar[stage], kc, bb, b_row);
+                    else ptx::tma_load_3d(sb, &tmB, &full_bar[stage], kc, b_row, bb);
+                }
+                ++nload;
                 if (++stage == p.stages) { stage = 0; phase ^= 1; }
             }
+            ensure_wait();                  // total_tiles (devm) is final before the next tile test
         }
     } else if (warp == 1 && lane == 0 && (!PAIR || prank == 0)) {
         // ================= MMA issuer (single thread; the even CTA of a pair issues for both)
@@ -467,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++ntile_m;
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)(acc * g.n_full);
-            for (int kb = kb0; kb < kb1; ++kb) {
+            for (int kb = kb0; kb < kb1; kb += kd) {
                 ptx::mbar_wait(&full_bar[stage], phase);
                 if ((p.dbg & 4) && trace && cta_lin == 0 && nkb_m < 4096) {
                     p.trace[8192 + nkb_m] = clock64();
@@ -478,18 +448,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ++nkb_m;
                 ptx::tc_fence_after();
                 if (kb == kb0 && t == t_first) NIMBLE_TRACE(2);
-                const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
-                const uint32_t sb = sa + kABytes;
-                const uint64_t adesc = ptx::smem_desc_sw128(sa, 0, 1024);
-                // K-major B: 8-row groups 1024 B apart.  MN-major B: 64-column chunks 8 KiB
-                // apart (LBO), 8-row k groups 1024 B apart (SBO).
-                const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb, 8192, 1024) : ptx::smem_desc_sw128(sb, 0, 1024);
+                const uint32_t sa0 = ptx::smem_u32(smem + stage * stage_bytes);
+                const int nkb = min(kd, kb1 - kb);        // a partial last stage: its 2nd block is not ours
+                for (int j = 0; j < nkb; ++j) {
+                    const uint32_t sa = sa0 + (uint32_t)(j * kABytes);
+                    const uint32_t sb = sa0 + (uint32_t)(kd * kABytes + j * b_bytes);
+                    const uint64_t adesc = ptx::smem_desc_sw128(sa, 0, 1024);
+                    // K-major B: 8-row groups 1024 B apart.  MN-major B: 64-column chunks 8 KiB
+                    // apart (LBO), 8-row k groups 1024 B apart (SBO).
+                    const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb, 8192, 1024) : ptx::smem_desc_sw128(sb, 0, 1024);
 #pragma unroll
-                for (int kk = 0; kk < kBlockK / 16; ++kk) {
-                    const uint64_t a_k = adesc + (uint64_t)((kk * 32) >> 4);            // +32 B along K
-                    const uint64_t b_k = bdesc + (uint64_t)(B_MN ? ((kk * 2048) >> 4) : ((kk * 32) >> 4));
-                    if (PAIR) ptx::umma_bf16_pair(d_tmem, a_k, b_k, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
-                    else ptx::umma_bf16(d_tmem, a_k, b_k, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < kBlockK / 16; ++kk) {
+                        const uint64_t a_k = adesc + (uint64_t)((kk * 32) >> 4);            // +32 B along K
+                        const uint64_t b_k = bdesc + (uint64_t)(B_MN ? ((kk * 2048) >> 4) : ((kk * 32) >> 4));
+                        const uint32_t accum = (kb > kb0 || j > 0 || kk > 0) ? 1u : 0u;
+                        if (PAIR) ptx::umma_bf16_pair(d_tmem, a_k, b_k, idesc, accum);
+                        else ptx::umma_bf16(d_tmem, a_k, b_k, idesc, accum);
+                    }
                 }
                 if (PAIR) ptx::umma_commit_pair(&empty_bar[stage], 0x3);   // frees the stage in both CTAs
                 else ptx::umma_commit(&empty_bar[stage]);    // smem stage free once these MMAs retire
@@ -912,14 +887,14 @@ bool pdl_enabled() {
     return on;
 }
 
-int umma_max_stages(int box_n, int b_mn_major) {
-    const int stage = kABytes + b_stage_bytes(box_n, b_mn_major);
+int umma_max_stages(int box_n, int b_mn_major, int kd) {
+    const int stage = kd * (kABytes + b_stage_bytes(box_n, b_mn_major));
     return (kSmemLimit - 1024 - kTailBytes) / stage;
 }
 
 size_t umma_smem_bytes(int box_n, int b_mn_major, int stages, int split, int out_bytes, int transposed, int pair,
-                       int half_stg) {
-    const size_t ring = (size_t)stages * (kABytes + b_stage_bytes(box_n, b_mn_major));
+                       int half_stg, int kd) {
+    const size_t ring = (size_t)stages * kd * (kABytes + b_stage_bytes(box_n, b_mn_major));
     const int n_stage = pair ? 2 * box_n : box_n;
     const size_t part = split > 1 ? (size_t)128 * n_stage * 4 : 0;
     const size_t stg = split > 1 ? (size_t)128 * n_stage * 4
