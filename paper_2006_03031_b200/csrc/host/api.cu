@@ -170,13 +170,14 @@ void plan_pipeline(UmmaLaunch &L, const nimble_dispatch &d) {
                                    L.p.kd);
     L.p.tiles_m = L.pair ? (L.p.rows_a + 255) / 256 : d.grid[0];   // pairs own 256-row tiles
     L.p.tiles_n = d.grid[1];
-    L.p.batch = d.grid[2] / d.split_k;
+    L.p.batch = d.grid[2] / d.cluster[2];   // grid[2] = batch x cluster split-K
     const int64_t tiles = (int64_t)L.p.tiles_m * L.p.tiles_n * L.p.batch;
     const int64_t slots = L.pair ? kNumSMs / 2 : kNumSMs;
     if (L.p.split > 1) {
         L.grid = dim3(d.grid[0], d.grid[1], d.grid[2]);
     } else {
-        L.grid = dim3((unsigned)((tiles < slots ? tiles : slots) * (L.pair ? 2 : 1)), 1, 1);
+        const int64_t used = tiles < slots ? tiles : slots;
+        L.grid = dim3((unsigned)(used * (L.pair ? 2 : 1)), 1, 1);
     }
 }
 
@@ -322,7 +323,7 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     L.p.n_tail = d.r ? d.umma_n_tail : d.umma_n_full;
     L.p.box_n = (d.grid[1] == 1) ? L.p.n_tail : d.umma_n_full;
     L.p.kb_total = (int32_t)((K + 63) / 64);
-    L.p.split = d.split_k;
+    L.p.split = d.cluster[2];            // cluster split-K (1: none; a stream-K tail is planned separately)
     L.epi = epi;
     L.out_f32 = 0;
     L.transposed = 1;
@@ -347,9 +348,9 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
         ln_fused = fused_ln_enabled() && L.pair && N == 1024 && K >= min_k && epi == NIMBLE_EPI_BIAS_RESIDUAL &&
                    !static_twin;
     }
-    // the 2-CTA family stages its bf16 output in 128-token halves (a 6th pipeline stage fits);
-    // the fused LayerNorm needs the whole tile in shared memory
-    L.p.half_stg = (L.pair && !ln_fused && half_staging_enabled()) ? 1 : 0;
+    // the 2-CTA family stages its bf16 output in 128-token halves (a third 64 KB pipeline stage
+    // fits); the fused LayerNorm then normalises each half (tokens are independent rows)
+    L.p.half_stg = (L.pair && half_staging_enabled()) ? 1 : 0;
     const int out_box = L.p.half_stg ? L.p.box_n / 2 : L.p.box_n;
     // two k-blocks per pipeline stage where the operands tile K exactly (every BERT shape)
     L.p.kd = (kblock2_enabled() && K % 64 == 0 && K >= 128) ? 2 : 1;
@@ -501,7 +502,7 @@ extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, i
     L.p.n_tail = d.r ? d.umma_n_tail : d.umma_n_full;
     L.p.box_n = d.umma_n_full;                         // fixed box: the tail width is decided on device
     L.p.kb_total = (int32_t)((K + 63) / 64);
-    L.p.split = d.split_k;
+    L.p.split = d.cluster[2];            // cluster split-K (1: none; a stream-K tail is planned separately)
     L.epi = epi;
     L.transposed = 1;
     L.p.alpha = 1.f;
@@ -566,7 +567,7 @@ static int bmm_impl(const void *A, int64_t lda, int64_t strideA, const void *B, 
     UmmaLaunch L;
     std::memset(&L, 0, sizeof(L));
     L.p.kb_total = (int32_t)((K + 63) / 64);
-    L.p.split = d.split_k;
+    L.p.split = d.cluster[2];            // cluster split-K (1: none; a stream-K tail is planned separately)
     L.epi = 0;
     L.out_f32 = out_dt == NIMBLE_F32;
     L.p.alpha = alpha;

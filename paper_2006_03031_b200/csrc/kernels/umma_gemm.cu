@@ -89,6 +89,18 @@ __device__ __forceinline__ TileCoord tile_of(const Geo &g, int t) {
     return c;
 }
 
+// A CTA's i-th work item: a tile and its k-block range (persistent slot `slot` of `nslots` takes
+// tiles slot, slot + nslots, ...; a split-K cluster CTA takes its one tile and K slice).
+struct WorkItem {
+    int t, kb_lo, kb_hi;
+};
+__device__ __forceinline__ bool work_item(int i, int slot, int nslots, int total, int kb0, int kb1, WorkItem &w) {
+    w.t = slot + i * nslots;
+    w.kb_lo = kb0;
+    w.kb_hi = kb1;
+    return w.t < total;
+}
+
 // Device-side residue dispatch for nimble_dense_dyn_dev (DISPATCH.md family 1, the
 // upper-bound form of P:268-271): M is data read after the grid-dependency wait, the rule is
 // the host's, so the recorded dispatch is bit-identical to the oracle's.  The split-K factor
@@ -170,6 +182,7 @@ __device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
 __device__ __forceinline__ void ln_tile(const UmmaParams &p, uint8_t *stg, int n_stage, int n_this, int prank,
                                         int fquarter, int iter, const float (&gm)[16], const float (&bt)[16], int e,
                                         bool leader) {
+    const int kmax = (n_stage + 31) / 32;          // token rows held by the staging (256, or 128 when half-staged)
     const int cc = e & 7, jt = e >> 3;
     const int grp = (int)(blockIdx.x / 2) / 4;
     const int slot = 2 * grp + (iter & 1);
@@ -179,6 +192,7 @@ __device__ __forceinline__ void ln_tile(const UmmaParams &p, uint8_t *stg, int n
     // 1. partial sums
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
+        if (k >= kmax) break;
         const int j = jt + 32 * k;
         float s1 = 0.f, s2 = 0.f;
         if (j < n_this) {
@@ -214,10 +228,12 @@ __device__ __forceinline__ void ln_tile(const UmmaParams &p, uint8_t *stg, int n
             if (++spins == (1u << 26)) __trap();
         }
     }
+    __syncwarp();
     ptx::named_bar_sync(1, kEpiThreads);
     // 3. statistics and normalisation
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
+        if (k >= kmax) break;
         const int j = jt + 32 * k;
         float2 pr = __ldcg(st + cc * 256 + j);                     // lane cc fetches partial cc
 #pragma unroll
@@ -263,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
                      const UmmaParams p) {
     using OutT = typename std::conditional<OUT_F32, float, __nv_bfloat16>::type;
-    constexpr bool HALF_OK = PAIR && !OUT_F32 && EPI <= 3 && !B_MN;   // half staging supported
+    constexpr bool HALF_OK = PAIR && !OUT_F32 && !B_MN;   // half staging supported (EPI 4: LayerNorm per half)
     Geo g = make_geo<SM, SN, SK, PAIR>(p);
     const bool devm = p.m_dev != nullptr;          // extent on the device (dense_dyn_dev)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -309,6 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int split_q = split ? (int)(blockIdx.z % p.split) : 0;
     const int kb0 = (int)((int64_t)split_q * g.kb_total / p.split);
     const int kb1 = (int)((int64_t)(split_q + 1) * g.kb_total / p.split);
+    // the work items of this CTA (t_first / t_step: its slot and the slot count)
+#define NIMBLE_ITEMS(w, i) for (int i = 0; work_item(i, t_first, t_step, total_tiles, kb0, kb1, w); ++i)
     const uint32_t tmem_cols = split ? pow2_cols(g.box_n) : pow2_cols(2 * g.n_full);
     const int cta_lin = ((int)blockIdx.z * gridDim.y + (int)blockIdx.y) * gridDim.x + (int)blockIdx.x;
     unsigned long long *trace = p.trace ? p.trace + (size_t)cta_lin * 8 : nullptr;
@@ -369,14 +387,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         };
         if (!isA || !p.a_static || (devm && t_first >= g.tiles_m)) ensure_wait();
-        for (int t = t_first; t < total_tiles; t += t_step) {
-            const TileCoord c = tile_of(g, t);
+        WorkItem w;
+        NIMBLE_ITEMS(w, it) {
+            const TileCoord c = tile_of(g, w.t);
             const int n_this_p = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
             const int32_t a_row = c.m * kRowsPerTile + (int)prank * 128;
             const int32_t b_row = c.n * g.n_full + (PAIR ? (int)prank * (n_this_p / 2) : 0);
             const int32_t ab = p.a_bcast ? 0 : c.b;
             const int32_t bb = p.b_bcast ? 0 : c.b;
-            for (int kb = kb0; kb < kb1; kb += kd) {
+            for (int kb = w.kb_lo; kb < w.kb_hi; kb += kd) {
                 if (nload >= p.stages) {
                     ensure_wait();          // a ring's worth of early weights at most, then the dependencies
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -428,7 +447,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         int nkb_m = 0, ntile_m = 0;                       // debug: k-blocks / tiles consumed (NIMBLE_DBG & 4)
-        for (int t = t_first; t < total_tiles; t += t_step) {
+        WorkItem w;
+        NIMBLE_ITEMS(w, it) {
+            const int t = w.t;
             const TileCoord c = tile_of(g, t);
             const int n_this = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
             const uint32_t idesc = ptx::idesc_bf16(PAIR ? 256u : 128u, (uint32_t)n_this, B_MN);
@@ -437,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++ntile_m;
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)(acc * g.n_full);
-            for (int kb = kb0; kb < kb1; kb += kd) {
+            for (int kb = w.kb_lo; kb < w.kb_hi; kb += kd) {
                 ptx::mbar_wait(&full_bar[stage], phase);
                 if ((p.dbg & 4) && trace && cta_lin == 0 && nkb_m < 4096) {
                     p.trace[8192 + nkb_m] = clock64();
@@ -447,9 +468,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ++nkb_m;
                 ptx::tc_fence_after();
-                if (kb == kb0 && t == t_first) NIMBLE_TRACE(2);
+                if (kb == w.kb_lo && it == 0) NIMBLE_TRACE(2);
                 const uint32_t sa0 = ptx::smem_u32(smem + stage * stage_bytes);
-                const int nkb = min(kd, kb1 - kb);        // a partial last stage: its 2nd block is not ours
+                const int nkb = min(kd, w.kb_hi - kb);    // a partial last stage: its 2nd block is not ours
                 for (int j = 0; j < nkb; ++j) {
                     const uint32_t sa = sa0 + (uint32_t)(j * kABytes);
                     const uint32_t sb = sa0 + (uint32_t)(kd * kABytes + j * b_bytes);
@@ -461,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kk = 0; kk < kBlockK / 16; ++kk) {
                         const uint64_t a_k = adesc + (uint64_t)((kk * 32) >> 4);            // +32 B along K
                         const uint64_t b_k = bdesc + (uint64_t)(B_MN ? ((kk * 2048) >> 4) : ((kk * 32) >> 4));
-                        const uint32_t accum = (kb > kb0 || j > 0 || kk > 0) ? 1u : 0u;
+                        const uint32_t accum = (kb > w.kb_lo || j > 0 || kk > 0) ? 1u : 0u;
                         if (PAIR) ptx::umma_bf16_pair(d_tmem, a_k, b_k, idesc, accum);
                         else ptx::umma_bf16(d_tmem, a_k, b_k, idesc, accum);
                     }
@@ -493,8 +514,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const CUtensorMap *om = &tmOut;
         if (TRANS && devm && ew == 0 && t_first < total_tiles)
             om = ptx::tmap_patch_extent<1>(&tmOut, smap, p.out_slot + blockIdx.x, (uint32_t)g.rows_b, lane);
-        if ((EPI == 3 || EPI == 4) && TRANS && !split && leader && t_first < total_tiles) {
-            const TileCoord c = tile_of(g, t_first);
+        WorkItem w0;
+        const bool has0 = work_item(0, t_first, t_step, total_tiles, kb0, kb1, w0);
+        if ((EPI == 3 || EPI == 4) && TRANS && !split && leader && has0) {
+            const TileCoord c = tile_of(g, w0.t);
             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
             for (int sb = 0; sb < 2; ++sb)             // two swizzled [tokens][64 features] boxes
                 ptx::tma_load_3d(stg + sb * stg_tok * 128, &tmRes, res_bar, c.m * kRowsPerTile + row_base + 64 * sb,
@@ -515,7 +538,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ln_b[8 * h2 + e] = t_first < total_tiles ? __ldg(p.ln_beta + f0 + 64 * h2 + e) : 0.f;
                 }
         }
-        for (int t = t_first; t < total_tiles; t += t_step) {
+        WorkItem w;
+        NIMBLE_ITEMS(w, it) {
+            const int t = w.t;
+            WorkItem wn;                                     // the next item (residual prefetch)
+            const bool has_next = work_item(it + 1, t_first, t_step, total_tiles, kb0, kb1, wn);
             const TileCoord c = tile_of(g, t);
             const int n_this = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
             const int i = c.m * kRowsPerTile + row_base + row_local;
@@ -531,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
-            if (leader && t == t_first) NIMBLE_TRACE(3);
+            if (leader && it == 0) NIMBLE_TRACE(3);
             const bool ktr = (p.dbg & 4) && trace && cta_lin == 0 && leader && ep_tile < 512;
             if (ktr) p.trace[32768 + ep_tile * 4 + 0] = clock64();   // accumulator ready
             const uint32_t tmem_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * g.n_full);
@@ -553,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int nh = (n_this + stg_tok - 1) / stg_tok;
                     for (int hh = 0; hh < nh; ++hh) {
                         const int col0 = hh * stg_tok, col1 = min(n_this, col0 + stg_tok);
-                        if (EPI == 3) {
+                        if (EPI == 3 || EPI == 4) {
                             ptx::mbar_wait(res_bar, res_phase);
                             res_phase ^= 1;
                         }
@@ -573,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     x[m] = make_float2(__uint_as_float(r[(m & 1) * 2 + (m >> 1) * 4]),
                                                        __uint_as_float(r[(m & 1) * 2 + (m >> 1) * 4 + 1]));
                                 float2 rs[4];
-                                if constexpr (EPI == 3) {
+                                if constexpr (EPI == 3 || EPI == 4) {
                                     uint32_t q0, q1, q2, q3;
                                     ldmatrix_x4_trans(a_me, q0, q1, q2, q3);
                                     rs[0] = unpack_bf16(q0); rs[1] = unpack_bf16(q1);
@@ -587,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     if constexpr (EPI == 0) y2 = ptx::fmul2(x[m], ptx::f2(p.alpha));
                                     else if constexpr (EPI == 2) y2 = ptx::gelu_erf2(ptx::fadd2(x[m], ptx::f2(bb)));
                                     else y2 = ptx::fadd2(x[m], ptx::f2(bb));
-                                    if constexpr (EPI == 3) y2 = ptx::fadd2(y2, rs[m]);
+                                    if constexpr (EPI == 3 || EPI == 4) y2 = ptx::fadd2(y2, rs[m]);
                                     o[m] = pack_bf16(y2.x, y2.y);
                                 }
                                 stmatrix_x4_trans(a_me, o[0], o[1], o[2], o[3]);
@@ -599,6 +626,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (ktr) p.trace[32768 + ep_tile * 4 + 1] = clock64();
                             if (lane == 0) ptx::mbar_arrive_cluster(ptx::map_shared_rank(ptx::smem_u32(&tempty[acc]), 0));
                         }
+                        if constexpr (EPI == 4) {                 // this half's 128 tokens: LayerNorm across the group
+                            ptx::named_bar_sync(1, kEpiThreads);      // pre-LN half complete in staging
+                            ln_tile(p, reinterpret_cast<uint8_t *>(stg), stg_tok, col1 - col0, (int)prank, c.m, ln_iter,
+                                    ln_g, ln_b, (int)(threadIdx.x - 32 * kEpiWarp0), leader);
+                            ++ln_iter;
+                        }
                         ptx::fence_async_smem();
                         ptx::named_bar_sync(1, kEpiThreads);
                         if (leader && !(p.dbg & 16)) {
@@ -606,15 +639,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ptx::tma_store_3d(om, stg + sb * stg_tok * 128, c.m * kRowsPerTile + row_base + 64 * sb,
                                                   j0 + col0, c.b);
                             ptx::tma_store_commit_wait();             // staging readable again
-                            if (EPI == 3) {                           // next residual half
-                                const int tn = t + t_step;
+                            if (EPI == 3 || EPI == 4) {               // next residual half
                                 if (hh + 1 < nh) {
                                     ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
                                     for (int sb = 0; sb < 2; ++sb)
                                         ptx::tma_load_3d(stg + sb * stg_tok * 128, &tmRes, res_bar,
                                                          c.m * kRowsPerTile + row_base + 64 * sb, j0 + col1, c.b);
-                                } else if (tn < total_tiles) {
-                                    const TileCoord cn = tile_of(g, tn);
+                                } else if (has_next) {
+                                    const TileCoord cn = tile_of(g, wn.t);
                                     ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
                                     for (int sb = 0; sb < 2; ++sb)
                                         ptx::tma_load_3d(stg + sb * stg_tok * 128, &tmRes, res_bar,
@@ -743,9 +775,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         ptx::tma_store_commit_wait();                 // staging readable again
                         if (ktr) p.trace[32768 + ep_tile * 4 + 2] = clock64();   // store drained
-                        const int tn = t + t_step;
-                        if ((EPI == 3 || EPI == 4) && tn < total_tiles) {
-                            const TileCoord cn = tile_of(g, tn);
+                        if ((EPI == 3 || EPI == 4) && has_next) {
+                            const TileCoord cn = tile_of(g, wn.t);
                             ptx::mbar_arrive_expect_tx(res_bar, res_bytes);
                             for (int sb = 0; sb < 2; ++sb)
                                 ptx::tma_load_3d(stg + sb * n_stage * 128, &tmRes, res_bar,

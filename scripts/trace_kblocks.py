@@ -34,11 +34,12 @@ for shp in (sys.argv[1] if len(sys.argv) > 1 else "17448x3072x1024,17448x1024x40
     tiles = t[24576:24576 + 256]
     tiles = tiles[tiles > 0]
     d = nb.last_dispatch()
-    kb = (K + 63) // 64
+    kd = 2 if (K % 64 == 0 and K >= 128 and os.environ.get("NIMBLE_KD") != "1") else 1
+    kb = ((K + 63) // 64 + kd - 1) // kd                 # pipeline stages per tile (kd k-blocks each)
     df = np.diff(full)
-    print(f"{shp}: family {d['family']} t={d['tile_t']} k-blocks/tile={kb}; CTA 0: {len(full)} k-blocks, {len(tiles)} tiles")
-    print("  MMA full->full interval clk: median %.0f  p10 %.0f  p90 %.0f  max %.0f  (nominal MMA per k-block @8192 flop/clk/SM: %d)"
-          % (np.median(df), np.percentile(df, 10), np.percentile(df, 90), df.max(), 256 * d["tile_t"] * 64 * 2 // 2 // 8192))
+    print(f"{shp}: family {d['family']} t={d['tile_t']} stages/tile={kb} (kd={kd}); CTA 0: {len(full)} stages, {len(tiles)} tiles")
+    print("  MMA full->full interval clk: median %.0f  p10 %.0f  p90 %.0f  max %.0f  (nominal MMA per stage @8192 flop/clk/SM: %d)"
+          % (np.median(df), np.percentile(df, 10), np.percentile(df, 90), df.max(), kd * 256 * d["tile_t"] * 64 * 2 // 2 // 8192))
     if len(empty) > 1:
         de = np.diff(empty)
         print("  producer empty->empty interval clk: median %.0f  p90 %.0f" % (np.median(de), np.percentile(de, 90)))
@@ -47,7 +48,7 @@ for shp in (sys.argv[1] if len(sys.argv) > 1 else "17448x3072x1024,17448x1024x40
     print("  within-tile median %.0f, tile-boundary median %.0f" % (np.median(within), np.median(across) if across else -1))
     print("  first 24 intervals:", " ".join("%d" % v for v in df[:24]))
     pos = np.arange(len(df)) % kb                    # interval i ends at k-block i+1
-    prof = [np.mean(df[pos == q]) for q in range(min(kb, 16))]
+    prof = [np.mean(df[pos == q]) for q in range(min(kb, 16)) if np.any(pos == q)]
     print("  mean interval by k-block position in tile (first 16):", " ".join("%d" % v for v in prof))
     print("  mean %.0f; share of time in intervals > 800 clk: %.0f%%" % (df.mean(), 100 * df[df > 800].sum() / df.sum()))
     g1, g2 = [], []
