@@ -293,7 +293,12 @@ int nimble_lstm_seq(const float *G, int64_t ldg, const float *W_hh, int64_t ldw,
  * X W_ih1^T + (b_ih1 + b_hh1) (hoisted, nimble_dense_dyn); W_hh1, W_ih2, W_hh2 [4H x ldw]
  * (PyTorch row blocks i, f, g, o; layer 2's input is h1, so W_ih2 is [4H x H]); b2 [4H] =
  * b_ih2 + b_hh2; zero initial states.  Writes H1 [T x ldh], H2 [T x ldh] and hT, cT
- * [2 x H] (layer 0 then layer 1).  workspace: nimble_lstm2_workspace_bytes(H) bytes.
+ * [2 x H] (layer 0 then layer 1).  workspace: nimble_lstm2_workspace_bytes(H) bytes,
+ * ZERO-FILLED by the caller before its first use; every call leaves it zero again (the last
+ * CTA clears it), so no per-call memset sits on the hot path.  One workspace per concurrently
+ * running call.  The weights are staged into shared memory before the kernel's
+ * grid-dependency wait (PDL), overlapping the preceding input GEMM: W_hh1 / W_ih2 / W_hh2 must
+ * not be written by the immediately preceding kernel on the stream.
  * H <= 1024 (E_UNSUPPORTED beyond: the weights must fit in shared memory). */
 size_t nimble_lstm2_workspace_bytes(int64_t H);
 int nimble_lstm2_seq(const float *G1, int64_t ldg, const float *W_hh1, const float *W_ih2, const float *W_hh2,

@@ -158,7 +158,7 @@ int orc_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, int c, orc_dispa
         d->residue_class = (int32_t)d->r;
         d->variant = orc_variant(d->residue_class, 8, c);
         d->split_k = 1;
-        d->grid[0] = (int32_t)orc_ceil_div(N, 128);
+        d->grid[0] = (int32_t)orc_ceil_div(N, 32);    /* 32 output features per CTA */
         d->grid[1] = (int32_t)(d->k + (d->r > 0));
         d->grid[2] = 1;
         d->cluster[0] = d->cluster[1] = d->cluster[2] = 1;

@@ -75,7 +75,7 @@ int dispatch_simt8(int64_t M, int64_t N, nimble_dispatch *d) {
     d->residue_class = static_cast<int32_t>(d->r);
     d->variant = select_variant(kSIMT8, d->residue_class);
     d->split_k = 1;
-    d->grid[0] = static_cast<int32_t>(cdiv(N, 128));
+    d->grid[0] = static_cast<int32_t>(cdiv(N, 32));     // 32 output features per CTA (4 warps split K)
     d->grid[1] = static_cast<int32_t>(d->k + (d->r ? 1 : 0));
     d->grid[2] = 1;
     d->cluster[0] = d->cluster[1] = d->cluster[2] = 1;

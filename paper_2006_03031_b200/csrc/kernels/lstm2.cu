@@ -73,17 +73,21 @@ __device__ __forceinline__ void gather_h(float *dst, const unsigned long long *s
 }
 
 constexpr int kRowsPerWarp = 8;                 // gate rows per matrix per CTA <= 8 * kWarps
-// acc[rr] += W[row_rr] . x over the zero-padded row length Hp (multiple of 32): all of the
-// warp's rows advance together, one independent FMA chain each, no per-element guards.
+// acc[rr] += W[row_rr] . x over the zero-padded row length Hp (multiple of 128): all of the
+// warp's rows advance together, one independent FMA chain each, no per-element guards;
+// 16-B shared-memory loads (a lane takes 4 consecutive k of every 128).
 __device__ __forceinline__ void warp_rows_dot(float (&acc)[kRowsPerWarp], const float *W, const float *x, int Hp,
                                               int warp, int nrows, int lane) {
-#pragma unroll 4
-    for (int k = lane; k < Hp; k += 32) {
-        const float xv = x[k];
+#pragma unroll 2
+    for (int k = 4 * lane; k < Hp; k += 128) {
+        const float4 xv = *reinterpret_cast<const float4 *>(x + k);
 #pragma unroll
         for (int rr = 0; rr < kRowsPerWarp; ++rr) {
             const int r = warp + kWarps * rr;
-            if (r < nrows) acc[rr] = fmaf(W[(size_t)r * Hp + k], xv, acc[rr]);
+            if (r < nrows) {
+                const float4 wv = *reinterpret_cast<const float4 *>(W + (size_t)r * Hp + k);
+                acc[rr] = fmaf(wv.x, xv.x, fmaf(wv.y, xv.y, fmaf(wv.z, xv.z, fmaf(wv.w, xv.w, acc[rr]))));
+            }
         }
     }
 }
@@ -97,7 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
     const int j0 = cta * JB;
     const int R = 4 * JB;                       // gate rows per matrix
     const int nmat = l2 ? 2 : 1;
-    const int Hp = 32 * ((H + 31) / 32);        // rows zero-padded to whole warp chunks
+    const int Hp = 128 * ((H + 127) / 128);     // rows zero-padded to whole 128-wide warp chunks
     float *W = sm;                              // [nmat][R][Hp]
     float *x1 = W + (size_t)nmat * R * Hp;      // h1_{s-1} (zero-padded to Hp)
     float *x2 = x1 + Hp;                        // h2_{s-2} (layer 2 only)
@@ -105,16 +109,34 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
     float *cs = z + R;                          // [JB]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    // weights (static): staged before the grid-dependency wait, so with PDL this overlaps the
+    // preceding input-projection GEMM.  One warp per row, lanes along k, asynchronous 8-byte
+    // copies (cp.async, zero-filled past H): every copy of the CTA is in flight at once.
+    const bool even = ((a.ldw & 1) == 0) && ((H & 1) == 0);
     for (int m = 0; m < nmat; ++m) {
         const float *src = l2 ? (m == 0 ? a.Wih2 : a.Whh2) : a.Whh1;
-        for (int e = threadIdx.x; e < R * Hp; e += kThreads) {
-            const int r = e / Hp, k = e % Hp, g = r / JB, u = r % JB, j = j0 + u;
-            W[(size_t)m * R * Hp + e] = (j < H && k < H) ? src[(int64_t)(g * H + j) * a.ldw + k] : 0.f;
+        for (int r = warp; r < R; r += kWarps) {
+            const int g = r / JB, u = r - g * JB, j = j0 + u;
+            const float *row = src + (int64_t)(g * H + (j < H ? j : 0)) * a.ldw;
+            float *dst = W + ((size_t)m * R + r) * Hp;
+            if (even) {
+                for (int k = 2 * lane; k < Hp; k += 64) {
+                    const uint32_t nbytes = (j < H && k < H) ? 8u : 0u;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(ptx::smem_u32(dst + k)),
+                                 "l"(row + (k < H ? k : 0)), "r"(nbytes)
+                                 : "memory");
+                }
+            } else {
+                for (int k = lane; k < Hp; k += 32) dst[k] = (j < H && k < H) ? __ldg(row + k) : 0.f;
+            }
         }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     for (int u = threadIdx.x; u < JB; u += kThreads) cs[u] = 0.f;
     for (int k = threadIdx.x; k < Hp; k += kThreads) { x1[k] = 0.f; x2[k] = 0.f; }
     __syncthreads();
+    ptx::pdl_trigger();
+    ptx::pdl_wait();                            // G1 (the input GEMM) and the workspace of the previous call
 
     unsigned long long *tr = nullptr;
     if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || (int)blockIdx.x == a.n1))
@@ -184,11 +206,27 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
         __syncthreads();                        // z / x reuse in the next step
         if (tr) tr[s * 4 + 3] = ptx::globaltimer();
     }
+    // leave the tagged buffers zeroed for the next call (no host memset on the hot path): the
+    // last CTA to finish — every CTA has then consumed every word it polls — clears them
+    __shared__ int is_last;
+    unsigned *done = reinterpret_cast<unsigned *>(a.hbuf + 4 * (size_t)H);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (is_last) {
+        __threadfence();
+        for (int k = threadIdx.x; k < 4 * H; k += kThreads) a.hbuf[k] = 0ull;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) *done = 0u;
+    }
 }
 
 }  // namespace
 
-size_t lstm2_workspace_bytes(int64_t H) { return sizeof(unsigned long long) * 4 * (size_t)H; }
+size_t lstm2_workspace_bytes(int64_t H) { return sizeof(unsigned long long) * (4 * (size_t)H + 2); }   // + exit counter
 
 cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, const float *Wih2, const float *Whh2,
                              int64_t ldw, const float *b2, float *H1, float *H2, int64_t ldh, float *hT, float *cT,
@@ -200,16 +238,16 @@ cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, co
     int n2 = 2 * n1;
     const int JB2 = (int)((H + n2 - 1) / n2);
     n2 = (int)((H + JB2 - 1) / JB2);
-    const int64_t Hp = 32 * ((H + 31) / 32);
+    const int64_t Hp = 128 * ((H + 127) / 128);
     const size_t smem1 = sizeof(float) * ((size_t)4 * JB1 * Hp + 2 * Hp + 4 * JB1 + JB1);
     const size_t smem2 = sizeof(float) * ((size_t)8 * JB2 * Hp + 2 * Hp + 4 * JB2 + JB2);
     const size_t smem = smem1 > smem2 ? smem1 : smem2;
-    if (smem > 232448 || n1 + n2 > 148 || 4 * JB1 > 8 * kWarps || 4 * JB2 > 8 * kWarps) return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lstm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (smem > 232448 - 1024 || n1 + n2 > 148 || 4 * JB1 > 8 * kWarps || 4 * JB2 > 8 * kWarps) return cudaErrorInvalidValue;
+    static size_t attr = 0;                    // the kernel also has a few bytes of static smem
+    if (attr < smem) {
+        cudaError_t e = cudaFuncSetAttribute(lstm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr = smem;
     }
     Lstm2Args a;
     a.G1 = G1; a.ldg = ldg; a.Whh1 = Whh1; a.Wih2 = Wih2; a.Whh2 = Whh2; a.ldw = ldw; a.b2 = b2;
@@ -217,11 +255,22 @@ cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, co
     a.hbuf = static_cast<unsigned long long *>(workspace);
     a.T = (int)T; a.H = (int)H; a.n1 = n1; a.JB1 = JB1; a.JB2 = JB2;
     a.trace = lstm_trace_buffer();
-    cudaError_t e = cudaMemsetAsync(workspace, 0, lstm2_workspace_bytes(H), s);   // tag 0 = not yet written
-    if (e != cudaSuccess) return e;
-    void *args[] = {&a};
-    return cudaLaunchCooperativeKernel((const void *)lstm2_kernel, dim3((unsigned)(n1 + n2)), dim3(kThreads), args,
-                                       smem, s);
+    // the workspace is zero on entry (caller-zeroed before the first call; every call leaves it
+    // zeroed): tag 0 = not yet written.  Cooperative (all CTAs co-resident: they poll each other)
+    // and programmatic (the weight staging overlaps the preceding kernel).
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(n1 + n2));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, lstm2_kernel, a);
 }
 
 }  // namespace nimble

@@ -1,7 +1,7 @@
 // fp32 CUDA-core dense with the paper's residue-specialised symbolic tiling
 // (Nimble §3.5): the symbolic row extent M is tiled by t = 8
 // (the factor the paper's tuner chose) and rewritten M = 8k + r.
-// Each CTA owns 128 output features (one per thread) and one 8-row tile:
+// Each CTA owns 32 output features (lane = feature, 4 warps splitting K) and one 8-row tile:
 // CTAs blockIdx.y < k run the full tile with no guards; the single tail CTA
 // (blockIdx.y == k) runs a loop compiled for exactly r rows (variant r, no
 // guards).  The FALLBACK variant (-1) is the "fully guarded symbolic kernel":
@@ -15,49 +15,69 @@ namespace nimble {
 
 namespace {
 
-constexpr int kChunk = 64;
+constexpr int kChunk = 64;               // k per warp per round
+constexpr int kWarps = 4;                // the CTA's warps split K; lane = output feature
+constexpr int kFeat = 32;                // output features per CTA
 
 // ROWS >= 0: compile-time row count (no guards); ROWS < 0: runtime-guarded rows.
+// CTA = 32 features x one 8-row tile; warp w takes the k-chunks w, w + 4, ... (64 wide) of
+// every staged 256-wide round, and the four partial sums are added in warp order (fixed,
+// deterministic).  4x the CTAs of a thread-per-feature-whole-K layout: the weight stream of a
+// small-M call (LSTM input projection at T = 1, N = 2600) spreads over 4x the SMs.
 template <int ROWS>
 __device__ __forceinline__ void simt8_tile(const Simt8Params &p, int row0, int rows_rt) {
-    __shared__ float xs[8][kChunk];
-    const int n = blockIdx.x * 128 + threadIdx.x;
+    __shared__ float xs[8][kWarps * kChunk];
+    __shared__ float part[kWarps - 1][8][kFeat];
+    const int lane = (int)threadIdx.x & 31, warp = (int)threadIdx.x >> 5;
+    const int n = blockIdx.x * kFeat + lane;
     const bool n_ok = n < p.N;
     float acc[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) acc[r] = 0.f;
 
-    for (int k0 = 0; k0 < p.K; k0 += kChunk) {
+    for (int k0 = 0; k0 < p.K; k0 += kWarps * kChunk) {
         __syncthreads();
-        // stage the 8 x 64 x-chunk (rows beyond the tile / K are zeros, never read from memory)
-        for (int e = threadIdx.x; e < 8 * kChunk; e += 128) {
-            const int r = e / kChunk, kk = e % kChunk;
+        // stage the 8 x 256 x-round (rows beyond the tile / K are zeros, never read from memory)
+        for (int e = threadIdx.x; e < 8 * kWarps * kChunk; e += 32 * kWarps) {
+            const int r = e / (kWarps * kChunk), kk = e % (kWarps * kChunk);
             const bool live = (ROWS >= 0 ? r < ROWS : r < rows_rt) && (k0 + kk < p.K);
             xs[r][kk] = live ? p.x[(int64_t)(row0 + r) * p.ldx + k0 + kk] : 0.f;
         }
+        const int kw = k0 + warp * kChunk;               // this warp's 64-wide chunk
         float w[kChunk];
-        const float *wrow = p.W + (int64_t)n * p.ldw + k0;
+        const float *wrow = p.W + (int64_t)n * p.ldw + kw;
 #pragma unroll
         for (int q = 0; q < kChunk / 4; ++q) {
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (n_ok && k0 + 4 * q < p.K) v = *reinterpret_cast<const float4 *>(wrow + 4 * q);
+            if (n_ok && kw + 4 * q < p.K) v = *reinterpret_cast<const float4 *>(wrow + 4 * q);
             w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
         }
         __syncthreads();
+        const float *xw = &xs[0][warp * kChunk];
         if (ROWS >= 0) {
 #pragma unroll
             for (int r = 0; r < (ROWS >= 0 ? ROWS : 0); ++r)
 #pragma unroll
-                for (int kk = 0; kk < kChunk; ++kk) acc[r] = fmaf(w[kk], xs[r][kk], acc[r]);
+                for (int kk = 0; kk < kChunk; ++kk) acc[r] = fmaf(w[kk], xw[r * kWarps * kChunk + kk], acc[r]);
         } else {
 #pragma unroll
             for (int r = 0; r < 8; ++r)
                 if (r < rows_rt)                                   // the boundary check residue
 #pragma unroll                                                     // specialisation removes
-                    for (int kk = 0; kk < kChunk; ++kk) acc[r] = fmaf(w[kk], xs[r][kk], acc[r]);
+                    for (int kk = 0; kk < kChunk; ++kk) acc[r] = fmaf(w[kk], xw[r * kWarps * kChunk + kk], acc[r]);
         }
     }
-    if (!n_ok) return;
+    // partial sums of warps 1..3 -> warp 0, added in warp order
+    if (warp > 0) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) part[warp - 1][r][lane] = acc[r];
+    }
+    __syncthreads();
+    if (warp > 0 || !n_ok) return;
+#pragma unroll
+    for (int q = 0; q < kWarps - 1; ++q)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) acc[r] += part[q][r][lane];
     const float b = (p.epi >= 1) ? p.bias[n] : 0.f;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {

@@ -44,12 +44,11 @@ class LSTMStack:
         self.Hs = [torch.zeros((max_T, self.Hp), dtype=torch.float32, device=device) for _ in layers]
         self.hT = torch.empty((len(layers), H), dtype=torch.float32, device=device)
         self.cT = torch.empty((len(layers), H), dtype=torch.float32, device=device)
-        self.ws = torch.empty((max(nb.lstm_workspace_bytes(H), nb.lstm2_workspace_bytes(H)),), dtype=torch.uint8,
-                              device=device)
-        self.hT2 = torch.empty((2, H), dtype=torch.float32, device=device)
+        self.ws = torch.empty((nb.lstm_workspace_bytes(H),), dtype=torch.uint8, device=device)
+        # zeroed once: the wavefront kernel leaves its tagged buffers zeroed after every call
+        self.ws2 = torch.zeros((nb.lstm2_workspace_bytes(H),), dtype=torch.uint8, device=device)
         # the wavefront kernel takes W_hh1, W_ih2, W_hh2 with one leading dimension (H)
         self.Wi2u = layers[1][0].to(device).contiguous() if len(layers) == 2 and layers[1][0].shape[1] == H else None
-        self.cT2 = torch.empty((2, H), dtype=torch.float32, device=device)
 
     def flops_per_token(self) -> int:
         return sum(2 * 4 * self.H * (Kp + self.H) for (_, _, _, Kp) in self.layers)
@@ -61,9 +60,7 @@ class LSTMStack:
         if wavefront and self.Wi2u is not None:
             (Wi1, Wh1, b1, _), (Wi2, Wh2, b2, _) = self.layers
             nb.dense_dyn(x, Wi1, b1, self.G, epi=nb.EPI_BIAS, M=T)           # hoisted input GEMM (M = T)
-            nb.lstm2_seq(self.G, Wh1, self.Wi2u, Wh2, b2, self.Hs[0], self.Hs[1], self.hT2, self.cT2, self.ws, T=T)
-            self.hT.copy_(self.hT2)
-            self.cT.copy_(self.cT2)
+            nb.lstm2_seq(self.G, Wh1, self.Wi2u, Wh2, b2, self.Hs[0], self.Hs[1], self.hT, self.cT, self.ws2, T=T)
             return self.Hs[1][:T, :self.H]
         inp = x
         for li, (Wi, Wh, b, Kp) in enumerate(self.layers):

@@ -84,3 +84,50 @@ def test_shard_covers_and_balances():
         assert np.array_equal(allids, np.arange(len(lens)))
         loads = [sum(nb.request_cost(int(lens[i])) for i in p) for p in parts]
         assert max(loads) / (sum(loads) / G) < 1.001             # LPT at R = 4096: near-perfect balance
+
+
+def _worker_steps(rank, world, port, lens, d, steps, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2006_03031_b200.serve import ResultGather, shard
+    from paper_2006_03031_b200 import nimble as nb
+    ids = shard(lens, world, rank)
+    max_count = int(max(np.bincount(nb.partition_lpt(lens, world), minlength=world)))
+    g = ResultGather(max_count, d, world, rank, "cpu")
+    ids_t = torch.tensor(ids, dtype=torch.int64)
+    for step in range(steps):              # the bench's hot loop: gather every step, no host compaction
+        cls = torch.stack([_fake_cls(int(i) + 7919 * step, int(lens[i]), d) for i in ids]) if len(ids) else \
+            torch.zeros((0, d), dtype=torch.bfloat16)
+        g.step(ids_t, cls)
+    gids, gcls = g.result()                # once, after the loop: the last step's rows by id
+    if rank == 0:
+        q.put((gids.numpy().tolist(), gcls.float().numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_result_gather_multi_step_equals_single_process(world):
+    """ResultGather (bench.py's per-step collective, no host sync inside the loop): after several
+    steps rank 0 holds exactly the last step's [CLS] rows of every request, ordered by id, bit
+    for bit the same for G = 1 and G = 2."""
+    from paper_2006_03031_b200 import build
+    build.build()
+    lens = np.random.default_rng(11).integers(1, 513, 23).astype(np.int64)
+    d, steps = 8, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_steps, args=(r, world, port, lens, d, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ids, cls = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ids == list(range(len(lens)))
+    ref = torch.stack([_fake_cls(i + 7919 * (steps - 1), int(lens[i]), d) for i in range(len(lens))]).float().numpy()
+    assert np.array_equal(cls, ref)
