@@ -11,6 +11,8 @@
 // trip per step).  Ping-pong safety: before a CTA overwrites slot t & 1 it has polled every
 // CTA's later output (h1_{t-1} from layer 1, h2_{t-2} from layer 2), and each CTA produces
 // those only after it consumed what the slot held.
+#include <cstdlib>
+
 #include "launch.h"
 #include "ptx.cuh"
 
@@ -224,6 +226,162 @@ __global__ void __launch_bounds__(kThreads, 1) lstm2_kernel(const Lstm2Args a) {
     }
 }
 
+// ---- register-resident variant (H <= 672): 16 warps, each CTA's (matrix, gate-row) jobs
+// spread over the warps (<= 4 per warp); a lane keeps k = lane + 32 i (i < NI) of each of its
+// rows in registers for the whole sequence, so a step reads only x from shared memory (the
+// shared-memory variant re-reads its whole weight block, ~170 KB, every step).
+constexpr int kRegThreads = 512;
+constexpr int kRegWarps = kRegThreads / 32;
+constexpr int kJobsPerWarp = 4;
+
+template <int NI>
+__global__ void __launch_bounds__(kRegThreads, 1) lstm2_reg_kernel(const Lstm2Args a) {
+    extern __shared__ float sm[];
+    const int H = a.H;
+    const bool l2 = (int)blockIdx.x >= a.n1;
+    const int cta = l2 ? (int)blockIdx.x - a.n1 : (int)blockIdx.x;
+    const int JB = l2 ? a.JB2 : a.JB1;
+    const int j0 = cta * JB;
+    const int R = 4 * JB;                       // gate rows per matrix
+    const int nmat = l2 ? 2 : 1;
+    const int J = nmat * R;                     // jobs: (matrix, row)
+    constexpr int Hp = 32 * NI;
+    float *x1 = sm;                             // h1_{s-1} (zero-padded to Hp)
+    float *x2 = x1 + Hp;                        // h2_{s-2} (layer 2 only)
+    float *z = x2 + Hp;                         // [2][R] per-matrix gate pre-activations
+    float *cs = z + 2 * R;                      // [JB]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // weights -> registers (static: before the grid-dependency wait, overlapping the input GEMM)
+    float w[kJobsPerWarp][NI];
+    int jm[kJobsPerWarp];                       // matrix of job q (-1: none)
+#pragma unroll
+    for (int q = 0; q < kJobsPerWarp; ++q) {
+        const int jb = warp + kRegWarps * q;
+        jm[q] = jb < J ? jb / R : -1;
+        const int r = jb < J ? jb % R : 0;
+        const int g = r / JB, u = r - g * JB, j = j0 + u;
+        const float *src = l2 ? (jm[q] == 0 ? a.Wih2 : a.Whh2) : a.Whh1;
+        const float *row = src + (int64_t)(g * H + (j < H ? j : 0)) * a.ldw;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int k = lane + 32 * i;
+            w[q][i] = (jm[q] >= 0 && j < H && k < H) ? __ldg(row + k) : 0.f;
+        }
+    }
+    for (int u = threadIdx.x; u < JB; u += kRegThreads) cs[u] = 0.f;
+    for (int k = threadIdx.x; k < Hp; k += kRegThreads) { x1[k] = 0.f; x2[k] = 0.f; }
+    __syncthreads();
+    ptx::pdl_trigger();
+    ptx::pdl_wait();                            // G1 (the input GEMM) and the workspace of the previous call
+
+    unsigned long long *tr = nullptr;
+    if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || (int)blockIdx.x == a.n1))
+        tr = a.trace + (size_t)(blockIdx.x == 0 ? 0 : 1) * (a.T + 1) * 4;
+    for (int s = 0; s <= a.T; ++s) {
+        const int t = l2 ? s - 1 : s;           // the time step this CTA computes
+        const bool active = t >= 0 && t < a.T;
+        if (tr) tr[s * 4 + 0] = ptx::globaltimer();
+        float gpre[4] = {0.f, 0.f, 0.f, 0.f};
+        if (!l2 && active && threadIdx.x < JB && j0 + (int)threadIdx.x < H) {
+            const float *g = a.G1 + (int64_t)t * a.ldg + j0 + threadIdx.x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) gpre[q] = __ldg(g + q * H);
+        }
+        if (s > 0) {
+            gather_h(x1, a.hbuf + (size_t)((s - 1) & 1) * H, H, (unsigned)s);
+            if (s >= 2) gather_h(x2, a.hbuf + (size_t)(2 + ((s - 2) & 1)) * H, H, (unsigned)(s - 1));
+            __syncthreads();
+        }
+        if (tr) tr[s * 4 + 1] = ptx::globaltimer();
+        if (active) {
+            float acc[kJobsPerWarp];
+#pragma unroll
+            for (int q = 0; q < kJobsPerWarp; ++q) acc[q] = 0.f;
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const float xa = x1[lane + 32 * i];
+                const float xb = l2 ? x2[lane + 32 * i] : 0.f;
+#pragma unroll
+                for (int q = 0; q < kJobsPerWarp; ++q) acc[q] = fmaf(w[q][i], jm[q] == 1 ? xb : xa, acc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < kJobsPerWarp; ++q) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int q = 0; q < kJobsPerWarp; ++q) {
+                    const int jb = warp + kRegWarps * q;
+                    if (jb < J) z[jb] = acc[q];          // z[m R + r]
+                }
+            }
+            __syncthreads();
+            if (tr) tr[s * 4 + 2] = ptx::globaltimer();
+            if (threadIdx.x < JB) {
+                const int u = threadIdx.x, j = j0 + u;
+                if (j < H) {
+                    float zi, zf, zg, zo;
+                    if (l2) {
+                        zi = z[u] + z[R + u] + a.b2[j];
+                        zf = z[JB + u] + z[R + JB + u] + a.b2[H + j];
+                        zg = z[2 * JB + u] + z[R + 2 * JB + u] + a.b2[2 * H + j];
+                        zo = z[3 * JB + u] + z[R + 3 * JB + u] + a.b2[3 * H + j];
+                    } else {
+                        zi = z[u] + gpre[0]; zf = z[JB + u] + gpre[1]; zg = z[2 * JB + u] + gpre[2];
+                        zo = z[3 * JB + u] + gpre[3];
+                    }
+                    const float c = ptx::sigmoidf_(zf) * cs[u] + ptx::sigmoidf_(zi) * tanhf(zg);
+                    const float h = ptx::sigmoidf_(zo) * tanhf(c);
+                    cs[u] = c;
+                    st_relaxed_u64(a.hbuf + (size_t)((l2 ? 2 : 0) + (t & 1)) * H + j,
+                                   ((unsigned long long)(t + 1) << 32) | __float_as_uint(h));
+                    (l2 ? a.H2 : a.H1)[(int64_t)t * a.ldh + j] = h;
+                    if (t == a.T - 1) {
+                        a.hT[(l2 ? H : 0) + j] = h;
+                        a.cT[(l2 ? H : 0) + j] = c;
+                    }
+                }
+            }
+        }
+        __syncthreads();                        // z / x reuse in the next step
+        if (tr) tr[s * 4 + 3] = ptx::globaltimer();
+    }
+    __shared__ int is_last;
+    unsigned *done = reinterpret_cast<unsigned *>(a.hbuf + 4 * (size_t)H);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (is_last) {
+        __threadfence();
+        for (int k = threadIdx.x; k < 4 * H; k += kRegThreads) a.hbuf[k] = 0ull;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) *done = 0u;
+    }
+}
+
+template <int NI>
+cudaError_t launch_reg(const Lstm2Args &a, unsigned grid, cudaStream_t s) {
+    const size_t smem = sizeof(float) * ((size_t)2 * 32 * NI + 2 * 4 * a.JB1 + a.JB1 + 64);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kRegThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, lstm2_reg_kernel<NI>, a);
+}
+
 }  // namespace
 
 size_t lstm2_workspace_bytes(int64_t H) { return sizeof(unsigned long long) * (4 * (size_t)H + 2); }   // + exit counter
@@ -255,6 +413,17 @@ cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, co
     a.hbuf = static_cast<unsigned long long *>(workspace);
     a.T = (int)T; a.H = (int)H; a.n1 = n1; a.JB1 = JB1; a.JB2 = JB2;
     a.trace = lstm_trace_buffer();
+    // register-resident weights when every CTA's (matrix, row) jobs fit 4 per warp and a row's
+    // k-slice per lane fits NI <= 21 registers (H <= 672: config 2's 650, the paper's 512)
+    static const bool reg_on = [] { const char *e = std::getenv("NIMBLE_LSTM_REG"); return !(e && e[0] == '0'); }();
+    const int ni = (int)((H + 31) / 32);
+    if (reg_on && ni <= 21 && 4 * JB1 <= kRegWarps * kJobsPerWarp && 8 * JB2 <= kRegWarps * kJobsPerWarp) {
+        const unsigned grid = (unsigned)(n1 + n2);
+        if (ni <= 8) return launch_reg<8>(a, grid, s);
+        if (ni <= 12) return launch_reg<12>(a, grid, s);
+        if (ni <= 16) return launch_reg<16>(a, grid, s);
+        return launch_reg<21>(a, grid, s);
+    }
     // the workspace is zero on entry (caller-zeroed before the first call; every call leaves it
     // zeroed): tag 0 = not yet written.  Cooperative (all CTAs co-resident: they poll each other)
     // and programmatic (the weight staging overlaps the preceding kernel).
