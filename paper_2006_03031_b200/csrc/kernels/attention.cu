@@ -436,9 +436,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             float *rd = red + (ns & 1) * 256;         // parity buffer: a fast half never overwrites
             ++ns;                                     // the max its partner has not read yet
             const int kbase = j * 128 + half * 64;    // key index of v[0]
-            const bool full = kbase + 64 <= L;
+            const int nvalid = min(max(L - kbase, 0), 64);   // keys of this half-block inside the request
+            // a partial half-block runs the same vectorised code: keys >= L are left out of the max
+            // (read as -inf) and their exponentials zeroed; a fully masked one skips the exponentials
             float mx = -INFINITY;
-            if (full) {
+            if (nvalid == 64) {
                 float ma = v[0], mb = v[1];
 #pragma unroll
                 for (int e = 2; e < 62; e += 4) {
@@ -446,10 +448,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                     mb = fmax3(mb, v[e + 2], v[e + 3]);
                 }
                 mx = fmax3(ma, mb, fmaxf(v[62], v[63]));
-            } else {
+            } else if (nvalid > 0) {
+                float ma = -INFINITY, mb = -INFINITY;
 #pragma unroll
-                for (int e = 0; e < 64; ++e)
-                    if (kbase + e < L) mx = fmaxf(mx, v[e]);
+                for (int e = 0; e < 64; e += 4) {
+                    ma = fmax3(ma, e < nvalid ? v[e] : -INFINITY, e + 1 < nvalid ? v[e + 1] : -INFINITY);
+                    mb = fmax3(mb, e + 2 < nvalid ? v[e + 2] : -INFINITY, e + 3 < nvalid ? v[e + 3] : -INFINITY);
+                }
+                mx = fmaxf(ma, mb);
             }
             if (tr) ATT_TRACE(tb, 1);
             rd[half * 128 + q] = mx;
@@ -468,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             const float alpha = grow ? ptx::ex2_approx((m_run - m_new) * sl2) : 1.f;   // -inf -> 0
             const float ms = m_new * sl2;
             float2 sa = make_float2(0.f, 0.f), sb = sa;
-            if (full) {
+            if (nvalid > 0) {
                 const float2 sc = make_float2(sl2, sl2), nm = make_float2(-ms, -ms);
 #pragma unroll
                 for (int e = 0; e < 64; e += 2) {
@@ -482,9 +488,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                     v[e] = x.x;
                     v[e + 1] = x.y;
                 }
-            } else {
+            }
+            if (nvalid < 64) {                        // exactly 0 past L (the poly floors at 2^-125)
 #pragma unroll
-                for (int e = 0; e < 64; ++e) v[e] = (kbase + e < L) ? ptx::ex2_approx(fmaf(v[e], sl2, -ms)) : 0.f;
+                for (int e = 0; e < 64; ++e) v[e] = e < nvalid ? v[e] : 0.f;
             }
 #pragma unroll
             for (int e = 0; e < 64; e += 4) {
