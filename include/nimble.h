@@ -76,8 +76,10 @@ typedef enum {
 
 /* The dispatch record: exactly what the matching kernel entry point launches.
  * Field meanings are DISPATCH.md's.  family: 0 SIMT8 (fp32), 1 UMMA_T (bf16,
- * tokens on the UMMA-N slot), 2 UMMA_D (bf16 bmm with trans_b).  variant -1 is
- * the guarded fallback.  x = tile_t*k + r. */
+ * tokens on the UMMA-N slot), 2 UMMA_D (bf16 bmm with trans_b), 3 UMMA_T256 (bf16,
+ * M >= 2048, CTA pairs), 4 UMMA_WS (bf16 dense, M <= 128: weight streaming, the K
+ * splits of a feature tile one cluster).  variant -1 is the guarded fallback.
+ * x = tile_t*k + r. */
 typedef struct {
     int32_t family, tile_t, granule, n_classes, residue_class, variant, split_k;
     int32_t umma_m, umma_n_full, umma_n_tail;
@@ -138,7 +140,12 @@ int nimble_last_dispatch(nimble_dispatch *out);
  * dt = NIMBLE_F32: fp32 in/out, CUDA-core FFMA (SIMT8, t = 8 residue variants).
  * dt = NIMBLE_BF16: bf16 in/out, fp32 accumulation in TMEM (tcgen05 + TMA),
  *      output rounded to bf16 (RNE); rows >= M are never read (TMA bounds) nor
- *      written.  The dynamic extent is never padded.
+ *      written.  The dynamic extent is never padded.  With M <= 128 and no tuned
+ *      schedule (family 4) the K splits' fp32 partials go through a library workspace
+ *      owned by the calling STREAM (a pool of 16 per device, allocated on the stream's first
+ *      family-4 launch, in relaxed capture mode inside a graph capture); more than 16
+ *      streams share slots round-robin, and concurrent launches on two streams that share a
+ *      slot are not supported.
  * ------------------------------------------------------------------------- */
 int nimble_dense_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
                      const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,

@@ -148,6 +148,31 @@ static int orc_umma_t(int64_t batch, int64_t M, int64_t N, int64_t K, int c, orc
     return orc_umma_t_sched(batch, M, N, K, c, 0, 8, d);
 }
 
+/* family 4, UMMA_WS (DISPATCH.md): a bf16 dense whose symbolic extent fits one token tile
+ * (M <= 128) and whose 128-feature tiles fit one wave (ceil(N/128) <= 148) streams W over
+ * ceil(N/128) x S CTAs, S = min(ceil(K/64), floor(148 / ceil(N/128)), 16) (at least 1) splits
+ * of K (the S splits of a feature tile are one thread-block cluster, at most 16 CTAs).
+ * The residue split of M is family 1's (t = 128, granule 16, 9 classes). */
+static int orc_umma_ws(int64_t M, int64_t N, int64_t K, int c, orc_dispatch *d) {
+    memset(d, 0, sizeof(*d));
+    d->family = 4; d->tile_t = 128; d->granule = 16; d->n_classes = 9;
+    d->k = M / 128; d->r = M % 128;                  /* x = t k + r */
+    d->residue_class = (int32_t)orc_ceil_div(d->r, 16);
+    d->variant = orc_variant(d->residue_class, 9, c);
+    d->umma_m = 128; d->umma_n_full = 128;
+    d->umma_n_tail = (d->r == 0) ? 0 : ((d->variant >= 0) ? 16 * d->residue_class : 128);
+    int64_t feature_tiles = orc_ceil_div(N, 128);
+    int64_t kblocks = orc_ceil_div(K, 64);
+    int64_t splits = 148 / feature_tiles;
+    if (splits > kblocks) splits = kblocks;
+    if (splits > 16) splits = 16;                    /* the splits of a tile form one cluster */
+    if (splits < 1) splits = 1;
+    d->split_k = (int32_t)splits;
+    d->grid[0] = (int32_t)feature_tiles; d->grid[1] = 1; d->grid[2] = (int32_t)splits;
+    d->cluster[0] = 1; d->cluster[1] = 1; d->cluster[2] = 1;
+    return ORC_OK;
+}
+
 int orc_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, int c, orc_dispatch *d) {
     if (M < 1 || N < 1 || K < 1 || M > ORC_MAXEXT || N > ORC_MAXEXT || K > ORC_MAXEXT) return ORC_E_EXTENT;
     if (c < 0) return ORC_E_EXTENT;
@@ -165,6 +190,7 @@ int orc_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, int c, orc_dispa
         return ORC_OK;
     }
     if (dt != 1) return ORC_E_DTYPE;
+    if (M <= 128 && orc_ceil_div(N, 128) <= 148) return orc_umma_ws(M, N, K, c, d);
     return orc_umma_t(1, M, N, K, c, d);
 }
 

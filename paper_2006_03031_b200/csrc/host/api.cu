@@ -272,6 +272,101 @@ struct LnArgs {
 }  // namespace
 }  // namespace nimble
 
+// Library workspace of the weight-streaming family (4): per stream, the fp32 partial slabs of
+// one launch (<= 148 CTAs x 128 tokens x 128 features).  Allocated when a stream is first seen
+// (inside a graph capture the allocation runs in relaxed capture mode).  More than kWsSlots
+// streams share slots round-robin (include/nimble.h: concurrent family-4 launches on streams
+// that share a slot are not supported).
+namespace nimble {
+namespace {
+constexpr int kWsSlots = 16;
+constexpr size_t kWsPartElems = (size_t)kNumSMs * 128 * 128;
+struct WsWorkspace {
+    std::mutex mu;
+    std::vector<std::pair<cudaStream_t, int>> owner[64];
+    float *part[64][kWsSlots] = {};
+};
+WsWorkspace g_ws;
+cudaError_t ws_workspace(cudaStream_t stream, float **part) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_ws.mu);
+    auto &own = g_ws.owner[dev];
+    int slot = -1;
+    for (const auto &o : own)
+        if (o.first == stream) slot = o.second;
+    if (slot < 0) {
+        slot = (int)(own.size() % kWsSlots);
+        own.emplace_back(stream, slot);
+    }
+    if (!g_ws.part[dev][slot]) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if ((e = cudaStreamIsCapturing(stream, &cs)) != cudaSuccess) return e;
+        const bool capturing = cs != cudaStreamCaptureStatusNone;
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        if (capturing) cudaThreadExchangeStreamCaptureMode(&mode);
+        e = cudaMalloc(&g_ws.part[dev][slot], sizeof(float) * kWsPartElems);
+        if (capturing) cudaThreadExchangeStreamCaptureMode(&mode);
+        if (e != cudaSuccess) return e;
+    }
+    *part = g_ws.part[dev][slot];
+    return cudaSuccess;
+}
+
+// Family 4 launch (DISPATCH.md): returns NIMBLE_OK, an error, or 1 when a cluster of S CTAs
+// cannot be scheduled on this device (an SM partition smaller than the cluster under MPS /
+// green contexts): the caller then takes family 1.
+int launch_ws(const nimble_dispatch &d, const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
+              const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N, int64_t K, int epi,
+              cudaStream_t s) {
+    WsLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    L.p.M = (int32_t)M;
+    L.p.N = (int32_t)N;
+    L.p.m_tiles = d.grid[0];
+    L.p.S = d.split_k;
+    L.p.kb_total = (int32_t)((K + 63) / 64);
+    L.p.n_umma = d.r ? d.umma_n_tail : d.umma_n_full;
+    L.p.n_box = L.p.n_umma;
+    const int kb_max = (L.p.kb_total + L.p.S - 1) / L.p.S;
+    L.p.stages = kb_max < 3 ? kb_max : 3;
+    L.smem_bytes = ws_smem_bytes(L.p.n_box, L.p.stages);
+    static std::mutex fit_mu;
+    static std::vector<std::pair<int, size_t>> fits;     // (S, smem) known to schedule
+    {
+        std::lock_guard<std::mutex> lk(fit_mu);
+        bool known = false;
+        for (const auto &f : fits) known |= (f.first == L.p.S && f.second == L.smem_bytes);
+        if (!known) {
+            if (!ws_cluster_fits(L.p.S, L.smem_bytes)) return 1;
+            fits.emplace_back(L.p.S, L.smem_bytes);
+        }
+    }
+    float *part = nullptr;
+    cudaError_t e = ws_workspace(s, &part);
+    if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn(family 4) workspace", e);
+    L.p.part = part;
+    L.p.trace = g_trace;
+    L.p.alpha = 1.f;
+    L.p.bias = bias;
+    L.p.res = static_cast<const __nv_bfloat16 *>(residual);
+    L.p.ld_res = ldr;
+    L.p.out = static_cast<__nv_bfloat16 *>(y);
+    L.p.ld_out = ldy;
+    L.epi = epi;
+    int st, mid = 0;
+    if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &mid)) != NIMBLE_OK) return st;
+    if ((st = encode_operand(&L.tmB, x, K, M, ldx, 1, 0, L.p.n_box, &mid)) != NIMBLE_OK) return st;
+    L.stream = s;
+    e = launch_ws_gemm(L);
+    if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn(family 4) launch", e);
+    return NIMBLE_OK;
+}
+}  // namespace
+}  // namespace nimble
+
 static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
                       const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N,
                       int64_t K, int dt, int epi, void *stream, bool static_twin, LnArgs *ln = nullptr) {
@@ -309,9 +404,20 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     if (!aligned16(x) || !aligned16(W) || !aligned16(y) || ((ldx * 2) % 16) || ((ldw * 2) % 16) || ((ldy * 2) % 16) ||
         (epi == NIMBLE_EPI_BIAS_RESIDUAL && (!aligned16(residual) || (ldr * 2) % 16)))
         return fail(NIMBLE_E_ALIGN, "nimble_dense_dyn(bf16): TMA needs 16-B aligned x/W/y/residual and ld*2 % 16 == 0");
-    {
-        int32_t t = 0, cap = 8;                       // tuned schedule for this op, if registered
-        if (!static_twin) dense_schedule(N, K, &t, &cap);  // (static twins are compiled for t = 128)
+    if (static_twin) dispatch_umma_t(1, M, N, K, &d);   // static twins are compiled for family 1/3, t = 128
+    else dispatch_dense_bf16(M, N, K, &d);               // tuned schedule, if registered; family 4 at M <= 128
+    if (d.family == 4) {
+        // (dense_ln_dyn: the LayerNorm needs whole rows across feature tiles, i.e. across
+        // clusters: it stays a separate launch after the family-4 GEMM)
+        const int ws = launch_ws(d, x, ldx, W, ldw, bias, residual, ldr, y, ldy, M, N, K, epi, s);
+        if (ws == NIMBLE_OK) {
+            record_dispatch(d);
+            clear_error();
+            return NIMBLE_OK;
+        }
+        if (ws != 1) return ws;
+        int32_t t = 0, cap = 8;                      // not co-resident here: family 1
+        dense_schedule(N, K, &t, &cap);
         dispatch_umma_t(1, M, N, K, &d, t, cap);
     }
     UmmaLaunch L;

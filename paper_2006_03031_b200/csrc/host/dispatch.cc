@@ -26,6 +26,7 @@ constexpr ResidueFamily kUMMA_T{1, 128, 16, 9};    // bf16 tcgen05, tokens on UM
 constexpr ResidueFamily kUMMA_T256{3, 256, 16, 17}; // same, M >= 2048 (no split-K)
 constexpr int64_t kWideTileFrom = 2048;
 constexpr ResidueFamily kUMMA_D{2, 128, 128, 2}; // bf16 tcgen05 bmm with MN-major B
+constexpr ResidueFamily kUMMA_WS{4, 128, 16, 9};  // bf16 tcgen05 dense, M <= 128: weight streaming
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -112,6 +113,41 @@ int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, 
     d->cluster[1] = 1;
     d->cluster[2] = d->split_k;
     return NIMBLE_OK;
+}
+
+// Family 4 (DISPATCH.md): a dense with one token tile (M <= 128) and no tuned schedule streams
+// its weights over one wave of CTAs: 128-feature tiles x S splits of K (one cluster per tile,
+// S <= 16), S a function of (N, K) only.
+constexpr int64_t kWsMaxCluster = 16;            // largest (non-portable) thread-block cluster
+bool ws_applies(int64_t M, int64_t N) { return M <= kUMMA_WS.t && cdiv(N, 128) <= kNumSMs; }
+
+int dispatch_umma_ws(int64_t M, int64_t N, int64_t K, nimble_dispatch *d) {
+    *d = nimble_dispatch{};
+    split_residue(kUMMA_WS, M, d);
+    d->residue_class = static_cast<int32_t>(cdiv(d->r, kUMMA_WS.granule));
+    d->variant = select_variant(kUMMA_WS, d->residue_class);
+    d->umma_m = 128;
+    d->umma_n_full = kUMMA_WS.t;
+    d->umma_n_tail = d->r == 0 ? 0 : (d->variant < 0 ? kUMMA_WS.t : kUMMA_WS.granule * d->residue_class);
+    const int64_t m_tiles = cdiv(N, 128);
+    const int64_t kb = cdiv(K, 64);
+    int64_t s = kNumSMs / m_tiles;                  // one wave of CTAs ...
+    if (s > kb) s = kb;                             // ... each with >= 1 k-block of 64 ...
+    if (s > kWsMaxCluster) s = kWsMaxCluster;       // ... the splits of a tile one cluster
+    if (s < 1) s = 1;
+    d->split_k = static_cast<int32_t>(s);
+    d->grid[0] = static_cast<int32_t>(m_tiles);
+    d->grid[1] = 1;
+    d->grid[2] = d->split_k;
+    d->cluster[0] = d->cluster[1] = d->cluster[2] = 1;
+    return NIMBLE_OK;
+}
+
+int dispatch_dense_bf16(int64_t M, int64_t N, int64_t K, nimble_dispatch *d) {
+    int32_t t, cap;
+    dense_schedule(N, K, &t, &cap);
+    if (t == 0 && ws_applies(M, N)) return dispatch_umma_ws(M, N, K, d);
+    return dispatch_umma_t(1, M, N, K, d, t, cap);
 }
 
 int dispatch_umma_d(int64_t batch, int64_t M, int64_t N, int64_t K, nimble_dispatch *d) {
@@ -202,11 +238,7 @@ extern "C" int nimble_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, ni
     if (!out) return fail(NIMBLE_E_NULL, "nimble_dispatch_dense: out is NULL");
     if (!extents_valid({M, N, K})) return fail(NIMBLE_E_EXTENT, "nimble_dispatch_dense: extents must be in [1, 2^31-1]");
     if (dt == NIMBLE_F32) return dispatch_simt8(M, N, out);
-    if (dt == NIMBLE_BF16) {
-        int32_t t, cap;
-        dense_schedule(N, K, &t, &cap);
-        return dispatch_umma_t(1, M, N, K, out, t, cap);
-    }
+    if (dt == NIMBLE_BF16) return dispatch_dense_bf16(M, N, K, out);
     return fail(NIMBLE_E_DTYPE, "nimble_dispatch_dense: unknown dtype");
 }
 

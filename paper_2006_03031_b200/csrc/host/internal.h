@@ -25,6 +25,9 @@ int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, 
                     int32_t tile_t = 0, int32_t split_max = 8);
 // bf16 dense: the tuned schedule registered for (N, K) (nimble_set_dense_schedule), if any
 void dense_schedule(int64_t N, int64_t K, int32_t *tile_t, int32_t *split_max);
+// bf16 dense: family 4 (weight streaming, M <= 128, no tuned schedule) or families 1 / 3
+int dispatch_dense_bf16(int64_t M, int64_t N, int64_t K, nimble_dispatch *d);
+int dispatch_umma_ws(int64_t M, int64_t N, int64_t K, nimble_dispatch *d);
 int dispatch_umma_d(int64_t batch, int64_t M, int64_t N, int64_t K, nimble_dispatch *d);
 
 }  // namespace nimble

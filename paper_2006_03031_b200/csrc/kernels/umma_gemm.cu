@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (isA && (p.dbg & 4) && trace && cta_lin == 0 && nkb_p < 4096) p.trace[16384 + nkb_p] = clock64();
                 ++nkb_p;
-                if (arms) ptx::mbar_arrive_expect_tx(&full_bar[stage], tx);
+                if (arms) ptx::mbar_arrive_expect_tx_relaxed(&full_bar[stage], tx);
                 const int32_t kc = kb * kBlockK;
                 uint8_t *sa = smem + stage * stage_bytes;
                 if (isA) {

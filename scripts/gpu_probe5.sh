@@ -1,0 +1,7 @@
+set -u
+mkdir -p gpurun_out; O=gpurun_out
+timeout 900 python -m pytest tests/test_gpu_ws.py -x -q -p no:cacheprovider > $O/ws_tests.log 2>&1; echo "rc=$?" >> $O/ws_tests.log; tail -5 $O/ws_tests.log
+timeout 300 python scripts/trace_ws.py > $O/trace_ws.txt 2>&1; cat $O/trace_ws.txt
+rm -f $O/sweep_ws.jsonl
+timeout 600 python scripts/gemm_sweep.py --Ms 1,16,64,128 --tag ws --out $O/sweep_ws.jsonl > /dev/null 2>&1; echo "sweep rc=$?"
+timeout 600 python scripts/gemm_sweep.py --shapes base --Ms 1,16,64,128 --tag ws_base --out $O/sweep_ws.jsonl > /dev/null 2>&1; echo "sweep rc=$?"

@@ -132,7 +132,14 @@ def test_dispatch_invariants(orc, dt):
                     assert d["r"] <= d["umma_n_tail"] < d["r"] + 16 and d["umma_n_tail"] % 16 == 0
                 else:
                     assert d["umma_n_tail"] == t
-            if dt == 1:
+            if dt == 1 and M <= 128:
+                # family 4 (weight streaming): 8 feature tiles x S splits of the 16 k-blocks,
+                # one wave (8 S <= 148), no cluster; S does not depend on M
+                s = d["split_k"]
+                assert d["family"] == 4 and d["umma_m"] == 128 and list(d["cluster"]) == [1, 1, 1]
+                assert list(d["grid"]) == [8, 1, s] and 8 * s <= 148 and 1 <= s <= 16
+                assert s == 16                                     # min(16 k-blocks, 148 // 8)
+            elif dt == 1:
                 s = d["split_k"]
                 assert s in (1, 2, 4, 8) and d["cluster"] == ((1 if M < 2048 else 2), 1, s)
                 assert d["umma_m"] == (128 if M < 2048 else 256)
@@ -159,6 +166,33 @@ def test_dispatch_bmm_families(orc):
     assert d["umma_n_full"] == 64 and d["umma_n_tail"] == 64 and d["grid"][1] == 1
 
 
+def test_dispatch_weight_streaming_family(orc):
+    """Family 4 pins (DISPATCH.md): taken exactly when M <= 128 and the 128-feature tiles fit
+    one wave; grid = tiles x S with S = min(k-blocks, 148 // tiles, 16) >= 1 — every CTA owns at
+    least one k-block of 64, the grid never exceeds one wave of 148 and a tile's splits fit one
+    cluster; S is the same for every M (pad-then-slice invariant); the residue split equals
+    family 1's."""
+    cases = [(2304, 768, 8), (768, 768, 12), (3072, 768, 6), (768, 3072, 16), (1024, 1024, 16),
+             (3072, 1024, 6), (4096, 1024, 4), (1024, 4096, 16), (128, 64, 1), (128, 100000, 16),
+             (18944, 512, 1), (300, 200, 4)]
+    for N, K, S in cases:
+        tiles = -(-N // 128)
+        for M in (1, 2, 15, 16, 17, 100, 127, 128):
+            st, d = orc.dispatch_dense(M, N, K, 1)
+            assert st == 0 and d["family"] == 4 and d["split_k"] == S, (N, K, M, d)
+            assert tiles * S <= 148 and S <= -(-K // 64) and S <= 16
+            assert list(d["grid"]) == [tiles, 1, S]
+            d1 = orc.dispatch_dense(M, N, K, 1, 0, 128, 1)[1]      # family 1 with the same t
+            for key in ("k", "r", "residue_class", "variant", "umma_n_full", "umma_n_tail", "n_classes"):
+                assert d[key] == d1[key], key
+        assert orc.dispatch_dense(129, N, K, 1)[1]["family"] == 1
+    # more feature tiles than one wave: family 1
+    assert orc.dispatch_dense(5, 149 * 128, 256, 1)[1]["family"] == 1
+    assert orc.dispatch_dense(5, 148 * 128, 256, 1)[1]["family"] == 4
+    # fp32 keeps the paper's SIMT8 family
+    assert orc.dispatch_dense(5, 1024, 1024, 0)[1]["family"] == 0
+
+
 @pytest.mark.parametrize("tile_t,split_max", [(32, 8), (64, 2), (128, 8), (256, 4)])
 def test_oracle_tuned_schedule_invariants(orc, tile_t, split_max):
     """Pins of the schedule-parameterised dispatch (DISPATCH.md "Tuned schedules"): the
@@ -181,7 +215,7 @@ def test_oracle_tuned_schedule_invariants(orc, tile_t, split_max):
         assert s in (1, 2, 4, 8) and s <= split_max and (s == 1 or m_tiles * n_tiles * s <= 148)
         assert tile_t <= 128 or s == 1
         assert d["grid"][2] == s and list(d["cluster"]) == [1, 1, s]
-        if tile_t == 128 and split_max == (8 if K >= 2048 else 1):
+        if tile_t == 128 and split_max == (8 if K >= 2048 else 1) and M > 128:
             assert d == orc.dispatch_dense(M, N, K, 1)[1]     # the default rule's (t, cap)
     for M in (2048, 5000):
         assert orc.dispatch_dense(M, N, K, 1, 0, tile_t, split_max)[1] == orc.dispatch_dense(M, N, K, 1)[1]
