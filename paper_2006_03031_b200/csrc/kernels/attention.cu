@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
     const int R = p.R, H = p.heads;
     unsigned long long *trace = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
+    const unsigned long long t_start = p.trace ? ptx::globaltimer() : 0ull;   // per-CTA span (debug)
 #define ATT_TRACE(blk, ev) do { if (trace && (blk) < 512) trace[(blk) * 8 + (ev)] = clock64(); } while (0)
 
     if (threadIdx.x == 0) {
@@ -618,6 +619,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     if (warp == 8) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, 256);
+    }
+    if (p.trace && threadIdx.x == 0) {                // per-CTA span (scripts/attn_balance.py)
+        p.trace[8192 + 2 * blockIdx.x] = t_start;
+        p.trace[8192 + 2 * blockIdx.x + 1] = ptx::globaltimer();
     }
 }
 
