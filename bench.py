@@ -210,13 +210,15 @@ STATIC_BMM = (128, 512, 513, 2048, 2049)
 def static_ratio(nb, reps=10, iters=3):
     """The "vs static shape" half of the metric (fig:sym-codegen): the SAME kernel
     source with the symbolic extent a run-time value (dense_dyn / bmm_dyn) vs compiled in
-    (dense_static / bmm_static), default dispatch rule for both (tuned schedules off while
-    measuring), device time per launch from CUDA-graph replays of `reps` launches."""
+    (dense_static / bmm_static), the default family-1/3 rule for both (the twins are family-1/3
+    kernels: where the default rule would pick the weight-streaming family 4, the symbolic
+    family-1 kernel is selected with the default rule's (t, cap) as a schedule), device time
+    per launch from CUDA-graph replays of `reps` launches."""
     import torch
     saved = {}
     for (_, N, K) in STATIC_DENSE:
         saved[(N, K)] = nb.get_dense_schedule(N, K)
-        nb.set_dense_schedule(N, K, 0, 8)
+        nb.set_dense_schedule(N, K, 128, 8 if K >= 2048 else 1)
 
     def tgraph(fn):
         s = torch.cuda.Stream()

@@ -140,7 +140,9 @@ int nimble_last_dispatch(nimble_dispatch *out);
  * dt = NIMBLE_F32: fp32 in/out, CUDA-core FFMA (SIMT8, t = 8 residue variants).
  * dt = NIMBLE_BF16: bf16 in/out, fp32 accumulation in TMEM (tcgen05 + TMA),
  *      output rounded to bf16 (RNE); rows >= M are never read (TMA bounds) nor
- *      written.  The dynamic extent is never padded.  With M <= 128 and no tuned
+ *      written.  The dynamic extent is never padded.  With N % 8 != 0 the TMA stores of
+ *      families 1 / 3 clip at 16-byte granularity: columns N .. ceil8(N)-1 of an output row
+ *      (inside ldy, which the alignment rule makes >= ceil8(N)) may be overwritten.  With M <= 128 and no tuned
  *      schedule (family 4) the K splits' fp32 partials go through a library workspace
  *      owned by the calling STREAM (a pool of 16 per device, allocated on the stream's first
  *      family-4 launch, in relaxed capture mode inside a graph capture); more than 16

@@ -148,11 +148,28 @@ static int orc_umma_t(int64_t batch, int64_t M, int64_t N, int64_t K, int c, orc
     return orc_umma_t_sched(batch, M, N, K, c, 0, 8, d);
 }
 
-/* family 4, UMMA_WS (DISPATCH.md): a bf16 dense whose symbolic extent fits one token tile
- * (M <= 128) and whose 128-feature tiles fit one wave (ceil(N/128) <= 148) streams W over
- * ceil(N/128) x S CTAs, S = min(ceil(K/64), floor(148 / ceil(N/128)), 16) (at least 1) splits
- * of K (the S splits of a feature tile are one thread-block cluster, at most 16 CTAs).
+/* family 4, UMMA_WS (DISPATCH.md): a bf16 dense without a tuned schedule whose
+ * (feature tile, token tile) units are few streams W over units x S CTAs,
+ * S = min(ceil(K/64), floor(148 / units), 16) (at least 1) splits of K (the S splits of a unit
+ * are one thread-block cluster, at most 16 CTAs); units = ceil(N/128) x ceil(M/128).
+ * Taken when M <= 128 and ceil(N/128) <= 148, or when 128 < M <= 1024, K >= 2048 and S >= 2.
  * The residue split of M is family 1's (t = 128, granule 16, 9 classes). */
+static int64_t orc_ws_splits(int64_t units, int64_t K) {
+    int64_t kblocks = orc_ceil_div(K, 64);
+    int64_t splits = 148 / units;
+    if (splits > kblocks) splits = kblocks;
+    if (splits > 16) splits = 16;
+    if (splits < 1) splits = 1;
+    return splits;
+}
+
+static int orc_ws_taken(int64_t M, int64_t N, int64_t K) {
+    int64_t token_tiles = orc_ceil_div(M, 128), feature_tiles = orc_ceil_div(N, 128);
+    if (token_tiles == 1) return feature_tiles <= 148;
+    if (token_tiles > 8 || K < 2048) return 0;
+    return orc_ws_splits(feature_tiles * token_tiles, K) >= 2;
+}
+
 static int orc_umma_ws(int64_t M, int64_t N, int64_t K, int c, orc_dispatch *d) {
     memset(d, 0, sizeof(*d));
     d->family = 4; d->tile_t = 128; d->granule = 16; d->n_classes = 9;
@@ -161,14 +178,10 @@ static int orc_umma_ws(int64_t M, int64_t N, int64_t K, int c, orc_dispatch *d) 
     d->variant = orc_variant(d->residue_class, 9, c);
     d->umma_m = 128; d->umma_n_full = 128;
     d->umma_n_tail = (d->r == 0) ? 0 : ((d->variant >= 0) ? 16 * d->residue_class : 128);
-    int64_t feature_tiles = orc_ceil_div(N, 128);
-    int64_t kblocks = orc_ceil_div(K, 64);
-    int64_t splits = 148 / feature_tiles;
-    if (splits > kblocks) splits = kblocks;
-    if (splits > 16) splits = 16;                    /* the splits of a tile form one cluster */
-    if (splits < 1) splits = 1;
+    int64_t feature_tiles = orc_ceil_div(N, 128), token_tiles = d->k + (d->r > 0);
+    int64_t splits = orc_ws_splits(feature_tiles * token_tiles, K);
     d->split_k = (int32_t)splits;
-    d->grid[0] = (int32_t)feature_tiles; d->grid[1] = 1; d->grid[2] = (int32_t)splits;
+    d->grid[0] = (int32_t)feature_tiles; d->grid[1] = (int32_t)token_tiles; d->grid[2] = (int32_t)splits;
     d->cluster[0] = 1; d->cluster[1] = 1; d->cluster[2] = 1;
     return ORC_OK;
 }
@@ -190,7 +203,7 @@ int orc_dispatch_dense(int64_t M, int64_t N, int64_t K, int dt, int c, orc_dispa
         return ORC_OK;
     }
     if (dt != 1) return ORC_E_DTYPE;
-    if (M <= 128 && orc_ceil_div(N, 128) <= 148) return orc_umma_ws(M, N, K, c, d);
+    if (orc_ws_taken(M, N, K)) return orc_umma_ws(M, N, K, c, d);
     return orc_umma_t(1, M, N, K, c, d);
 }
 

@@ -280,7 +280,7 @@ struct LnArgs {
 namespace nimble {
 namespace {
 constexpr int kWsSlots = 16;
-constexpr size_t kWsPartElems = (size_t)kNumSMs * 128 * 128;
+constexpr size_t kWsPartElems = (size_t)kNumSMs * 128 * 128;   // <= 148 slabs (units x S <= 148)
 struct WsWorkspace {
     std::mutex mu;
     std::vector<std::pair<cudaStream_t, int>> owner[64];
@@ -326,10 +326,11 @@ int launch_ws(const nimble_dispatch &d, const void *x, int64_t ldx, const void *
     L.p.M = (int32_t)M;
     L.p.N = (int32_t)N;
     L.p.m_tiles = d.grid[0];
+    L.p.n_tiles = d.grid[1];
     L.p.S = d.split_k;
     L.p.kb_total = (int32_t)((K + 63) / 64);
     L.p.n_umma = d.r ? d.umma_n_tail : d.umma_n_full;
-    L.p.n_box = L.p.n_umma;
+    L.p.n_box = d.grid[1] == 1 ? L.p.n_umma : d.umma_n_full;   // one box height for every token tile
     const int kb_max = (L.p.kb_total + L.p.S - 1) / L.p.S;
     L.p.stages = kb_max < 3 ? kb_max : 3;
     L.smem_bytes = ws_smem_bytes(L.p.n_box, L.p.stages);

@@ -115,11 +115,30 @@ int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, 
     return NIMBLE_OK;
 }
 
-// Family 4 (DISPATCH.md): a dense with one token tile (M <= 128) and no tuned schedule streams
-// its weights over one wave of CTAs: 128-feature tiles x S splits of K (one cluster per tile,
-// S <= 16), S a function of (N, K) only.
+// Family 4 (DISPATCH.md): a dense without a tuned schedule whose (feature tile, token tile)
+// units leave most SMs idle streams its weights over one wave of CTAs: units x S splits of K
+// (one cluster per unit, S <= 16), S a function of (N, K, ceil(M / 128)) only.
 constexpr int64_t kWsMaxCluster = 16;            // largest (non-portable) thread-block cluster
-bool ws_applies(int64_t M, int64_t N) { return M <= kUMMA_WS.t && cdiv(N, 128) <= kNumSMs; }
+constexpr int64_t kWsMaxTokenTiles = 8;          // M <= 1024
+
+int64_t ws_split(int64_t units, int64_t K) {
+    int64_t s = kNumSMs / units;                    // one wave of CTAs ...
+    const int64_t kb = cdiv(K, 64);
+    if (s > kb) s = kb;                             // ... each with >= 1 k-block of 64 ...
+    if (s > kWsMaxCluster) s = kWsMaxCluster;       // ... the splits of a unit one cluster
+    return s < 1 ? 1 : s;
+}
+
+// one token tile: whenever the feature tiles fit one wave; 2..8 token tiles: where family 1
+// would split K (K >= 2048) and the split stays >= 2 (fewer than 75 units).  Measured on B200
+// (profiles/r02_ws_sweep.jsonl): at K <= 1024 the 128-token partial exchange costs more than
+// family 1's whole K loop; at K >= 2048 the L2 + cluster-barrier exchange beats family 1's
+// DSMEM split-K by 1.2-2.3x.
+bool ws_applies(int64_t M, int64_t N, int64_t K) {
+    const int64_t n_tiles = cdiv(M, kUMMA_WS.t), m_tiles = cdiv(N, 128);
+    if (n_tiles == 1) return m_tiles <= kNumSMs;
+    return n_tiles <= kWsMaxTokenTiles && K >= 2048 && ws_split(m_tiles * n_tiles, K) >= 2;
+}
 
 int dispatch_umma_ws(int64_t M, int64_t N, int64_t K, nimble_dispatch *d) {
     *d = nimble_dispatch{};
@@ -130,14 +149,10 @@ int dispatch_umma_ws(int64_t M, int64_t N, int64_t K, nimble_dispatch *d) {
     d->umma_n_full = kUMMA_WS.t;
     d->umma_n_tail = d->r == 0 ? 0 : (d->variant < 0 ? kUMMA_WS.t : kUMMA_WS.granule * d->residue_class);
     const int64_t m_tiles = cdiv(N, 128);
-    const int64_t kb = cdiv(K, 64);
-    int64_t s = kNumSMs / m_tiles;                  // one wave of CTAs ...
-    if (s > kb) s = kb;                             // ... each with >= 1 k-block of 64 ...
-    if (s > kWsMaxCluster) s = kWsMaxCluster;       // ... the splits of a tile one cluster
-    if (s < 1) s = 1;
-    d->split_k = static_cast<int32_t>(s);
+    const int64_t n_tiles = d->k + (d->r ? 1 : 0);
+    d->split_k = static_cast<int32_t>(ws_split(m_tiles * n_tiles, K));
     d->grid[0] = static_cast<int32_t>(m_tiles);
-    d->grid[1] = 1;
+    d->grid[1] = static_cast<int32_t>(n_tiles);
     d->grid[2] = d->split_k;
     d->cluster[0] = d->cluster[1] = d->cluster[2] = 1;
     return NIMBLE_OK;
@@ -146,7 +161,7 @@ int dispatch_umma_ws(int64_t M, int64_t N, int64_t K, nimble_dispatch *d) {
 int dispatch_dense_bf16(int64_t M, int64_t N, int64_t K, nimble_dispatch *d) {
     int32_t t, cap;
     dense_schedule(N, K, &t, &cap);
-    if (t == 0 && ws_applies(M, N)) return dispatch_umma_ws(M, N, K, d);
+    if (t == 0 && ws_applies(M, N, K)) return dispatch_umma_ws(M, N, K, d);
     return dispatch_umma_t(1, M, N, K, d, t, cap);
 }
 

@@ -101,20 +101,22 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 }
 int umma_max_stages(int box_n, int b_mn_major, int kd);
 
-// Weight-streaming dense (family 4, DISPATCH.md): M <= 128 tokens, grid = S x m_tiles CTAs, the
-// S K-splits of a feature tile one cluster; fp32 partial slabs reduced in split order via L2.
+// Weight-streaming dense (family 4, DISPATCH.md): few (feature tile, token tile) units, grid =
+// S x m_tiles x n_tiles CTAs, the S K-splits of a unit one cluster; fp32 partial slabs reduced in
+// split order via L2.
 struct WsParams {
-    int32_t M, N;            // tokens (symbolic, <= 128), output features
+    int32_t M, N;            // tokens (symbolic), output features
     int32_t m_tiles, S;      // 128-feature tiles x K splits (cluster size S <= 16)
+    int32_t n_tiles;         // 128-token tiles (the last one of width n_umma)
     int32_t kb_total;        // ceil(K / 64)
-    int32_t n_umma;          // UMMA N of the token tile (16 ceil(M/16), or 128 for the fallback)
-    int32_t n_box;           // token rows per TMA box / partial slab row count (= n_umma)
+    int32_t n_umma;          // UMMA N of the last token tile (residue width, or 128 for the fallback)
+    int32_t n_box;           // token rows per TMA box / partial slab row count
     int32_t stages;          // smem ring depth (weights of the first `stages` k-blocks prefetched)
     float alpha;
     const float *bias;
     const __nv_bfloat16 *res; int64_t ld_res;
     __nv_bfloat16 *out; int64_t ld_out;
-    float *part;             // [m_tiles][S][n_box][128] fp32 partial slabs (workspace)
+    float *part;             // [n_tiles][m_tiles][S][n_box][128] fp32 partial slabs (workspace)
     unsigned long long *trace;   // debug (nimble_debug_trace): per CTA 8 globaltimer stamps, NULL = off
 };
 struct WsLaunch {

@@ -1,21 +1,22 @@
-// Weight-streaming tcgen05 dense for the single-token-tile regime (DISPATCH.md family 4:
-// bf16 dense_dyn with the symbolic extent M <= 128, Nimble §3.5 residue dispatch
-// PAPER.md:383-390).  At M <= 128 the operator is a weight stream: every weight byte is read
-// once and feeds at most 128 tokens, so the kernel spreads W over most SMs instead of one CTA
-// per 128-feature tile.
+// Weight-streaming tcgen05 dense for few (feature tile, token tile) units (DISPATCH.md
+// family 4: bf16 dense_dyn with M <= 128, or M <= 1024 where the tiles leave most SMs idle;
+// Nimble §3.5 residue dispatch PAPER.md:383-390).  With few tiles every weight byte feeds few
+// tokens and one CTA per tile would use a handful of SMs, so the kernel splits K over S CTAs
+// per tile and spreads the weight stream over most SMs.
 //
-// Grid = S x m_tiles CTAs; the S CTAs of a 128-feature tile form one thread-block cluster
-// along K (S <= 16).  CTA (q, mt) owns weight rows [128 mt, 128 mt + 128) and the k-blocks
-// [q kb / S, (q+1) kb / S) (S depends on (N, K) only, so a token's result does not depend on
-// M: dynamic M == pad-then-slice, bit for bit).
+// Grid = S x m_tiles x n_tiles CTAs; the S CTAs of a (feature tile, token tile) unit form one
+// thread-block cluster along K (S <= 16).  CTA (q, mt, nt) owns weight rows [128 mt, +128),
+// tokens [128 nt, +128) and the k-blocks [q kb / S, (q+1) kb / S) (S depends on (N, K) and
+// the token-tile count only, so a token's result is the same for M and for M padded to a
+// multiple of 128: dynamic M == pad-then-slice, bit for bit).
 //   warp 0 lane 0  TMA producer: the CTA's weight k-blocks are requested BEFORE the PDL
 //                  grid-dependency wait (they overlap the previous kernel), the token
 //                  k-blocks after it; rows >= M are zero-filled by TMA bounds.
-//   warp 1         TMEM allocation; lane 0 issues tcgen05.mma (M = 128, N = 16 ceil(M/16):
-//                  the residue variant's width, or 128 for the fallback) into one fp32
-//                  accumulator.
+//   warp 1         TMEM allocation; lane 0 issues tcgen05.mma (M = 128, N = 128, or on the
+//                  last token tile the residue variant's width 16 ceil(r/16) / 128 for the
+//                  fallback) into one fp32 accumulator.
 //   all 8 warps    drain TMEM (warp w: lane quarter w % 4, token half w / 4) into this CTA's
-//                  fp32 partial slab part[mt][q][token][128] in L2 (128-B warp stores), one
+//                  fp32 partial slab part[nt][mt][q][token][128] in L2 (128-B warp stores), one
 //                  cluster barrier (release / acquire at cluster
 //                  scope: ~0.1 us, where a global-memory flag barrier measured ~2 us on B200,
 //                  scripts/exp/pdl_floor.cu), then CTA q reduces tokens j = q, q + S, ...: a
@@ -65,7 +66,11 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
     const uint32_t lane = ptx::lane_id();
     const int q = (int)blockIdx.x;                // rank in the K-split cluster
     const int mt = (int)blockIdx.y;               // 128-feature tile
+    const int nt = (int)blockIdx.z;               // 128-token tile
     const int S = p.S;
+    const int tok0 = nt * 128;
+    const int Mt = min(128, p.M - tok0);          // valid tokens of this token tile
+    const uint32_t n_this = (nt == p.n_tiles - 1) ? (uint32_t)p.n_umma : 128u;   // residue width on the tail tile
     const int kb0 = (int)((int64_t)q * p.kb_total / S);
     const int kb1 = (int)((int64_t)(q + 1) * p.kb_total / S);
     const int nkb = kb1 - kb0;
@@ -102,17 +107,17 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
         ptx::pdl_wait();
         if (tr) ts2 = ptx::globaltimer();
         for (int i = 0; i < pre; ++i)
-            ptx::tma_load_3d(smem + i * stage_bytes + kAB, &tmB, &full[i], (kb0 + i) * kBK, 0, 0);
+            ptx::tma_load_3d(smem + i * stage_bytes + kAB, &tmB, &full[i], (kb0 + i) * kBK, tok0, 0);
         for (int i = pre; i < nkb; ++i) {
             const int s = i % p.stages;
             ptx::mbar_wait(&empty[s], (uint32_t)(((i / p.stages) & 1) ^ 1));
             ptx::mbar_arrive_expect_tx_relaxed(&full[s], (uint32_t)stage_bytes);
             ptx::tma_load_3d(smem + s * stage_bytes, &tmA, &full[s], (kb0 + i) * kBK, mt * 128, 0);
-            ptx::tma_load_3d(smem + s * stage_bytes + kAB, &tmB, &full[s], (kb0 + i) * kBK, 0, 0);
+            ptx::tma_load_3d(smem + s * stage_bytes + kAB, &tmB, &full[s], (kb0 + i) * kBK, tok0, 0);
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer
-        const uint32_t idesc = ptx::idesc_bf16(128u, (uint32_t)p.n_umma, 0u);
+        const uint32_t idesc = ptx::idesc_bf16(128u, n_this, 0u);
         for (int i = 0; i < nkb; ++i) {
             const int s = i % p.stages;
             ptx::mbar_wait(&full[s], (uint32_t)((i / p.stages) & 1));
@@ -134,7 +139,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
     // store of one token covers 32 consecutive features (128 B).  (Transposing through shared
     // memory for 16-B stores measured slower: scripts/gpu_probe6.sh, NIMBLE_WS_FLAGS history.)
     const size_t slab = (size_t)p.n_box * 128;                  // floats per (tile, split) slab
-    float *part_tile = p.part + (size_t)mt * S * slab;
+    float *part_tile = p.part + ((size_t)nt * p.m_tiles + mt) * S * slab;
     {
         ptx::mbar_wait(tfull, 0);
         ptx::tc_fence_after();
@@ -142,12 +147,12 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
         const int quarter = (int)(warp & 3), half = (int)(warp >> 2);
         const int f = quarter * 32 + (int)lane;
         float *mine = part_tile + (size_t)q * slab;
-        for (int c0 = half * 16; c0 < p.M; c0 += 32) {
+        for (int c0 = half * 16; c0 < Mt; c0 += 32) {
             float v[16];
             ptx::tmem_ld16(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                if (c0 + j < p.M) __stcg(mine + (size_t)(c0 + j) * 128 + f, v[j]);
+                if (c0 + j < Mt) __stcg(mine + (size_t)(c0 + j) * 128 + f, v[j]);
         }
         ptx::tc_fence_before();
     }
@@ -164,11 +169,12 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
     // ---- reduction over the S splits of this tile (fixed order 0..S-1) + epilogue.  CTA q owns
     // tokens q, q + S, ...; its threads take (token, 4-feature quad) items and issue every
     // split's load of an item before summing (one L2 round trip per item).
-    const int n_tok = p.M > q ? (p.M - q + S - 1) / S : 0;
+    const int n_tok = Mt > q ? (Mt - q + S - 1) / S : 0;
     const int items = n_tok * 32;
     for (int it = (int)threadIdx.x; it < items; it += kWsThreads) {
-        const int j = q + S * (it >> 5), l = it & 31;
-        const float *src = part_tile + (size_t)j * 128 + 4 * l;
+        const int jl = q + S * (it >> 5), l = it & 31;
+        const float *src = part_tile + (size_t)jl * 128 + 4 * l;
+        const int j = tok0 + jl;                          // output row
         float4 v[kWsMaxSplit];
 #pragma unroll
         for (int u = 0; u < kWsMaxSplit; ++u)
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
         }
     }
     if (tr && threadIdx.x == 0) {
-        unsigned long long *t = p.trace + ((size_t)mt * S + q) * 8;
+        unsigned long long *t = p.trace + (((size_t)nt * p.m_tiles + mt) * S + q) * 8;
         t[0] = ts0; t[1] = ts1; t[2] = ts2; t[3] = ts3; t[4] = ts4; t[5] = ts5; t[6] = ptx::globaltimer();
     }
 }
@@ -210,7 +216,7 @@ cudaError_t launch_ws_t(const WsLaunch &L) {
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)L.p.S, (unsigned)L.p.m_tiles, 1);
+    cfg.gridDim = dim3((unsigned)L.p.S, (unsigned)L.p.m_tiles, (unsigned)L.p.n_tiles);
     cfg.blockDim = dim3(kWsThreads, 1, 1);
     cfg.dynamicSmemBytes = L.smem_bytes;
     cfg.stream = L.stream;

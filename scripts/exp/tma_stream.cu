@@ -25,6 +25,8 @@ struct P {
     int stages, boxes, nprod, iters, box_rows, kd, rows_total, kblocks;
     long long *out;
     int csize;           // > 1: cluster of csize CTAs; box b is issued by rank b % csize, multicast to all
+    int mode;            // 0 tensor / try_wait, 1 consumer test_wait spin, 2 1-D cp.async.bulk, 3 no L2 promotion
+    const uint8_t *g;
 };
 __device__ __forceinline__ uint32_t ctarank() { uint32_t r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r; }
 
@@ -39,7 +41,7 @@ __global__ void __launch_bounds__(256, 1) stream(const __grid_constant__ CUtenso
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm) : "memory");
         for (int s = 0; s < p.stages; ++s) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[s])), "r"(p.nprod));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[s])), "r"(p.mode == 5 ? 1 : p.nprod));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&empty[s])), "r"(p.csize));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -56,10 +58,11 @@ __global__ void __launch_bounds__(256, 1) stream(const __grid_constant__ CUtenso
         for (int b = w; b < p.boxes; b += p.nprod) ++nb;
         for (int it = 0; it < p.iters; ++it) {
             const int s = it % p.stages;
+            if (p.mode == 5 && (it % p.nprod) != w) continue;     // producer w owns stages w, w + nprod, ...
             if (it >= p.stages) wait(&empty[s], ((it / p.stages) & 1) ^ 1);
             // every CTA's full barrier expects the whole stage (multicast boxes land from peers)
             asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])),
-                         "r"(p.csize > 1 ? (w == 0 ? p.boxes * box_bytes : 0) : nb * box_bytes) : "memory");
+                         "r"(p.mode == 5 ? p.boxes * box_bytes : (p.csize > 1 ? (w == 0 ? p.boxes * box_bytes : 0) : nb * box_bytes)) : "memory");
             const int kb = (it * p.kd) % p.kblocks;
             if (p.csize > 1) {
                 for (int b = w; b < p.boxes; b += p.nprod) {
@@ -72,10 +75,14 @@ __global__ void __launch_bounds__(256, 1) stream(const __grid_constant__ CUtenso
                 }
                 continue;
             }
-            for (int b = w; b < p.boxes; b += p.nprod) {
+            for (int b = (p.mode == 5 ? 0 : w); b < p.boxes; b += (p.mode == 5 ? 1 : p.nprod)) {
                 uint8_t *dst = sm + s * stage_bytes + b * box_bytes;
                 const int r = row0 + b * p.box_rows;
-                if (p.kd > 1)
+                if (p.mode == 2) {
+                    const uint8_t *src = p.g + ((size_t)r * 2048 + (size_t)kb * box_bytes) % ((size_t)p.rows_total * 2048 - box_bytes);
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                 ::"r"(su32(dst)), "l"((uint64_t)src), "r"(box_bytes), "r"(su32(&full[s])) : "memory");
+                } else if (p.kd > 1)
                     asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
                                  ::"r"(su32(dst)), "l"((uint64_t)&tm), "r"(su32(&full[s])), "r"(0), "r"(r), "r"(kb) : "memory");
                 else
@@ -86,7 +93,11 @@ __global__ void __launch_bounds__(256, 1) stream(const __grid_constant__ CUtenso
     } else if (warp == 1 && lane == 0) {
         for (int it = 0; it < p.iters; ++it) {
             const int s = it % p.stages;
-            wait(&full[s], (it / p.stages) & 1);
+            if (p.mode == 1) {
+                asm volatile("{\n.reg .pred p;\nW1: mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W1;\n}" ::"r"(su32(&full[s])), "r"((it / p.stages) & 1) : "memory");
+            } else {
+                wait(&full[s], (it / p.stages) & 1);
+            }
             if (p.csize > 1) {
                 for (int c = 0; c < p.csize; ++c) {     // release the stage in every CTA of the cluster
                     uint32_t a;
@@ -116,8 +127,16 @@ int main() {
     CK(cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
     CK(cudaMemset(out, 0, 148 * 8));
     printf("box_rows kd box_KB boxes stage_KB stages ring_KB nprod | B/clk/SM med (min)\n");
-    struct C { int box_rows, kd, boxes, stages, nprod, csize = 1; };
+    struct C { int box_rows, kd, boxes, stages, nprod, csize = 1, mode = 0; };
     std::vector<C> cs = {
+        {128, 1, 1, 12, 2, 1, 5}, {128, 1, 1, 12, 4, 1, 5}, {128, 1, 2, 6, 2, 1, 5}, {128, 1, 2, 6, 3, 1, 5},
+        {128, 2, 2, 3, 3, 1, 5},
+        {128, 1, 1, 12, 1, 1, 4}, {128, 1, 2, 6, 1, 1, 4}, {128, 2, 2, 3, 1, 1, 4}, {128, 2, 1, 6, 1, 1, 4},
+        {128, 1, 1, 12, 1, 1, 0}, {128, 1, 1, 12, 1, 1, 1}, {128, 1, 1, 12, 1, 1, 2}, {128, 1, 1, 12, 1, 1, 3},
+        {128, 1, 2, 6, 1, 1, 0}, {128, 1, 2, 6, 1, 1, 1}, {128, 1, 2, 6, 1, 1, 2}, {128, 1, 2, 6, 1, 1, 3},
+        {128, 1, 4, 3, 1, 1, 2}, {128, 2, 2, 3, 1, 1, 3},
+        {128, 1, 1, 12, 1}, {128, 1, 1, 6, 1}, {128, 1, 1, 3, 1}, {64, 1, 1, 12, 1},   // 16 / 8 KB stages
+        {64, 1, 2, 6, 1}, {128, 1, 2, 3, 1},                                          // 16 / 32 KB, shallow
         {128, 2, 2, 3, 2, 2}, {128, 1, 4, 3, 2, 2}, {128, 1, 4, 3, 2, 4}, {128, 2, 4, 1, 2, 4},
         {128, 1, 2, 6, 2, 2}, {128, 2, 2, 2, 2, 2},
         {128, 1, 3, 4, 2}, {128, 3, 1, 4, 1},            // 48 KB stages
@@ -136,16 +155,21 @@ int main() {
         CUtensorMap tm;
         cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64)};
         cuuint64_t strides[2] = {(cuuint64_t)cols * 2, 128};
+        if (c.mode == 4) {            // contiguous: row r of k-block kb at (kb * rows + r) * 128 B
+            strides[0] = 128;
+            strides[1] = (cuuint64_t)rows * 128;
+        }
         cuuint32_t box[3] = {64, (cuuint32_t)c.box_rows, (cuuint32_t)c.kd}, es[3] = {1, 1, 1};
         if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+                CU_TENSOR_MAP_SWIZZLE_128B, c.mode == 3 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
             printf("encode failed\n");
             continue;
         }
         const int box_bytes = c.box_rows * 128 * c.kd, stage_bytes = box_bytes * c.boxes;
         const size_t smem = 1024 + (size_t)c.stages * stage_bytes + 256;
         if (smem > 232448) { printf("skip (smem)\n"); continue; }
-        P p{c.stages, c.boxes, c.nprod, 1024, c.box_rows, c.kd, rows, cols / 64, out, c.csize};
+        P p{c.stages, c.boxes, c.nprod, 1024, c.box_rows, c.kd, rows, cols / 64, out, c.csize, c.mode, (const uint8_t *)buf};
         const int grid = 148 / c.csize * c.csize;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
@@ -164,6 +188,7 @@ int main() {
         const double bytes = (double)p.iters * stage_bytes;
         printf("%8d %2d %6d %5d %8d %6d %7d %5d | %6.1f (%6.1f)\n", c.box_rows, c.kd, box_bytes / 1024, c.boxes,
                stage_bytes / 1024, c.stages, c.stages * stage_bytes / 1024, c.nprod, bytes / h[grid / 2], bytes / h[grid - 1]);
+        printf("        mode %d\n", c.mode);
         if (c.csize > 1) printf("        (cluster %d, multicast: L2 reads per SM = %.1f B/clk)\n", c.csize, bytes / c.csize / h[grid / 2]);
     }
     return 0;

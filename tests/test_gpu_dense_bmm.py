@@ -249,14 +249,13 @@ def test_bmm_integer_exact(nb, orc):
 # ------------------------------------------------------------------ static twins
 def test_static_twin_bitwise_equal(nb, orc):
     # the static-shape instantiation computes exactly what the symbolic kernel computes.  The
-    # twins are family-1/3 kernels; at M <= 128 the default rule picks family 4, so there the
-    # symbolic family-1 kernel is selected with the default rule's (t, cap) as a schedule.
+    # twins are family-1/3 kernels; where the default rule picks family 4 the symbolic family-1
+    # kernel is selected with the default rule's (t, cap) as a schedule.
     for (M, N, K) in ((128, 3072, 1024), (527, 3072, 1024), (513, 1024, 4096), (128, 768, 3072)):
         W = synth.normal((N, K), 0.05, 3 + M)
         b = synth.normal((N,), 0.1, 4 + M, torch.float32)
         x = synth.normal((M, K), 1.0, 5 + M)
-        if M <= 128:
-            nb.set_dense_schedule(N, K, 128, 8 if K >= 2048 else 1)
+        nb.set_dense_schedule(N, K, 128, 8 if K >= 2048 else 1)
         try:
             y1 = _dense_gpu(nb, x, W, b, nb.EPI_BIAS)
             assert nb.last_dispatch()["family"] in (1, 3)

@@ -133,12 +133,11 @@ def test_dispatch_invariants(orc, dt):
                 else:
                     assert d["umma_n_tail"] == t
             if dt == 1 and M <= 128:
-                # family 4 (weight streaming): 8 feature tiles x S splits of the 16 k-blocks,
-                # one wave (8 S <= 148), no cluster; S does not depend on M
+                # family 4 (weight streaming): 8 feature tiles x 1 token tile x S splits of the
+                # 16 k-blocks, one wave (8 S <= 148), no cluster record; S does not depend on M
                 s = d["split_k"]
                 assert d["family"] == 4 and d["umma_m"] == 128 and list(d["cluster"]) == [1, 1, 1]
-                assert list(d["grid"]) == [8, 1, s] and 8 * s <= 148 and 1 <= s <= 16
-                assert s == 16                                     # min(16 k-blocks, 148 // 8)
+                assert list(d["grid"]) == [8, 1, s] and s == 16            # min(16 k-blocks, 148 // 8, 16)
             elif dt == 1:
                 s = d["split_k"]
                 assert s in (1, 2, 4, 8) and d["cluster"] == ((1 if M < 2048 else 2), 1, s)
@@ -185,7 +184,19 @@ def test_dispatch_weight_streaming_family(orc):
             d1 = orc.dispatch_dense(M, N, K, 1, 0, 128, 1)[1]      # family 1 with the same t
             for key in ("k", "r", "residue_class", "variant", "umma_n_full", "umma_n_tail", "n_classes"):
                 assert d[key] == d1[key], key
-        assert orc.dispatch_dense(129, N, K, 1)[1]["family"] == 1
+    # several token tiles (M <= 1024): family 4 only at K >= 2048 and while the split stays >= 2
+    # (fewer than 75 units), with S = min(k-blocks, 148 // units, 16); the same S for M and M
+    # padded to 128 k
+    for (N, K, M, fam, S) in [(2304, 768, 129, 1, 1), (3072, 1024, 129, 1, 1), (4096, 2048, 200, 4, 2),
+                              (4096, 2048, 300, 1, 1), (1024, 4096, 1024, 4, 2), (1024, 4096, 1025, 1, 1),
+                              (1024, 4096, 513, 4, 3), (768, 3072, 1000, 4, 3), (3072, 3072, 384, 4, 2),
+                              (3072, 3072, 512, 1, 1), (1024, 1024, 513, 1, 1)]:
+        d = orc.dispatch_dense(M, N, K, 1)[1]
+        assert d["family"] == fam, (N, K, M, d)
+        if fam == 4:
+            Mp = 128 * -(-M // 128)
+            assert d["split_k"] == S and list(d["grid"]) == [-(-N // 128), -(-M // 128), S]
+            assert orc.dispatch_dense(Mp, N, K, 1)[1]["split_k"] == S
     # more feature tiles than one wave: family 1
     assert orc.dispatch_dense(5, 149 * 128, 256, 1)[1]["family"] == 1
     assert orc.dispatch_dense(5, 148 * 128, 256, 1)[1]["family"] == 4
@@ -215,7 +226,7 @@ def test_oracle_tuned_schedule_invariants(orc, tile_t, split_max):
         assert s in (1, 2, 4, 8) and s <= split_max and (s == 1 or m_tiles * n_tiles * s <= 148)
         assert tile_t <= 128 or s == 1
         assert d["grid"][2] == s and list(d["cluster"]) == [1, 1, s]
-        if tile_t == 128 and split_max == (8 if K >= 2048 else 1) and M > 128:
+        if tile_t == 128 and split_max == (8 if K >= 2048 else 1) and orc.dispatch_dense(M, N, K, 1)[1]["family"] != 4:
             assert d == orc.dispatch_dense(M, N, K, 1)[1]     # the default rule's (t, cap)
     for M in (2048, 5000):
         assert orc.dispatch_dense(M, N, K, 1, 0, tile_t, split_max)[1] == orc.dispatch_dense(M, N, K, 1)[1]
