@@ -51,6 +51,7 @@ constexpr int kRedBytes = 4 * 256 * 4;    // [2 parity][2 halves][128] row max +
 constexpr int kListBytes = (2 * kMaxReq * 4 + kMaxReq * 2 + 2 * (kMaxQT + 1) * 4 + 1023) / 1024 * 1024;
 constexpr int kSmemBytes = 1024 + 6 * kTile + kRedBytes + kListBytes + 512;   // + barriers, 2 map scratches
 constexpr int kCtasPerSm = 2;
+constexpr uint32_t kPCol = 192;           // TMEM column of P_j (128 x 128 bf16 = 64 columns)
 
 // TMA maps of the output with boxes of 64, 32, 16 and 8 rows: a partial query tile's valid
 // rows leave as a 64/32/16/8-row decomposition (starting rows stay multiples of 8, so every
@@ -85,6 +86,28 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
         : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 32 lanes x 32 consecutive columns (lane i of the warp -> TMEM lane base + i)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem]: A is a 128 x 16 bf16 tile in TMEM (lane = row, two k per
+// 32-bit column: 8 columns), B the usual shared-memory descriptor
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 
 using ptx::fadd2;
 using ptx::ffma2;
@@ -278,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;             // S: cols [0,128), O: cols [128,192)
+    const uint32_t tmem = *tmem_slot;             // S: cols [0,128), O: [128,192), P (bf16 pairs): [192,256)
     const int n_items = cum[R];
 
     // device token count (nimble_attention_varlen_dev): T = seq_off[R] is data, so this CTA
@@ -379,12 +402,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 ATT_TRACE(npv, 7);
 #pragma unroll
                 for (int kb = 0; kb < 2; ++kb) {
-                    const uint64_t pd = ptx::smem_desc_sw128(ptx::smem_u32(sP + kb * kTile), 0, 1024);
                     const uint64_t vd = ptx::smem_desc_sw128(ptx::smem_u32(sV + st * kTile + kb * kVBox), 8192, 1024);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        ptx::umma_bf16(tmem + 128, pd + (uint64_t)(kk * 2), vd + (uint64_t)(kk * 128), idesc_o,
-                                       (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < 4; ++kk)            // P_j in TMEM cols [192, 256): 16 keys = 8 cols
+                        umma_bf16_ts(tmem + 128, tmem + kPCol + (uint32_t)(8 * (4 * kb + kk)), vd + (uint64_t)(kk * 128),
+                                     idesc_o, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
                 }
                 ptx::umma_commit(pv_done);
                 ptx::umma_commit(&v_empty[st]);
@@ -511,17 +533,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 ptx::tc_fence_after();
             }
             if (tr) ATT_TRACE(tb, 4);
-            // P_j: this warp group's 64 keys = one K-major 128-B-swizzled atom column block
-            uint8_t *rowp = sP + half * kTile + q * 128;
+            // P_j as bf16 pairs into TMEM (the A operand of P.V): this row's 64 keys of the block half
+            // are 32 columns of lane q, keys (2c, 2c+1) in column c
+            {
+                uint32_t pw[32];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                uint32_t w[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    __nv_bfloat162 h2 = __floats2bfloat162_rn(v[c * 8 + 2 * e], v[c * 8 + 2 * e + 1]);
-                    w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                for (int c = 0; c < 32; ++c) {
+                    __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * c], v[2 * c + 1]);
+                    pw[c] = *reinterpret_cast<uint32_t *>(&h2);
                 }
-                *reinterpret_cast<uint4 *>(rowp + ((c ^ (q & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+                tmem_st32(trow + kPCol + (uint32_t)(half * 32), pw);
             }
             // rescale this row's O half (32 of the 64 output columns) when the running max grew
             if (j > 0 && __any_sync(0xffffffffu, grow)) {
@@ -536,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 }
                 tmem_st_wait();
             }
-            ptx::fence_async_smem();                  // P (generic stores) -> tensor-core reads
+            tmem_st_wait();                           // P (tcgen05.st) complete before the MMA reads it
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(p_ready);
