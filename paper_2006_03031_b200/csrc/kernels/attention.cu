@@ -224,7 +224,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const int R = p.R, H = p.heads;
     unsigned long long *trace = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
     const unsigned long long t_start = p.trace ? ptx::globaltimer() : 0ull;   // per-CTA span (debug)
-#define ATT_TRACE(blk, ev) do { if (trace && (blk) < 512) trace[(blk) * 8 + (ev)] = clock64(); } while (0)
+    // debug timeline of CTA 0 (nimble_debug_trace): clock64 stamps kept in shared memory (the upper
+    // half of the P buffer; the O staging uses the lower 16 KB) and copied out at the end, so the
+    // trace adds no global stores (and no release-arrive waiting for them) on the hot path.
+    // Slots: blocks 0-63, producer 256+n, MMA items 384+i, softmax items 448+i (n, i < 64).
+    unsigned long long *strace = reinterpret_cast<unsigned long long *>(sP + 16384);
+    auto trace_slot = [](int blk) { return blk < 64 ? blk : blk < 256 ? -1 : blk < 320 ? blk - 192 : blk < 384 ? -1
+                                         : blk < 448 ? blk - 256 : blk < 512 ? blk - 256 : -1; };
+#define ATT_TRACE(blk, ev) do { if (trace) { const int sl_ = trace_slot(blk); if (sl_ >= 0) strace[sl_ * 8 + (ev)] = clock64(); } } while (0)
 
     if (threadIdx.x == 0) {
         ptx::prefetch_tmap(&tmQK);
@@ -247,6 +254,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         ptx::fence_async_smem();
     }
     if (warp == 8) ptx::tmem_alloc(tmem_slot, 256);
+    if (trace)
+        for (int i = threadIdx.x; i < 256 * 8; i += kThreads) strace[i] = 0ull;
     for (int i = threadIdx.x; i <= kMaxQT; i += kThreads) cnt[i] = 0;
     ptx::pdl_wait();                              // QKV and seq_off come from earlier work
     ptx::pdl_trigger();
@@ -641,6 +650,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, 256);
     }
+    if (trace)                                        // CTA 0's timeline -> the global trace buffer
+        for (int i = threadIdx.x; i < 256 * 8; i += kThreads) {
+            const int sl = i >> 3, blk = sl < 64 ? sl : sl < 128 ? sl + 192 : sl + 256;
+            trace[blk * 8 + (i & 7)] = strace[i];
+        }
     if (p.trace && threadIdx.x == 0) {                // per-CTA span (scripts/attn_balance.py)
         p.trace[8192 + 2 * blockIdx.x] = t_start;
         p.trace[8192 + 2 * blockIdx.x + 1] = ptx::globaltimer();
