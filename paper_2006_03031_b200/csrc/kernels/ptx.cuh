@@ -222,7 +222,8 @@ __device__ __forceinline__ float gelu_erf(float z) { return 0.5f * z * (1.0f + e
 //   * 1/sqrt2 is folded into the coefficients (b_i = a_i 2^(-i/2)),
 //   * the 1/2 of Phi is folded in too: scaling p by 2^(1/16) gives h = p^-16 = (1 - erf) / 2,
 //   * Phi = 1 - h (z >= 0) or h (z < 0), so z Phi = max(z, 0) - |z h| with no select,
-//   * p^-16 = ex2(-16 lg2 p) (lg2/ex2.approx relative error ~2^-22, x16 -> ~4e-6 relative on h).
+//   * p^-16 = rcp(p)^16 (rcp.approx relative error ~2^-23, x16 -> ~2e-6 relative on h; the
+//     former ex2(-16 lg2 p) form, NIMBLE_GELU_LG2EX2, costs two MUFU per value).
 __device__ __forceinline__ float gelu_erf(float z) {
     const float q = fabsf(z);
     float p = fmaf(5.621299664e-06f, q, 5.105520901e-05f);
@@ -231,8 +232,8 @@ __device__ __forceinline__ float gelu_erf(float z) {
     p = fmaf(p, q, 2.207699846e-02f);
     p = fmaf(p, q, 5.207516304e-02f);
     p = fmaf(p, q, 1.044273782e+00f);
-#ifdef NIMBLE_GELU_RCP
-    float h = rcp_approx(p);
+#ifndef NIMBLE_GELU_LG2EX2
+    float h = rcp_approx(p);                         // p^-16 = rcp(p)^16: one MUFU + four squarings
     h *= h; h *= h; h *= h; h *= h;                  // 2^-1 (1 + sum a_i x^i)^-16
 #else
     float h;                                         // p^-16 = 2^(-16 log2 p): 3 instructions, 2 MUFU
@@ -287,11 +288,29 @@ __device__ __forceinline__ float2 gelu_erf2(float2 z) {
     p = ffma2(p, q, f2(5.207516304e-02f));
     p = ffma2(p, q, f2(1.044273782e+00f));
     float2 h;
+#if defined(NIMBLE_GELU_NR)                          // experiment: measured 4 % slower (FMA issue)
+    // 1/p without MUFU: magic-constant estimate (|rel err| < 0.125 for p >= 1) + 3 Newton steps
+    // (rel err ~ 3e-8) on the FMA pipes, then p^-16 by squaring
+    h = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(p.x)), __int_as_float(0x7EF311C3 - __float_as_int(p.y)));
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+        const float2 e = ffma2(make_float2(-p.x, -p.y), h, f2(1.0f));
+        h = ffma2(h, e, h);
+    }
+    h = fmul2(h, h); h = fmul2(h, h); h = fmul2(h, h); h = fmul2(h, h);
+#elif !defined(NIMBLE_GELU_LG2EX2)
+    // one MUFU per value and p^-16 by squaring: half the MUFU traffic of lg2 + ex2, which the
+    // GELU GEMM's main loop felt (stage interval 1278 -> 1149 clk, FFN1 at M = 17448
+    // 123.5 -> 120.6 us, scripts/trace_stages.py); rcp.approx's 2^-23 error x16 stays < 4e-6
+    h = make_float2(rcp_approx(p.x), rcp_approx(p.y));
+    h = fmul2(h, h); h = fmul2(h, h); h = fmul2(h, h); h = fmul2(h, h);
+#else
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(h.x) : "f"(p.x));
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(h.y) : "f"(p.y));
     h = fmul2(h, f2(-16.0f));
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(h.x) : "f"(h.x));
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(h.y) : "f"(h.y));
+#endif
     const float2 w = fmul2(z, h);
     return make_float2(fmaxf(z.x, 0.0f) - fabsf(w.x), fmaxf(z.y, 0.0f) - fabsf(w.y));
 }
