@@ -457,18 +457,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         int nkb_m = 0, ntile_m = 0;                       // debug: k-blocks / tiles consumed (NIMBLE_DBG & 4)
+        bool acc_waited = false;                          // the next tile's accumulator is known free
         WorkItem w;
         NIMBLE_ITEMS(w, it) {
             const int t = w.t;
             const TileCoord c = tile_of(g, t);
             const int n_this = (c.n == g.tiles_n - 1) ? g.n_tail : g.n_full;
             const uint32_t idesc = ptx::idesc_bf16(PAIR ? 256u : 128u, (uint32_t)n_this, B_MN);
-            ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);     // epilogue drained this accumulator
+            if ((p.dbg & 32) && trace && cta_lin == 0 && ntile_m < 24)   // tile start: before / after the accumulator wait
+                reinterpret_cast<long long *>(reinterpret_cast<uint8_t *>(full_bar) + 128)[2 * ntile_m] = clock64();
+            if (!acc_waited) ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);     // epilogue drained this accumulator
+            acc_waited = false;
+            if ((p.dbg & 32) && trace && cta_lin == 0 && ntile_m < 24)
+                reinterpret_cast<long long *>(reinterpret_cast<uint8_t *>(full_bar) + 128)[2 * ntile_m + 1] = clock64();
             if ((p.dbg & 4) && trace && cta_lin == 0 && ntile_m < 256) p.trace[24576 + ntile_m] = clock64();
             ++ntile_m;
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)(acc * g.n_full);
             for (int kb = w.kb_lo; kb < w.kb_hi; kb += kd) {
+                if (kb + kd >= w.kb_hi) {
+                    // before the tile's last stage: wait for the NEXT tile's accumulator (its
+                    // epilogue, two tiles back, is long done) so the next tile's first MMAs follow
+                    // this stage's without a gap at the tile boundary (measured ~500-700 clk idle)
+                    WorkItem wn;
+                    if (work_item(it + 1, t_first, t_step, total_tiles, kb0, kb1, wn)) {
+                        ptx::mbar_wait(&tempty[acc ^ 1], ((acc ^ 1) == 0 ? acc_phase ^ 1u : acc_phase) ^ 1u);
+                        acc_waited = true;
+                    }
+                }
                 ptx::mbar_wait(&full_bar[stage], phase);
                 if ((p.dbg & 32) && trace && cta_lin == 0 && nkb_m < 48)   // smem-resident stamps (no global store)
                     reinterpret_cast<long long *>(reinterpret_cast<uint8_t *>(full_bar) + 640)[nkb_m] = clock64();
@@ -895,8 +911,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         else ptx::tmem_dealloc(tmem_base, tmem_cols);
     }
     if (threadIdx.x == 0) NIMBLE_TRACE(6);
-    if ((p.dbg & 32) && trace && cta_lin == 0 && threadIdx.x < 48)   // NIMBLE_DBG & 32: stage arrivals, CTA 0
+    if ((p.dbg & 32) && trace && cta_lin == 0 && threadIdx.x < 48) {   // NIMBLE_DBG & 32: stage arrivals, CTA 0
         p.trace[8192 + threadIdx.x] = reinterpret_cast<const long long *>(reinterpret_cast<const uint8_t *>(full_bar) + 640)[threadIdx.x];
+        p.trace[8192 + 64 + threadIdx.x] = reinterpret_cast<const long long *>(reinterpret_cast<const uint8_t *>(full_bar) + 128)[threadIdx.x];
+    }
 #undef NIMBLE_TRACE
 }
 

@@ -33,5 +33,10 @@ for shp in (sys.argv[1] if len(sys.argv) > 1 else "17448x3072x1024,17448x4096x10
         kb = (K // 64 + 1) // 2
         print(f"{shp} epi {epi}: {len(t)} stages (tile = {kb} stages); intervals clk: "
               + " ".join("%d" % v for v in d[:40]))
+        ts = buf.cpu().numpy()[8192 + 64:8192 + 64 + 48].astype(np.float64).reshape(-1, 2)
+        for ti in range(1, 4):
+            if ts[ti, 0] > 0 and ti * kb < len(t):
+                print("   tile %d: last stage of previous tile -> acc wait start %+d, acc free %+d, first stage %+d clk"
+                      % (ti, ts[ti, 0] - t[ti * kb - 1], ts[ti, 1] - t[ti * kb - 1], t[ti * kb] - t[ti * kb - 1]))
         within = [d[i] for i in range(len(d)) if (i + 1) % kb]
         print("   within-tile median %.0f  boundary %s" % (np.median(within), [int(d[i]) for i in range(len(d)) if (i + 1) % kb == 0]))
