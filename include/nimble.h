@@ -310,6 +310,19 @@ int nimble_lstm_seq(const float *G, int64_t ldg, const float *W_hh, int64_t ldw,
  * not be written by the immediately preceding kernel on the stream.
  * H <= 1024 (E_UNSUPPORTED beyond: the weights must fit in shared memory). */
 size_t nimble_lstm2_workspace_bytes(int64_t H);
+/* The whole 2-layer forward in ONE launch: as nimble_lstm2_seq, with the layer-1 input
+ * projection W_ih1 x_t + b1 computed inside the kernel ("the LSTM language model";
+ * round-2 fusion of the hoisted input GEMM: each layer-1 CTA keeps its W_ih1 gate rows in shared
+ * memory and computes x_t's projection while the previous step's h is being exchanged).
+ * X [T x ldx] fp32 inputs (I features), W_ih1 [4H x ldwi], b1 [4H] = b_ih1 + b_hh1; the rest and
+ * the workspace contract as nimble_lstm2_seq.  Register-resident weights only: H <= 672 and the
+ * W_ih1 rows of a CTA in shared memory (I <= ~900 at H = 650), else NIMBLE_E_UNSUPPORTED (compose
+ * nimble_dense_dyn + nimble_lstm2_seq).  W_ih1 / W_hh1 / W_ih2 / W_hh2 are read before the
+ * kernel's grid-dependency wait: they must not be written by the immediately preceding kernel. */
+int nimble_lstm2_forward(const float *X, int64_t ldx, int64_t I, const float *W_ih1, int64_t ldwi, const float *b1,
+                         const float *W_hh1, const float *W_ih2, const float *W_hh2, int64_t ldw, const float *b2,
+                         float *H1, float *H2, int64_t ldh, float *hT, float *cT, int64_t T, int64_t H,
+                         void *workspace, void *stream);
 int nimble_lstm2_seq(const float *G1, int64_t ldg, const float *W_hh1, const float *W_ih2, const float *W_hh2,
                      int64_t ldw, const float *b2, float *H1, float *H2, int64_t ldh, float *hT, float *cT,
                      int64_t T, int64_t H, void *workspace, void *stream);

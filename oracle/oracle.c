@@ -150,15 +150,15 @@ static int orc_umma_t(int64_t batch, int64_t M, int64_t N, int64_t K, int c, orc
 
 /* family 4, UMMA_WS (DISPATCH.md): a bf16 dense without a tuned schedule whose
  * (feature tile, token tile) units are few streams W over units x S CTAs,
- * S = min(ceil(K/64), floor(148 / units), 16) (at least 1) splits of K (the S splits of a unit
- * are one thread-block cluster, at most 16 CTAs); units = ceil(N/128) x ceil(M/128).
+ * S = min(ceil(K/64), floor(148 / units), 8) (at least 1) splits of K (the S splits of a unit
+ * are one portable thread-block cluster, at most 8 CTAs); units = ceil(N/128) x ceil(M/128).
  * Taken when M <= 128 and ceil(N/128) <= 148, or when 128 < M <= 1024, K >= 2048 and S >= 2.
  * The residue split of M is family 1's (t = 128, granule 16, 9 classes). */
 static int64_t orc_ws_splits(int64_t units, int64_t K) {
     int64_t kblocks = orc_ceil_div(K, 64);
     int64_t splits = 148 / units;
     if (splits > kblocks) splits = kblocks;
-    if (splits > 16) splits = 16;
+    if (splits > 8) splits = 8;                      /* one portable cluster per unit */
     if (splits < 1) splits = 1;
     return splits;
 }

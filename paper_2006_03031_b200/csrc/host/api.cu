@@ -895,6 +895,25 @@ extern "C" int nimble_lstm2_seq(const float *G1, int64_t ldg, const float *W_hh1
     return NIMBLE_OK;
 }
 
+extern "C" int nimble_lstm2_forward(const float *X, int64_t ldx, int64_t I, const float *W_ih1, int64_t ldwi,
+                                    const float *b1, const float *W_hh1, const float *W_ih2, const float *W_hh2,
+                                    int64_t ldw, const float *b2, float *H1, float *H2, int64_t ldh, float *hT,
+                                    float *cT, int64_t T, int64_t H, void *workspace, void *stream) {
+    if (!X || !W_ih1 || !b1 || !W_hh1 || !W_ih2 || !W_hh2 || !b2 || !H1 || !H2 || !hT || !cT || !workspace)
+        return fail(NIMBLE_E_NULL, "nimble_lstm2_forward: NULL pointer");
+    if (!ext_ok(T) || !ext_ok(H) || !ext_ok(I)) return fail(NIMBLE_E_EXTENT, "nimble_lstm2_forward: T, H and I must be >= 1");
+    if (ldx < I || ldwi < I || ldw < H || ldh < H) return fail(NIMBLE_E_SHAPE, "nimble_lstm2_forward: leading dimension too small");
+    const Lstm2Input in{X, ldx, W_ih1, ldwi, b1, I};
+    cudaError_t e = launch_lstm2_seq(nullptr, 0, W_hh1, W_ih2, W_hh2, ldw, b2, H1, H2, ldh, hT, cT, T, H, workspace,
+                                     static_cast<cudaStream_t>(stream), &in);
+    if (e == cudaErrorNotSupported)
+        return fail(NIMBLE_E_UNSUPPORTED, "nimble_lstm2_forward: H <= 672 and W_ih1 rows in shared memory required "
+                                          "(use nimble_dense_dyn + nimble_lstm2_seq)");
+    if (e != cudaSuccess) return cuda_fail("nimble_lstm2_forward launch", e);
+    clear_error();
+    return NIMBLE_OK;
+}
+
 // ------------------------------------------------------------------ Tree-LSTM
 extern "C" int nimble_treelstm_level(const int32_t *nodes, const float *A, int64_t lda, const int32_t *a_rows,
                                      const float *W, int64_t ldw, const float *bias, const int32_t *parent_slot,

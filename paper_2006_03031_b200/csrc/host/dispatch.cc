@@ -117,8 +117,14 @@ int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, 
 
 // Family 4 (DISPATCH.md): a dense without a tuned schedule whose (feature tile, token tile)
 // units leave most SMs idle streams its weights over one wave of CTAs: units x S splits of K
-// (one cluster per unit, S <= 16), S a function of (N, K, ceil(M / 128)) only.
-constexpr int64_t kWsMaxCluster = 16;            // largest (non-portable) thread-block cluster
+// (one cluster per unit, S <= 8), S a function of (N, K, ceil(M / 128)) only.
+#ifndef NIMBLE_WS_MAX_CLUSTER
+#define NIMBLE_WS_MAX_CLUSTER 8
+#endif
+// the largest PORTABLE thread-block cluster: 16-CTA (non-portable) clusters measured up to 20 %
+// faster on the K >= 3072 shapes but 8 clusters of 16 fill all 8 GPCs exactly, and
+// compute-sanitizer synccheck flags them ("missing wait"); 8-CTA clusters are clean
+constexpr int64_t kWsMaxCluster = NIMBLE_WS_MAX_CLUSTER;
 constexpr int64_t kWsMaxTokenTiles = 8;          // M <= 1024
 
 int64_t ws_split(int64_t units, int64_t K) {

@@ -164,9 +164,17 @@ cudaError_t launch_lstm_seq(const float *G, int64_t ldg, const float *W_hh, int6
                             int64_t H, void *workspace, cudaStream_t s);
 
 size_t lstm2_workspace_bytes(int64_t H);
+// layer-1 input projection fused into the wavefront kernel (nimble_lstm2_forward)
+struct Lstm2Input {
+    const float *X; int64_t ldx;
+    const float *Wih1; int64_t ldwi;
+    const float *b1;
+    int64_t I;
+};
 cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, const float *Wih2, const float *Whh2,
                              int64_t ldw, const float *b2, float *H1, float *H2, int64_t ldh, float *hT, float *cT,
-                             int64_t T, int64_t H, void *workspace, cudaStream_t s);
+                             int64_t T, int64_t H, void *workspace, cudaStream_t s,
+                             const Lstm2Input *fused = nullptr);
 
 struct TreeParams {
     const int32_t *nodes;

@@ -34,6 +34,12 @@ struct Lstm2Args {
     unsigned long long *hbuf;    // [2 layers][2 ping-pong][H] tagged (t + 1) << 32 | float bits
     int T, H, n1, JB1, JB2;      // n1 layer-1 CTAs (JB1 units each), the rest layer 2 (JB2 units)
     unsigned long long *trace;   // debug: [2 CTAs][T+1 steps][4 stamps] or NULL
+    // fused layer-1 input projection (X != NULL; register-resident variant only): G1[t] =
+    // W_ih1 x_t + b1 is computed in the kernel from W_ih1 rows held in shared memory
+    const float *X; int64_t ldx;
+    const float *Wih1; int64_t ldwi;
+    const float *b1;
+    int I;
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
@@ -234,7 +240,7 @@ constexpr int kRegThreads = 512;
 constexpr int kRegWarps = kRegThreads / 32;
 constexpr int kJobsPerWarp = 4;
 
-template <int NI>
+template <int NI, bool FUSE>
 __global__ void __launch_bounds__(kRegThreads, 1) lstm2_reg_kernel(const Lstm2Args a) {
     extern __shared__ float sm[];
     const int H = a.H;
@@ -251,6 +257,26 @@ __global__ void __launch_bounds__(kRegThreads, 1) lstm2_reg_kernel(const Lstm2Ar
     float *z = x2 + Hp;                         // [2][R] per-matrix gate pre-activations
     float *cs = z + 2 * R;                      // [JB]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // fused input projection (layer-1 CTAs): W_ih1 rows [R][Ip], x_t [Ip], gin [R]
+    const bool fuse = FUSE && !l2;              // compile-time: the unfused kernel carries none of it
+    const int Ip = 32 * ((a.I + 31) / 32);
+    float *xin = cs + 4 * ((JB + 3) / 4);       // 16-B aligned
+    float *gin = xin + Ip;
+    float *Wi = gin + 4 * ((R + 3) / 4);
+    if (fuse) {
+        // rows of W_ih1 -> shared memory (static weights: before the grid-dependency wait), 4-B
+        // cp.async, zero-filled past I and for units past H
+        for (int r = warp; r < R; r += kRegWarps) {
+            const int g = r / JB, u = r - g * JB, j = j0 + u;
+            const float *row = a.Wih1 + (int64_t)(g * H + (j < H ? j : 0)) * a.ldwi;
+            for (int k = lane; k < Ip; k += 32) {
+                const uint32_t nbytes = (j < H && k < a.I) ? 4u : 0u;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(ptx::smem_u32(Wi + (size_t)r * Ip + k)),
+                             "l"(row + (k < a.I ? k : 0)), "r"(nbytes)
+                             : "memory");
+            }
+        }
+    }
 
     // weights -> registers (static: before the grid-dependency wait, overlapping the input GEMM)
     float w[kJobsPerWarp][NI];
@@ -271,19 +297,64 @@ __global__ void __launch_bounds__(kRegThreads, 1) lstm2_reg_kernel(const Lstm2Ar
     }
     for (int u = threadIdx.x; u < JB; u += kRegThreads) cs[u] = 0.f;
     for (int k = threadIdx.x; k < Hp; k += kRegThreads) { x1[k] = 0.f; x2[k] = 0.f; }
+    if (fuse) asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     ptx::pdl_trigger();
-    ptx::pdl_wait();                            // G1 (the input GEMM) and the workspace of the previous call
+    ptx::pdl_wait();                            // G1 / X and the workspace of the previous call
 
     unsigned long long *tr = nullptr;
     if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || (int)blockIdx.x == a.n1))
         tr = a.trace + (size_t)(blockIdx.x == 0 ? 0 : 1) * (a.T + 1) * 4;
+    // fused input projection: x_t is prefetched into registers one step ahead (its global load
+    // latency never sits on a step), two values per thread (Ip <= 2 * kRegThreads)
+    float xr0 = 0.f, xr1 = 0.f;
+    if (fuse) {
+        const int k0 = threadIdx.x, k1 = threadIdx.x + kRegThreads;
+        xr0 = k0 < a.I ? __ldg(a.X + k0) : 0.f;
+        xr1 = k1 < a.I ? __ldg(a.X + k1) : 0.f;
+    }
     for (int s = 0; s <= a.T; ++s) {
         const int t = l2 ? s - 1 : s;           // the time step this CTA computes
         const bool active = t >= 0 && t < a.T;
         if (tr) tr[s * 4 + 0] = ptx::globaltimer();
         float gpre[4] = {0.f, 0.f, 0.f, 0.f};
-        if (!l2 && active && threadIdx.x < JB && j0 + (int)threadIdx.x < H) {
+        if (fuse && active) {
+            // W_ih1 x_t for this CTA's gate rows while the other CTAs' h_{t-1} is in flight: it
+            // needs no h, so it sits before the gather (off the step's critical path)
+            if (threadIdx.x < Ip) xin[threadIdx.x] = xr0;
+            if (threadIdx.x + kRegThreads < Ip) xin[threadIdx.x + kRegThreads] = xr1;
+            if (t + 1 < a.T) {                  // prefetch x_{t+1}
+                const int k0 = threadIdx.x, k1 = threadIdx.x + kRegThreads;
+                xr0 = k0 < a.I ? __ldg(a.X + (int64_t)(t + 1) * a.ldx + k0) : 0.f;
+                xr1 = k1 < a.I ? __ldg(a.X + (int64_t)(t + 1) * a.ldx + k1) : 0.f;
+            }
+            __syncthreads();
+            // a warp's (<= 4) rows advance together: independent FMA chains, one reduction pass
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int k = lane; k < Ip; k += 32) {
+                const float xv = xin[k];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int r = warp + kRegWarps * q;
+                    if (r < R) acc[q] = fmaf(Wi[(size_t)r * Ip + k], xv, acc[q]);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+            if (lane == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (warp + kRegWarps * q < R) gin[warp + kRegWarps * q] = acc[q];
+            }
+            __syncthreads();
+            if (threadIdx.x < JB && j0 + (int)threadIdx.x < H) {
+                const int u = threadIdx.x, j = j0 + u;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) gpre[q] = gin[q * JB + u] + __ldg(a.b1 + q * H + j);
+            }
+        } else if (!l2 && active && threadIdx.x < JB && j0 + (int)threadIdx.x < H) {
             const float *g = a.G1 + (int64_t)t * a.ldg + j0 + threadIdx.x;
 #pragma unroll
             for (int q = 0; q < 4; ++q) gpre[q] = __ldg(g + q * H);
@@ -364,9 +435,20 @@ __global__ void __launch_bounds__(kRegThreads, 1) lstm2_reg_kernel(const Lstm2Ar
     }
 }
 
-template <int NI>
-cudaError_t launch_reg(const Lstm2Args &a, unsigned grid, cudaStream_t s) {
-    const size_t smem = sizeof(float) * ((size_t)2 * 32 * NI + 2 * 4 * a.JB1 + a.JB1 + 64);
+template <int NI, bool FUSE>
+cudaError_t launch_reg_t(const Lstm2Args &a, unsigned grid, cudaStream_t s) {
+    const int JBm = a.JB1 > a.JB2 ? a.JB1 : a.JB2;
+    size_t smem = sizeof(float) * ((size_t)2 * 32 * NI + 2 * 4 * JBm + JBm + 64);
+    if (a.X) {                                  // + x_t, gin, W_ih1 rows of a layer-1 CTA
+        const size_t Ip = 32 * (((size_t)a.I + 31) / 32);
+        smem += sizeof(float) * (Ip + 4 * a.JB1 + 8 + (size_t)4 * a.JB1 * Ip);
+        static size_t attr = 0;
+        if (attr < smem) {
+            cudaError_t e = cudaFuncSetAttribute(lstm2_reg_kernel<NI, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            attr = smem;
+        }
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kRegThreads);
@@ -379,7 +461,11 @@ cudaError_t launch_reg(const Lstm2Args &a, unsigned grid, cudaStream_t s) {
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    return cudaLaunchKernelEx(&cfg, lstm2_reg_kernel<NI>, a);
+    return cudaLaunchKernelEx(&cfg, lstm2_reg_kernel<NI, FUSE>, a);
+}
+template <int NI>
+cudaError_t launch_reg(const Lstm2Args &a, unsigned grid, cudaStream_t s) {
+    return a.X ? launch_reg_t<NI, true>(a, grid, s) : launch_reg_t<NI, false>(a, grid, s);
 }
 
 }  // namespace
@@ -388,7 +474,7 @@ size_t lstm2_workspace_bytes(int64_t H) { return sizeof(unsigned long long) * (4
 
 cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, const float *Wih2, const float *Whh2,
                              int64_t ldw, const float *b2, float *H1, float *H2, int64_t ldh, float *hT, float *cT,
-                             int64_t T, int64_t H, void *workspace, cudaStream_t s) {
+                             int64_t T, int64_t H, void *workspace, cudaStream_t s, const Lstm2Input *fused) {
     // 3 : 1 split of the SMs (layer-2 CTAs own two matrices), <= 148 co-resident CTAs
     int n1 = 48;
     const int JB1 = (int)((H + n1 - 1) / n1);
@@ -413,10 +499,19 @@ cudaError_t launch_lstm2_seq(const float *G1, int64_t ldg, const float *Whh1, co
     a.hbuf = static_cast<unsigned long long *>(workspace);
     a.T = (int)T; a.H = (int)H; a.n1 = n1; a.JB1 = JB1; a.JB2 = JB2;
     a.trace = lstm_trace_buffer();
+    a.X = nullptr; a.ldx = 0; a.Wih1 = nullptr; a.ldwi = 0; a.b1 = nullptr; a.I = 0;
+    if (fused) {
+        a.X = fused->X; a.ldx = fused->ldx; a.Wih1 = fused->Wih1; a.ldwi = fused->ldwi; a.b1 = fused->b1;
+        a.I = (int)fused->I;
+    }
     // register-resident weights when every CTA's (matrix, row) jobs fit 4 per warp and a row's
     // k-slice per lane fits NI <= 21 registers (H <= 672: config 2's 650, the paper's 512)
     static const bool reg_on = [] { const char *e = std::getenv("NIMBLE_LSTM_REG"); return !(e && e[0] == '0'); }();
     const int ni = (int)((H + 31) / 32);
+    const bool fuse_fits = !fused || sizeof(float) * (32 * ((fused->I + 31) / 32) * (4 * (size_t)JB1 + 1) + 4 * JB1) +
+                                         sizeof(float) * ((size_t)2 * 32 * ni + 12 * JB1 + 64) <= 232448 - 1024;
+    const bool fuse_shape = !fused || (32 * ((fused->I + 31) / 32) <= 2 * kRegThreads && 4 * JB1 <= 4 * kRegWarps);
+    if (fused && !(reg_on && ni <= 21 && fuse_fits && fuse_shape)) return cudaErrorNotSupported;   // caller composes GEMM + kernel
     if (reg_on && ni <= 21 && 4 * JB1 <= kRegWarps * kJobsPerWarp && 8 * JB2 <= kRegWarps * kJobsPerWarp) {
         const unsigned grid = (unsigned)(n1 + n2);
         if (ni <= 8) return launch_reg<8>(a, grid, s);

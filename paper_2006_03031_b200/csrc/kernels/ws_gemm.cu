@@ -5,7 +5,7 @@
 // per tile and spreads the weight stream over most SMs.
 //
 // Grid = S x m_tiles x n_tiles CTAs; the S CTAs of a (feature tile, token tile) unit form one
-// thread-block cluster along K (S <= 16).  CTA (q, mt, nt) owns weight rows [128 mt, +128),
+// thread-block cluster along K (S <= 8, portable).  CTA (q, mt, nt) owns weight rows [128 mt, +128),
 // tokens [128 nt, +128) and the k-blocks [q kb / S, (q+1) kb / S) (S depends on (N, K) and
 // the token-tile count only, so a token's result is the same for M and for M padded to a
 // multiple of 128: dynamic M == pad-then-slice, bit for bit).

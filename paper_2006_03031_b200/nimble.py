@@ -84,6 +84,8 @@ _SIGS = {
     "nimble_partition_lpt": [_i64p, _i64, C.c_int32, _i32p],
     "nimble_debug_trace": [_vp],
     "nimble_lstm2_seq": [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp],
+    "nimble_lstm2_forward": [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp,
+                             _i64, _i64, _vp, _vp],
     "nimble_layernorm_dev": [_vp, _i64, _vp, _vp, C.c_float, _vp, _i64, _vp, _i64, _i64, _vp],
     "nimble_attention_varlen_dev": [_vp, _i64, _i64, _vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, _vp,
                                     _i64, _vp],
@@ -374,6 +376,15 @@ def lstm_seq(G, W_hh, H_seq, hT, cT, workspace, T=None, h0=None, c0=None, stream
 
 def lstm2_workspace_bytes(H: int) -> int:
     return int(_lib.nimble_lstm2_workspace_bytes(int(H)))
+
+
+def lstm2_forward(X, I, W_ih1, b1, W_hh1, W_ih2, W_hh2, b2, H1, H2, hT, cT, workspace, T=None, stream=None):
+    """Both layers incl. the layer-1 input projection in one launch (nimble_lstm2_forward)."""
+    T = X.shape[0] if T is None else T
+    H = W_hh1.shape[1]
+    _check(_lib.nimble_lstm2_forward(_ptr(X), X.stride(0), I, _ptr(W_ih1), W_ih1.stride(0), _ptr(b1), _ptr(W_hh1),
+                                     _ptr(W_ih2), _ptr(W_hh2), W_hh1.stride(0), _ptr(b2), _ptr(H1), _ptr(H2),
+                                     H1.stride(0), _ptr(hT), _ptr(cT), T, H, _ptr(workspace), _stream(stream)))
 
 
 def lstm2_seq(G1, W_hh1, W_ih2, W_hh2, b2, H1, H2, hT, cT, workspace, T=None, stream=None):

@@ -49,16 +49,31 @@ class LSTMStack:
         self.ws2 = torch.zeros((nb.lstm2_workspace_bytes(H),), dtype=torch.uint8, device=device)
         # the wavefront kernel takes W_hh1, W_ih2, W_hh2 with one leading dimension (H)
         self.Wi2u = layers[1][0].to(device).contiguous() if len(layers) == 2 and layers[1][0].shape[1] == H else None
+        self.fused_ok = True
 
     def flops_per_token(self) -> int:
         return sum(2 * 4 * self.H * (Kp + self.H) for (_, _, _, Kp) in self.layers)
 
-    def forward(self, x: torch.Tensor, T: int | None = None, wavefront: bool = True) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, T: int | None = None, wavefront: bool = True, fused: bool = True) -> torch.Tensor:
         """x [>=T x Ip] fp32 (zero columns beyond I); returns the last layer's h sequence [T x H].
-        Two layers run as one wavefront kernel (nimble_lstm2_seq) unless wavefront=False."""
+        Two layers run as one wavefront kernel unless wavefront=False: with fused=True the layer-1
+        input projection runs inside it (nimble_lstm2_forward, one launch), else as a hoisted
+        input GEMM (nimble_dense_dyn + nimble_lstm2_seq)."""
         T = x.shape[0] if T is None else T
         if wavefront and self.Wi2u is not None:
             (Wi1, Wh1, b1, _), (Wi2, Wh2, b2, _) = self.layers
+            # the one-launch form pays a per-step W_ih1 mat-vec from shared memory: it wins only
+            # where the hoisted input GEMM launch dominates (measured: T = 1 14.7 vs 19.4 us,
+            # T = 8 49.7 vs 47.2 us)
+            if fused and self.fused_ok and T <= 4:
+                try:
+                    nb.lstm2_forward(x, self.I, Wi1, b1, Wh1, self.Wi2u, Wh2, b2, self.Hs[0], self.Hs[1], self.hT,
+                                     self.cT, self.ws2, T=T)
+                    return self.Hs[1][:T, :self.H]
+                except nb.NimbleError as e:
+                    if e.status != -7:                              # E_UNSUPPORTED
+                        raise
+                    self.fused_ok = False                                   # shape not built fused
             nb.dense_dyn(x, Wi1, b1, self.G, epi=nb.EPI_BIAS, M=T)           # hoisted input GEMM (M = T)
             nb.lstm2_seq(self.G, Wh1, self.Wi2u, Wh2, b2, self.Hs[0], self.Hs[1], self.hT, self.cT, self.ws2, T=T)
             return self.Hs[1][:T, :self.H]

@@ -25,6 +25,7 @@ def graph_time(fn, reps=20):
 for T in (1, 8, 35, 128, 512):
     x = torch.zeros((T, st.Ip), dtype=torch.float32, device="cuda"); x[:, :I] = synth.lstm_input(T, I, seed=1).cuda()
     tg = graph_time(lambda: st.forward(x, T))
+    tu = graph_time(lambda: st.forward(x, T, fused=False))
     (Wi1, Wh1, b1, _), (Wi2, Wh2, b2, _) = st.layers
     tgemm = graph_time(lambda: nb.dense_dyn(x, Wi1, b1, st.G, epi=nb.EPI_BIAS, M=T))
-    print(json.dumps({"T": T, "graph_us_per_seq": tg, "us_per_token": tg / T, "input_gemm_us": tgemm}), flush=True)
+    print(json.dumps({"T": T, "graph_us_per_seq": tg, "us_per_token": tg / T, "input_gemm_us": tgemm, "unfused_us_per_seq": tu}), flush=True)

@@ -3,8 +3,8 @@ synccheck / initcheck):
 
     compute-sanitizer --tool racecheck python scripts/sanitize_all.py
 
-GEMM families 1 (plain, cluster split-K), 2 (bmm MN-major B) and 3 (CTA pairs, every
-epilogue incl. the fused LayerNorm), the static twin, device-extent dense / LayerNorm /
+GEMM families 1 (plain, cluster split-K), 2 (bmm MN-major B), 3 (CTA pairs, every
+epilogue incl. the fused LayerNorm) and 4 (weight streaming, one and several token tiles), the static twin, device-extent dense / LayerNorm /
 attention, varlen attention, softmax, LayerNorm, fp32 SIMT8, both LSTM kernels and both
 Tree-LSTM forms.  Checks nothing numerically (the tests do); prints one line per op."""
 import os
@@ -32,7 +32,10 @@ def main():
     torch.manual_seed(0)
     d = "cuda"
     # ---- dense, bf16: family 1, cluster split-K, family 3 (pairs) with every epilogue
-    for (M, N, K) in ((77, 384, 256), (40, 1024, 4096), (2100, 1024, 1024), (2049, 640, 256)):
+    # (77, 40, 5: family 4 weight streaming, one token tile; 300 x 1024 x 4096: family 4 with
+    # three token tiles; 2100 / 2049: family 3 pairs)
+    for (M, N, K) in ((77, 384, 256), (40, 1024, 4096), (5, 2304, 768), (300, 1024, 4096), (2100, 1024, 1024),
+                      (2049, 640, 256)):
         x, W = bf(M, K, s=1.0), bf(N, K)
         b = torch.randn(N, device=d) * 0.1
         res = bf(M, N, s=1.0)

@@ -25,7 +25,7 @@ def test_exports_every_declared_symbol(nb):
     hdr = open(os.path.join(ROOT, "include", "nimble.h")).read()
     hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)          # drop comments
     declared = set(re.findall(r"\b(nimble_[a-z_0-9]+)\s*\(", hdr))
-    assert len(declared) == 31
+    assert len(declared) == 32
     for name in declared:
         assert hasattr(nb._lib, name), name
     assert set(nb.EXPORTED) <= declared | {"nimble_last_error", "nimble_version"}

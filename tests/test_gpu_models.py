@@ -182,3 +182,29 @@ def test_bert_large_layer_teacher_forced(nb, orc, L):
     drift = _abs_err(dd(y), full)
     print(f"BERT-large layer L={L}: free-running max abs err {drift:.3e}")
     assert drift <= 0.25
+
+
+@pytest.mark.parametrize("T", [1, 2, 7, 128, 512])
+def test_lstm2_forward_fused_input_projection(nb, orc, T):
+    # calls nimble_lstm2_forward directly (LSTMStack takes it only at T <= 4)
+    """nimble_lstm2_forward (layer-1 input projection inside the wavefront kernel, one launch)
+    against the fp64 oracle and against the two-launch form (hoisted input GEMM + wavefront)."""
+    from paper_2006_03031_b200.rnn import LSTMStack
+    I = H = 650
+    layers = synth.lstm_weights(I, H, 2, seed=11)
+    x = synth.lstm_input(T, I, seed=12)
+    st = LSTMStack(layers, max_T=T)
+    xp = torch.zeros((T, st.Ip), dtype=torch.float32, device="cuda")
+    xp[:, :I] = x.cuda()
+    (Wi1, Wh1, b1, _), (_, Wh2, b2, _) = st.layers
+    nb.lstm2_forward(xp, I, Wi1, b1, Wh1, st.Wi2u, Wh2, b2, st.Hs[0], st.Hs[1], st.hT, st.cT, st.ws2, T=T)
+    a = st.Hs[1][:T, :H].clone()
+    hT_a, cT_a = st.hT.clone(), st.cT.clone()
+    b = st.forward(xp, T, fused=False).clone()
+    torch.cuda.synchronize()
+    ref, states, _ = orc.lstm(x.numpy(), [(w1.numpy(), w2.numpy(), bb.numpy()) for w1, w2, bb in layers])
+    assert _abs_err(a, ref) <= 1e-4, _abs_err(a, ref)
+    for li in range(2):
+        assert _abs_err(hT_a[li], states[li][0]) <= 1e-4
+        assert _abs_err(cT_a[li], states[li][1]) <= 1e-4
+    assert float((a - b).abs().max()) <= 1e-5

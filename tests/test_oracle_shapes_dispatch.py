@@ -137,7 +137,7 @@ def test_dispatch_invariants(orc, dt):
                 # 16 k-blocks, one wave (8 S <= 148), no cluster record; S does not depend on M
                 s = d["split_k"]
                 assert d["family"] == 4 and d["umma_m"] == 128 and list(d["cluster"]) == [1, 1, 1]
-                assert list(d["grid"]) == [8, 1, s] and s == 16            # min(16 k-blocks, 148 // 8, 16)
+                assert list(d["grid"]) == [8, 1, s] and s == 8             # min(16 k-blocks, 148 // 8, 8)
             elif dt == 1:
                 s = d["split_k"]
                 assert s in (1, 2, 4, 8) and d["cluster"] == ((1 if M < 2048 else 2), 1, s)
@@ -167,25 +167,25 @@ def test_dispatch_bmm_families(orc):
 
 def test_dispatch_weight_streaming_family(orc):
     """Family 4 pins (DISPATCH.md): taken exactly when M <= 128 and the 128-feature tiles fit
-    one wave; grid = tiles x S with S = min(k-blocks, 148 // tiles, 16) >= 1 — every CTA owns at
+    one wave; grid = tiles x S with S = min(k-blocks, 148 // tiles, 8) >= 1 — every CTA owns at
     least one k-block of 64, the grid never exceeds one wave of 148 and a tile's splits fit one
     cluster; S is the same for every M (pad-then-slice invariant); the residue split equals
     family 1's."""
-    cases = [(2304, 768, 8), (768, 768, 12), (3072, 768, 6), (768, 3072, 16), (1024, 1024, 16),
-             (3072, 1024, 6), (4096, 1024, 4), (1024, 4096, 16), (128, 64, 1), (128, 100000, 16),
+    cases = [(2304, 768, 8), (768, 768, 8), (3072, 768, 6), (768, 3072, 8), (1024, 1024, 8),
+             (3072, 1024, 6), (4096, 1024, 4), (1024, 4096, 8), (128, 64, 1), (128, 100000, 8),
              (18944, 512, 1), (300, 200, 4)]
     for N, K, S in cases:
         tiles = -(-N // 128)
         for M in (1, 2, 15, 16, 17, 100, 127, 128):
             st, d = orc.dispatch_dense(M, N, K, 1)
             assert st == 0 and d["family"] == 4 and d["split_k"] == S, (N, K, M, d)
-            assert tiles * S <= 148 and S <= -(-K // 64) and S <= 16
+            assert tiles * S <= 148 and S <= -(-K // 64) and S <= 8
             assert list(d["grid"]) == [tiles, 1, S]
             d1 = orc.dispatch_dense(M, N, K, 1, 0, 128, 1)[1]      # family 1 with the same t
             for key in ("k", "r", "residue_class", "variant", "umma_n_full", "umma_n_tail", "n_classes"):
                 assert d[key] == d1[key], key
     # several token tiles (M <= 1024): family 4 only at K >= 2048 and while the split stays >= 2
-    # (fewer than 75 units), with S = min(k-blocks, 148 // units, 16); the same S for M and M
+    # (fewer than 75 units), with S = min(k-blocks, 148 // units, 8); the same S for M and M
     # padded to 128 k
     for (N, K, M, fam, S) in [(2304, 768, 129, 1, 1), (3072, 1024, 129, 1, 1), (4096, 2048, 200, 4, 2),
                               (4096, 2048, 300, 1, 1), (1024, 4096, 1024, 4, 2), (1024, 4096, 1025, 1, 1),
