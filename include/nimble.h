@@ -192,8 +192,11 @@ int nimble_dense_ln_dyn(const void *x, int64_t ldx, const void *W, int64_t ldw, 
  * allocates by the bound M_max (1 <= M_max < 2048; nimble_shape_dense on (M_max, K) x
  * (N, K)); the true extent M is the int32 at M_dev (device memory, 1 <= M <= M_max, read
  * by the kernel after its grid-dependency wait, so an earlier kernel or copy on the stream
- * may write it).  The kernel runs the residue dispatch on the device: family 1 of
- * DISPATCH.md with the token tile of the registered schedule (else 128) and the variant
+ * may write it).  The kernel runs the residue dispatch on the device.  With M_max <= 128 and
+ * no schedule registered: family 4 of DISPATCH.md (weight streaming; its split S depends on
+ * (N, K) only, so the bound's launch serves every M; the residue width and the record are
+ * decided on the device; rows >= M of the token tile only feed unstored columns).  Otherwise
+ * family 1 of DISPATCH.md with the token tile of the registered schedule (else 128) and the variant
  * limit c current at launch; split_k is the host rule's with the schedule's cap, else the
  * default cap evaluated at the bound M_max, when M_max fits one token tile (then it is the
  * same for every M <= M_max), else 1.  Writes y rows [0, M) only (the store's tensor

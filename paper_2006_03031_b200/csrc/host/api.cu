@@ -320,7 +320,7 @@ cudaError_t ws_workspace(cudaStream_t stream, float **part) {
 // green contexts): the caller then takes family 1.
 int launch_ws(const nimble_dispatch &d, const void *x, int64_t ldx, const void *W, int64_t ldw, const float *bias,
               const void *residual, int64_t ldr, void *y, int64_t ldy, int64_t M, int64_t N, int64_t K, int epi,
-              cudaStream_t s) {
+              cudaStream_t s, const int32_t *m_dev = nullptr, nimble_dispatch *rec = nullptr) {
     WsLaunch L;
     std::memset(&L, 0, sizeof(L));
     L.p.M = (int32_t)M;
@@ -331,6 +331,7 @@ int launch_ws(const nimble_dispatch &d, const void *x, int64_t ldx, const void *
     L.p.kb_total = (int32_t)((K + 63) / 64);
     L.p.n_umma = d.r ? d.umma_n_tail : d.umma_n_full;
     L.p.n_box = d.grid[1] == 1 ? L.p.n_umma : d.umma_n_full;   // one box height for every token tile
+    if (m_dev) L.p.n_box = d.umma_n_full;        // device extent: any residue width (incl. the fallback) fits
     const int kb_max = (L.p.kb_total + L.p.S - 1) / L.p.S;
     L.p.stages = kb_max < 3 ? kb_max : 3;
     L.smem_bytes = ws_smem_bytes(L.p.n_box, L.p.stages);
@@ -350,6 +351,9 @@ int launch_ws(const nimble_dispatch &d, const void *x, int64_t ldx, const void *
     if (e != cudaSuccess) return cuda_fail("nimble_dense_dyn(family 4) workspace", e);
     L.p.part = part;
     L.p.trace = g_trace;
+    L.p.m_dev = m_dev;                            // device extent: M above is the bound M_max
+    L.p.var_c = variant_limit();
+    L.p.rec = rec;
     L.p.alpha = 1.f;
     L.p.bias = bias;
     L.p.res = static_cast<const __nv_bfloat16 *>(residual);
@@ -598,6 +602,18 @@ extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, i
     int32_t t = 0, cap = 8;
     dense_schedule(N, K, &t, &cap);                    // tuned token tile / split cap
     nimble_dispatch d;
+    if (t == 0 && M_max <= 128 && (N + 127) / 128 <= kNumSMs) {
+        // family 4 (one token tile): the split S depends on (N, K) only, so the launch geometry of
+        // the bound serves every M <= M_max; the kernel reads M and picks the residue width
+        dispatch_umma_ws(M_max, N, K, &d);
+        const int ws = launch_ws(d, x, ldx, W, ldw, bias, residual, ldr, y, ldy, M_max, N, K, epi,
+                                 static_cast<cudaStream_t>(stream), M_dev, dispatch_dev);
+        if (ws == NIMBLE_OK) {
+            clear_error();
+            return NIMBLE_OK;
+        }
+        if (ws != 1) return ws;
+    }
     // split-K needs a launch grid that does not depend on M: allowed when the bound fits ONE
     // token tile, where the host rule's split (a function of the tile count) is the same for
     // every M <= M_max; otherwise the device dispatch runs split 1

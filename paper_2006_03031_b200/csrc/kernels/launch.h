@@ -117,6 +117,12 @@ struct WsParams {
     const __nv_bfloat16 *res; int64_t ld_res;
     __nv_bfloat16 *out; int64_t ld_out;
     float *part;             // [n_tiles][m_tiles][S][n_box][128] fp32 partial slabs (workspace)
+    // device-resident extent (nimble_dense_dyn_dev, one token tile): M is read from m_dev after
+    // the grid-dependency wait, the residue dispatch (UMMA N of the tile) runs on the device and
+    // CTA (0, 0) writes the record; M above is then the bound M_max
+    const int32_t *m_dev;
+    int32_t var_c;
+    nimble_dispatch *rec;
     unsigned long long *trace;   // debug (nimble_debug_trace): per CTA 8 globaltimer stamps, NULL = off
 };
 struct WsLaunch {

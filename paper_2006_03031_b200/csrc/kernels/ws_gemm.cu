@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
     const int nt = (int)blockIdx.z;               // 128-token tile
     const int S = p.S;
     const int tok0 = nt * 128;
-    const int Mt = min(128, p.M - tok0);          // valid tokens of this token tile
-    const uint32_t n_this = (nt == p.n_tiles - 1) ? (uint32_t)p.n_umma : 128u;   // residue width on the tail tile
+    int Mt = min(128, p.M - tok0);                // valid tokens of this token tile (device extent: below)
+    uint32_t n_this = (nt == p.n_tiles - 1) ? (uint32_t)p.n_umma : 128u;   // residue width on the tail tile
     const int kb0 = (int)((int64_t)q * p.kb_total / S);
     const int kb1 = (int)((int64_t)(q + 1) * p.kb_total / S);
     const int nkb = kb1 - kb0;
@@ -96,6 +96,30 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
     const uint32_t tmem_base = *tmem_slot;
     ptx::pdl_trigger();                                // the next kernel's prologue may start
     if (tr) ts1 = ptx::globaltimer();
+    if (p.m_dev) {
+        // device extent (one token tile): the residue dispatch of DISPATCH.md family 4 on the
+        // device — every role but the producer (which waits in its own path) reads M here
+        if (!(warp == 0 && lane == 0)) ptx::pdl_wait();   // (the producer waits in its own path)
+        const int Md = warp == 0 && lane == 0 ? 0 : *p.m_dev;
+        if (!(warp == 0 && lane == 0)) {
+            if (Md < 1 || Md > p.M) __trap();          // outside [1, M_max]: caller bug, fail loudly
+            const int r = Md % 128, k = Md / 128;
+            const int cls = (r + 15) / 16, ncls = 9;
+            const int cc = (p.var_c <= 0 || p.var_c >= ncls) ? ncls : p.var_c;
+            const int variant = (cc == ncls || cls < cc - 1) ? cls : -1;
+            Mt = Md;
+            n_this = r ? (variant >= 0 ? 16u * (uint32_t)cls : 128u) : 128u;
+            if (p.rec && threadIdx.x == 32 && blockIdx.x == 0 && blockIdx.y == 0) {
+                nimble_dispatch d{};
+                d.family = 4; d.tile_t = 128; d.granule = 16; d.n_classes = ncls; d.residue_class = cls;
+                d.variant = variant; d.split_k = S; d.umma_m = 128; d.umma_n_full = 128;
+                d.umma_n_tail = r ? (int32_t)n_this : 0; d.k = k; d.r = r;
+                d.grid[0] = p.m_tiles; d.grid[1] = 1; d.grid[2] = S;
+                d.cluster[0] = d.cluster[1] = d.cluster[2] = 1;
+                *p.rec = d;
+            }
+        }
+    }
 
     if (warp == 0 && lane == 0) {
         // ---- producer: weights first (static: before the grid-dependency wait), tokens after
@@ -134,6 +158,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
         ptx::umma_commit(tfull);
     }
     __syncwarp();
+    if (p.m_dev) Mt = *p.m_dev;                        // every thread has passed the dependency wait
 
     // ---- drain the accumulator into this CTA's partial slab: TMEM lane = feature, so a warp's
     // store of one token covers 32 consecutive features (128 B).  (Transposing through shared

@@ -207,10 +207,11 @@ def test_bert_forward_dev_and_one_graph_bitwise(nb):
 
 @pytest.mark.parametrize("N,K", [(768, 3072), (2304, 768), (1024, 4096)])
 def test_dense_dyn_dev_split_k_within_one_tile(nb, orc, N, K):
-    """M_max <= 128 fits one token tile: the device dispatch keeps the host rule's split-K (the
-    same for every M <= M_max; the default cap evaluated at the bound), the record equals the
-    oracle's rule with that (t, cap), and outputs equal the host-extent launch with the same
-    schedule bit for bit (same tiles, same fixed-order split reduction)."""
+    """M_max <= 128 fits one token tile: with a family-1 schedule registered (the default rule
+    takes family 4 there, test_dense_dyn_dev_family4) the device dispatch keeps the host rule's
+    split-K (the same for every M <= M_max), the record equals the oracle's rule with that
+    (t, cap), and outputs equal the host-extent launch with the same schedule bit for bit (same
+    tiles, same fixed-order split reduction)."""
     M_max = 128
     W, b, x = _setup(N, K, M_max, 71)
     Wd, bd, xd = W.cuda(), b.cuda(), x.cuda()
@@ -218,9 +219,9 @@ def test_dense_dyn_dev_split_k_within_one_tile(nb, orc, N, K):
     for M in (1, 7, 16, 33, 100, 127, 128):
         rec = torch.zeros(nb.DISPATCH_BYTES, dtype=torch.uint8, device="cuda")
         y_dev = torch.empty((M_max, N), dtype=torch.bfloat16, device="cuda")
-        nb.dense_dyn_dev(xd, Wd, bd, y_dev, torch.tensor([M], dtype=torch.int32, device="cuda"), M_max, record=rec)
-        nb.set_dense_schedule(N, K, 128, cap)               # the host path with the same (t, cap)
+        nb.set_dense_schedule(N, K, 128, cap)               # family 1 with the default (t, cap)
         try:
+            nb.dense_dyn_dev(xd, Wd, bd, y_dev, torch.tensor([M], dtype=torch.int32, device="cuda"), M_max, record=rec)
             y_host = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
             nb.dense_dyn(xd[:M], Wd, bd, y_host)
         finally:
@@ -230,3 +231,52 @@ def test_dense_dyn_dev_split_k_within_one_tile(nb, orc, N, K):
         assert drec == orc.dispatch_dense(M, N, K, 1, 0, 128, cap)[1], M
         assert (drec["split_k"] > 1) == (K >= 2048)
         assert torch.equal(y_dev[:M], y_host), M
+
+
+@pytest.mark.parametrize("N,K,M_max", [(1024, 1024, 128), (768, 3072, 100), (2304, 768, 64)])
+def test_dense_dyn_dev_family4(nb, orc, N, K, M_max):
+    """Device extent with a one-token-tile bound: the weight-streaming family 4 with the residue
+    dispatch on the device (record vs the oracle's default rule, every variant limit), values vs
+    the oracle, rows >= M untouched, bitwise equal to the host-extent launch, and one captured
+    graph serving every M."""
+    W, b, x = _setup(N, K, M_max, 71)
+    Wd, bd, xd = W.cuda(), b.cuda(), x.cuda()
+    rec = torch.zeros(nb.DISPATCH_BYTES, dtype=torch.uint8, device="cuda")
+    for c in (0, 2):
+        nb.set_variant_limit(c)
+        try:
+            for M in sorted({1, 2, 15, 16, 17, M_max // 2, M_max - 1, M_max}):
+                y = torch.full((M_max, N), float(POISON), dtype=torch.bfloat16, device="cuda")
+                nb.dense_dyn_dev(xd, Wd, bd, y, torch.tensor([M], dtype=torch.int32, device="cuda"), M_max,
+                                 epi=nb.EPI_BIAS_GELU, record=rec)
+                torch.cuda.synchronize()
+                d = nb.dispatch_from_bytes(rec)
+                assert d == orc.dispatch_dense(M, N, K, 1, c)[1] and d["family"] == 4, (M, c, d)
+                ref, D = orc.dense(x[:M].double().numpy(), W.double().numpy(), b.numpy(), None, nb.EPI_BIAS_GELU)
+                assert _err(y[:M], ref, D) <= TOL_BF16, (M, c)
+                assert bool((y[M:] == POISON.cuda()).all())
+                y_host = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+                nb.dense_dyn(xd[:M].contiguous(), Wd, bd, y_host, epi=nb.EPI_BIAS_GELU)
+                torch.cuda.synchronize()
+                assert torch.equal(y_host, y[:M]), (M, c)
+        finally:
+            nb.set_variant_limit(0)
+    # one graph, every M
+    y = torch.empty((M_max, N), dtype=torch.bfloat16, device="cuda")
+    m_dev = torch.tensor([M_max], dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        nb.dense_dyn_dev(xd, Wd, bd, y, m_dev, M_max, record=rec)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            nb.dense_dyn_dev(xd, Wd, bd, y, m_dev, M_max, record=rec)
+    for M in (1, M_max, 7, M_max // 2 + 1):
+        y.fill_(float(POISON))
+        m_dev.fill_(M)
+        g.replay()
+        torch.cuda.synchronize()
+        ref, D = orc.dense(x[:M].double().numpy(), W.double().numpy(), b.numpy(), None, nb.EPI_BIAS)
+        assert _err(y[:M], ref, D) <= TOL_BF16, M
+        assert bool((y[M:] == POISON.cuda()).all()), M
+        assert nb.dispatch_from_bytes(rec) == orc.dispatch_dense(M, N, K, 1)[1], M
