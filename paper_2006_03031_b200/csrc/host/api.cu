@@ -334,7 +334,7 @@ int launch_ws(const nimble_dispatch &d, const void *x, int64_t ldx, const void *
     if (m_dev) L.p.n_box = d.umma_n_full;        // device extent: any residue width (incl. the fallback) fits
     const int kb_max = (L.p.kb_total + L.p.S - 1) / L.p.S;
     L.p.stages = kb_max < 3 ? kb_max : 3;
-    L.smem_bytes = ws_smem_bytes(L.p.n_box, L.p.stages);
+    L.smem_bytes = ws_smem_bytes(L.p.n_box, L.p.stages, L.p.S);
     static std::mutex fit_mu;
     static std::vector<std::pair<int, size_t>> fits;     // (S, smem) known to schedule
     {

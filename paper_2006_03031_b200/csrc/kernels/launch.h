@@ -133,7 +133,7 @@ struct WsLaunch {
     cudaStream_t stream;
 };
 cudaError_t launch_ws_gemm(const WsLaunch &L);
-size_t ws_smem_bytes(int n_box, int stages);
+size_t ws_smem_bytes(int n_box, int stages, int S);
 bool ws_cluster_fits(int S, size_t smem_bytes);
 
 // fp32 SIMT8 dense (family 0)

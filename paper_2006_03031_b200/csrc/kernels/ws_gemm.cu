@@ -39,6 +39,11 @@ constexpr int kAB = 128 * kBK * 2;            // 16 KB weight k-block
 constexpr int kWsMaxSplit = 16;               // cluster size limit (non-portable)
 
 __device__ __forceinline__ float4 ldcg4(const float *p) { return __ldcg(reinterpret_cast<const float4 *>(p)); }
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void add4(float4 &a, const float4 &v) { a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w; }
 
 template <int EPI>
@@ -50,6 +55,8 @@ __device__ __forceinline__ float epi1(float a, const WsParams &p, int f, int j) 
     return a;
 }
 
+__device__ __forceinline__ int S_of(const WsParams &p) { return p.S; }
+
 template <int EPI>
 __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-overlapped neighbour fits
     ws_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const WsParams p) {
@@ -57,7 +64,8 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
     uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int b_bytes = p.n_box * 128;            // token k-block: n_box rows of 128 B
     const int stage_bytes = kAB + b_bytes;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.stages * stage_bytes);
+    const int ring = (S_of(p) == 2 && p.stages * stage_bytes < p.n_box * 512) ? p.n_box * 512 : p.stages * stage_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + ring);   // after the ring (/ the S == 2 slab)
     uint64_t *empty = full + p.stages;
     uint64_t *tfull = empty + p.stages;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
@@ -172,12 +180,19 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
         const int quarter = (int)(warp & 3), half = (int)(warp >> 2);
         const int f = quarter * 32 + (int)lane;
         float *mine = part_tile + (size_t)q * slab;
+        float *sp = reinterpret_cast<float *>(smem);  // S == 2: the slab stays in shared memory (ring is free)
         for (int c0 = half * 16; c0 < Mt; c0 += 32) {
             float v[16];
             ptx::tmem_ld16(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
+            if (S == 2) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < Mt) __stcg(mine + (size_t)(c0 + j) * 128 + f, v[j]);
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < Mt) sp[(c0 + j) * 128 + f] = v[j];
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < Mt) __stcg(mine + (size_t)(c0 + j) * 128 + f, v[j]);
+            }
         }
         ptx::tc_fence_before();
     }
@@ -200,14 +215,25 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
         const int jl = q + S * (it >> 5), l = it & 31;
         const float *src = part_tile + (size_t)jl * 128 + 4 * l;
         const int j = tok0 + jl;                          // output row
-        float4 v[kWsMaxSplit];
+        float4 a;
+        if (S == 2) {
+            // the two slabs live in the two CTAs' shared memory: own + the peer's over DSMEM,
+            // summed in split order (part 0 + part 1) as the L2 path does
+            const uint32_t la = ptx::smem_u32(smem) + (uint32_t)((jl * 128 + 4 * l) * 4);
+            const float4 own = *reinterpret_cast<const float4 *>(smem + (size_t)(jl * 128 + 4 * l) * 4);
+            const float4 peer = ld_dsmem4(ptx::map_shared_rank(la, (uint32_t)(q ^ 1)));
+            a = q == 0 ? own : peer;
+            add4(a, q == 0 ? peer : own);
+        } else {
+            float4 v[kWsMaxSplit];
 #pragma unroll
-        for (int u = 0; u < kWsMaxSplit; ++u)
-            v[u] = u < S ? ldcg4(src + (size_t)u * slab) : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 a = v[0];
+            for (int u = 0; u < kWsMaxSplit; ++u)
+                v[u] = u < S ? ldcg4(src + (size_t)u * slab) : make_float4(0.f, 0.f, 0.f, 0.f);
+            a = v[0];
 #pragma unroll
-        for (int u = 1; u < kWsMaxSplit; ++u)
-            if (u < S) add4(a, v[u]);
+            for (int u = 1; u < kWsMaxSplit; ++u)
+                if (u < S) add4(a, v[u]);
+        }
         const int f = mt * 128 + 4 * l;
         if (f >= p.N) continue;
         __nv_bfloat16 *dst = p.out + (size_t)j * p.ld_out + f;
@@ -223,6 +249,10 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
             const float av[4] = {a.x, a.y, a.z, a.w};
             for (int e = 0; e < 4 && f + e < p.N; ++e) dst[e] = __float2bfloat16_rn(epi1<EPI>(av[e], p, f + e, j));
         }
+    }
+    if (S == 2) {                                      // the peer may still read this CTA's slab
+        ptx::cluster_arrive();
+        ptx::cluster_wait();
     }
     if (tr && threadIdx.x == 0) {
         unsigned long long *t = p.trace + (((size_t)nt * p.m_tiles + mt) * S + q) * 8;
@@ -262,8 +292,11 @@ cudaError_t launch_ws_t(const WsLaunch &L) {
 
 }  // namespace
 
-size_t ws_smem_bytes(int n_box, int stages) {
-    return 1024 /* alignment slack */ + (size_t)stages * (kAB + (size_t)n_box * 128) + 256 /* barriers, TMEM slot */;
+size_t ws_smem_bytes(int n_box, int stages, int S) {
+    // S == 2: the ring doubles as the fp32 [tokens][128] partial slab exchanged over DSMEM
+    size_t ring = (size_t)stages * (kAB + (size_t)n_box * 128);
+    if (S == 2 && ring < (size_t)n_box * 512) ring = (size_t)n_box * 512;
+    return 1024 /* alignment slack */ + ring + 256 /* barriers, TMEM slot */;
 }
 
 // Can a cluster of S CTAs of this size be scheduled at all on this device (under MPS / green
