@@ -89,12 +89,12 @@ int encode_operand(CUtensorMap *m, const void *base, int64_t inner, int64_t rows
 // K-blocked operand view for two-k-block pipeline stages (batch 1, K % 64 == 0):
 // dims {64 (k within a block), rows, K / 64 (k-block)}, strides {ld, 64 elements};
 // box {64, box_rows, 2}: one TMA moves two consecutive swizzled 64-wide k-blocks.
-int encode_operand_kb(CUtensorMap *m, const void *base, int64_t K, int64_t rows, int64_t ld, int box_rows) {
+int encode_operand_kb(CUtensorMap *m, const void *base, int64_t K, int64_t rows, int64_t ld, int box_rows, int kd = 2) {
     cudaError_t e = get_encoder();
     if (e != cudaSuccess) return cuda_fail("cuTensorMapEncodeTiled lookup", e);
     cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(K / 64)};
     cuuint64_t strides[2] = {(cuuint64_t)ld * 2, 128};
-    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 2}, estr[3] = {1, 1, 1};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)kd}, estr[3] = {1, 1, 1};
     CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -465,9 +465,11 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     const int out_box = L.p.half_stg ? L.p.box_n / 2 : L.p.box_n;
     // two k-blocks per pipeline stage where the operands tile K exactly (every BERT shape)
     L.p.kd = (kblock2_enabled() && K % 64 == 0 && K >= 128) ? 2 : 1;
-    if (L.p.kd == 2) {
-        if ((st = encode_operand_kb(&L.tmA, W, K, N, ldw, 128)) != NIMBLE_OK) return st;
-        if ((st = encode_operand_kb(&L.tmB, x, K, M, ldx, box_b)) != NIMBLE_OK) return st;
+    static const int kd_exp = [] { const char *e = std::getenv("NIMBLE_EXP_KD"); return e ? std::atoi(e) : 0; }();
+    if (kd_exp > 2 && L.p.kd == 2 && !L.pair) L.p.kd = kd_exp;   // experiment only: k-blocks per stage (family 1)
+    if (L.p.kd >= 2) {
+        if ((st = encode_operand_kb(&L.tmA, W, K, N, ldw, 128, L.p.kd)) != NIMBLE_OK) return st;
+        if ((st = encode_operand_kb(&L.tmB, x, K, M, ldx, box_b, L.p.kd)) != NIMBLE_OK) return st;
     } else {
         if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
         if ((st = encode_operand(&L.tmB, x, K, M, ldx, 1, 0, box_b, &L.p.b_batch_mid)) != NIMBLE_OK) return st;

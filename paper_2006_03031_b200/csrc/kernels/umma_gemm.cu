@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int32_t kc = kb * kBlockK;
                 uint8_t *sa = smem + stage * stage_bytes;
                 if (isA) {
-                    if (kd == 2) {          // {64 k, rows, k-block} view: two 16 KB swizzled blocks
+                    if (kd >= 2) {          // {64 k, rows, k-block} view: kd 16 KB swizzled blocks
                         if (PAIR) ptx::tma_load_3d_pair(sa, &tmA, &full_bar[stage], 0, a_row, kb);
                         else ptx::tma_load_3d(sa, &tmA, &full_bar[stage], 0, a_row, kb);
                     } else if (PAIR) {      // heads interleaved inside a row (QKV views): batch mid
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (p.b_batch_mid) ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[stage], b_row + 64 * q, bb, kc);
                             else ptx::tma_load_3d(sb + q * 8192, &tmB, &full_bar[stage], b_row + 64 * q, kc, bb);
                         }
-                    } else if (kd == 2) {
+                    } else if (kd >= 2) {
                         if (PAIR) ptx::tma_load_3d_pair(sb, &tmB, &full_bar[stage], 0, b_row, kb);
                         else ptx::tma_load_3d(sb, &tmB, &full_bar[stage], 0, b_row, kb);
                     } else if (PAIR) {
