@@ -465,8 +465,13 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     const int out_box = L.p.half_stg ? L.p.box_n / 2 : L.p.box_n;
     // two k-blocks per pipeline stage where the operands tile K exactly (every BERT shape)
     L.p.kd = (kblock2_enabled() && K % 64 == 0 && K >= 128) ? 2 : 1;
+    // the 1-CTA family without split-K takes THREE k-blocks per stage (96 KB stages, two in the
+    // ring): fewer, larger TMA stages per tile (the per-stage completion pacing);
+    // measured 2-7 % faster at M = 256-1024 on every BERT shape, while the CTA-pair family is
+    // 2-9 % slower with it (profiles/r02c_kd3_sweep.jsonl)
+    if (L.p.kd == 2 && !L.pair && L.p.split == 1 && K >= 192) L.p.kd = 3;
     static const int kd_exp = [] { const char *e = std::getenv("NIMBLE_EXP_KD"); return e ? std::atoi(e) : 0; }();
-    if (kd_exp > 2 && L.p.kd == 2 && !L.pair) L.p.kd = kd_exp;   // experiment only: k-blocks per stage (family 1)
+    if (kd_exp >= 2 && L.p.kd >= 2) L.p.kd = kd_exp;   // experiment only: k-blocks per stage
     if (L.p.kd >= 2) {
         if ((st = encode_operand_kb(&L.tmA, W, K, N, ldw, 128, L.p.kd)) != NIMBLE_OK) return st;
         if ((st = encode_operand_kb(&L.tmB, x, K, M, ldx, box_b, L.p.kd)) != NIMBLE_OK) return st;
@@ -643,9 +648,10 @@ extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, i
     L.p.var_c = variant_limit();
     L.p.rec = dispatch_dev;
     L.p.kd = (kblock2_enabled() && K % 64 == 0 && K >= 128) ? 2 : 1;
-    if (L.p.kd == 2) {
-        if ((st = encode_operand_kb(&L.tmA, W, K, N, ldw, 128)) != NIMBLE_OK) return st;
-        if ((st = encode_operand_kb(&L.tmB, x, K, M_max, ldx, L.p.box_n)) != NIMBLE_OK) return st;
+    if (L.p.kd == 2 && L.p.split == 1 && K >= 192) L.p.kd = 3;   // as dense_impl's 1-CTA family
+    if (L.p.kd >= 2) {
+        if ((st = encode_operand_kb(&L.tmA, W, K, N, ldw, 128, L.p.kd)) != NIMBLE_OK) return st;
+        if ((st = encode_operand_kb(&L.tmB, x, K, M_max, ldx, L.p.box_n, L.p.kd)) != NIMBLE_OK) return st;
     } else {
         if ((st = encode_operand(&L.tmA, W, K, N, ldw, 1, 0, 128, &L.p.a_batch_mid)) != NIMBLE_OK) return st;
         if ((st = encode_operand(&L.tmB, x, K, M_max, ldx, 1, 0, L.p.box_n, &L.p.b_batch_mid)) != NIMBLE_OK) return st;

@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // not generic ST/LD through the LSU).
     uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const bool split = p.split > 1;
-    const int kd = p.kd;                           // k-blocks of 64 per pipeline stage (1 or 2)
+    const int kd = p.kd;                           // k-blocks of 64 per pipeline stage (1, 2 or 3)
     const int b_bytes = b_stage_bytes(g.box_n, B_MN);   // per k-block
     const int stage_bytes = kd * (kABytes + b_bytes);
     const int ring_bytes = p.stages * stage_bytes;
