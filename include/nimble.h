@@ -77,7 +77,7 @@ typedef enum {
 /* The dispatch record: exactly what the matching kernel entry point launches.
  * Field meanings are DISPATCH.md's.  family: 0 SIMT8 (fp32), 1 UMMA_T (bf16,
  * tokens on the UMMA-N slot), 2 UMMA_D (bf16 bmm with trans_b), 3 UMMA_T256 (bf16,
- * M >= 2048, CTA pairs), 4 UMMA_WS (bf16 dense, M <= 128: weight streaming, the K
+ * CTA pairs where they need fewer waves than family 1, DISPATCH.md), 4 UMMA_WS (bf16 dense, M <= 128: weight streaming, the K
  * splits of a feature tile one cluster).  variant -1 is the guarded fallback.
  * x = tile_t*k + r. */
 typedef struct {
@@ -117,8 +117,8 @@ int nimble_dispatch_bmm(int64_t batch, int64_t M, int64_t N, int64_t K, int tran
  * shape (N, K) replaces family 1's token tile t (the residue tile: x = t k + r, classes
  * ceil(r/16) in 0..t/16, so t/16 + 1 variants) and caps its split-K factor (t = 256 runs
  * without split-K: the fp32 exchange buffers would not fit shared memory); it applies to
- * nimble_dispatch_dense and nimble_dense_dyn with M < 2048 (family 3 and the static twin are
- * not tuned).  tile_t in {32, 64, 128, 256} (0 removes the entry), split_max in {1, 2, 4, 8};
+ * nimble_dispatch_dense and nimble_dense_dyn with M < 2048 (at M >= 2048 the default rule,
+ * family 1 or 3, runs; the static twin is not tuned).  tile_t in {32, 64, 128, 256} (0 removes the entry), split_max in {1, 2, 4, 8};
  * anything else -> NIMBLE_E_EXTENT.  Process-wide, thread-safe.  get: tile_t = 0 when no
  * schedule is registered (the default applies: t = 128, split cap 8 if K >= 2048, else 1).
  * ------------------------------------------------------------------------- */
@@ -169,7 +169,7 @@ int nimble_dense_static(const void *x, int64_t ldx, const void *W, int64_t ldw, 
  * LayerNorm over the N features of each row (biased variance, eps inside the rsqrt;
  * DESIGN.md reading 10: post-LN, eps = 1e-12 in BERT).  Arguments as nimble_dense_dyn with
  * dt = NIMBLE_BF16 and the BIAS_RESIDUAL epilogue; gamma, beta: fp32 [N], 16-B aligned.
- * Where the residue dispatch picks the 2-CTA family (M >= 2048), N = 1024 and K >= 2048
+ * Where the residue dispatch picks the 2-CTA family (family 3), N = 1024 and K >= 2048
  * (a main loop long enough to hide the exchange) the LayerNorm runs in the GEMM epilogue: the 8 CTAs holding the four 256-feature quarters of a
  * 256-token tile exchange per-token (sum, sum of squares) partials through a library
  * workspace owned by the calling STREAM (a pool of 16 per device: launches on different

@@ -117,17 +117,27 @@ static int32_t orc_split(int64_t tiles, int64_t M, int64_t K) { return orc_split
 #define ORC_MAXEXT 2147483647LL
 
 /* families 1 / 3, UMMA_T: tokens (symbolic M) on the UMMA-N slot, granule 16;
- * t = 128 for M < 2048 (family 1, split-K allowed), t = 256 for M >= 2048 (family 3). */
+ * t = 128 (family 1, split-K allowed) or t = 256 (family 3, CTA pairs).  DISPATCH.md "Family 3":
+ * family 3 exactly when its 256 x 256 tiles take fewer waves over 74 CTA pairs than family 1's
+ * 128 x 128 tiles over 148 CTAs (round 2; measured rule, the paper leaves the tiling choice to
+ * the schedule). */
+static int orc_pairs_win(int64_t batch, int64_t M, int64_t N) {
+    int64_t tiles_128 = orc_ceil_div(N, 128) * orc_ceil_div(M, 128) * batch;
+    int64_t tiles_256 = orc_ceil_div(N, 256) * orc_ceil_div(M, 256) * batch;
+    int64_t waves_1 = orc_ceil_div(tiles_128, 148), waves_3 = orc_ceil_div(tiles_256, 74);
+    return waves_3 < waves_1;
+}
 /* tile_t / split_max: a tuned schedule for family 1 (DISPATCH.md "Tuned schedules",
- * P:392-406 three-step symbolic tuning picks them); tile_t = 0 -> the default (128, cap 8 if
- * K >= 2048, else 1). */
+ * P:392-406 three-step symbolic tuning picks them), used for M < 2048; tile_t = 0 -> the
+ * default (128, cap 8 if K >= 2048, else 1). */
 static int orc_umma_t_sched(int64_t batch, int64_t M, int64_t N, int64_t K, int c, int32_t tile_t,
                             int32_t split_max, orc_dispatch *d) {
     memset(d, 0, sizeof(*d));
-    int wide = (M >= 2048);
-    int32_t t = wide ? 256 : (tile_t > 0 ? tile_t : 128);
+    int tuned = (tile_t > 0 && M < 2048);
+    int wide = !tuned && orc_pairs_win(batch, M, N);
+    int32_t t = wide ? 256 : (tuned ? tile_t : 128);
     /* split-K exchanges two fp32 [128 x t] buffers through smem: only t <= 128 fits */
-    int32_t cap = (!wide && tile_t > 0) ? (t <= 128 ? split_max : 1) : orc_default_cap(M, K);
+    int32_t cap = tuned ? (t <= 128 ? split_max : 1) : orc_default_cap(M, K);
     d->family = wide ? 3 : 1; d->tile_t = t; d->granule = 16; d->n_classes = t / 16 + 1;
     d->k = M / t; d->r = M % t;                      /* x = t k + r */
     d->residue_class = (int32_t)orc_ceil_div(d->r, 16);

@@ -147,9 +147,10 @@ class BertPacked:
 
     def launches_per_forward(self, T: int | None = None) -> int:
         """Kernel launches of one forward at T packed tokens: 6 per layer where LN2 fuses into the
-        FFN2 epilogue (fused_ln, 2-CTA family M = T >= 2048, d = 1024, K = ffn >= 2048; LN1 after
+        FFN2 epilogue (fused_ln, the 2-CTA family 3 at M = T, d = 1024, K = ffn >= 2048; LN1 after
         the K = 1024 O-projection stays a launch, the library's rule), else 7."""
-        fused = self.fused_ln and T is not None and T >= 2048 and self.d == 1024 and self.f >= 2048
+        fused = (self.fused_ln and T is not None and self.d == 1024 and self.f >= 2048
+                 and nb.dispatch_dense(T, self.d, self.f, nb.BF16)[1]["family"] == 3)
         return (6 if fused else 7) * len(self.layers)
 
     def layer(self, x_ptr, out_ptr, T, seq_off_ptr, R, max_len, li, stream):

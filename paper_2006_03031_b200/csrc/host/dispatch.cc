@@ -22,9 +22,9 @@ struct ResidueFamily {
     int32_t id, t, granule, n_classes;
 };
 constexpr ResidueFamily kSIMT8{0, 8, 1, 8};      // fp32 CUDA-core dense, the paper's t = 8
-constexpr ResidueFamily kUMMA_T{1, 128, 16, 9};    // bf16 tcgen05, tokens on UMMA-N, M < 2048
-constexpr ResidueFamily kUMMA_T256{3, 256, 16, 17}; // same, M >= 2048 (no split-K)
-constexpr int64_t kWideTileFrom = 2048;
+constexpr ResidueFamily kUMMA_T{1, 128, 16, 9};    // bf16 tcgen05, tokens on UMMA-N (128 x 128 tiles)
+constexpr ResidueFamily kUMMA_T256{3, 256, 16, 17}; // same, CTA pairs (256 x 256 tiles, no split-K)
+constexpr int64_t kScheduleBelow = 2048;            // tuned family-1 schedules cover M < 2048
 constexpr ResidueFamily kUMMA_D{2, 128, 128, 2}; // bf16 tcgen05 bmm with MN-major B
 constexpr ResidueFamily kUMMA_WS{4, 128, 16, 9};  // bf16 tcgen05 dense, M <= 128: weight streaming
 
@@ -83,16 +83,34 @@ int dispatch_simt8(int64_t M, int64_t N, nimble_dispatch *d) {
     return NIMBLE_OK;
 }
 
+// Family 3 iff its 256 x 256 pair tiles need fewer waves (74 CTA pairs) than family 1's
+// 128 x 128 tiles (148 CTAs): measured on B200 (profiles/r02e_f1_vs_f3.jsonl), a pair tile at
+// K >= 768 costs about what a family-1 tile costs (both paced by the per-stage TMA feed,
+// DESIGN.md §6), so the family with fewer waves wins at every BERT shape for M = 768-8192; with
+// equal waves family 1 is faster (half the work per CTA).  Replaces the round-1 threshold M >= 2048.
+bool pair_rule(int64_t batch, int64_t M, int64_t N) {
+    const int64_t t1 = cdiv(N, 128) * cdiv(M, 128) * batch;
+    const int64_t t3 = cdiv(N, 256) * cdiv(M, 256) * batch;
+    return cdiv(t3, kNumSMs / 2) < cdiv(t1, kNumSMs);
+}
+
 int dispatch_umma_t(int64_t batch, int64_t M_tokens, int64_t N_rows, int64_t K, nimble_dispatch *d,
                     int32_t tile_t, int32_t split_max) {
     *d = nimble_dispatch{};
-    const bool wide = M_tokens >= kWideTileFrom;
-    // a tuned schedule replaces family 1's token tile t (residue classes
-    // t/16 + 1) and caps its split-K; family 3 (M >= 2048) is not tuned.
+    // family 3 (CTA pairs, 256 x 256 tiles) where it needs fewer waves than family 1's 128 x 128
+    // tiles (pair_rule); a tuned schedule replaces the default rule below M = 2048
+    const bool sched = tile_t > 0 && M_tokens < kScheduleBelow;
+    bool wide = !sched && pair_rule(batch, M_tokens, N_rows);
+    // experiment-only overrides (break oracle parity): NIMBLE_EXP_PAIR_FROM replaces the rule by
+    // a token threshold, NIMBLE_EXP_T3 sets family 3's token tile
+    static const int64_t pair_from = [] { const char *e = std::getenv("NIMBLE_EXP_PAIR_FROM"); return e ? std::atoll(e) : 0; }();
+    static const int32_t t3 = [] { const char *e = std::getenv("NIMBLE_EXP_T3"); return e ? std::atoi(e) : kUMMA_T256.t; }();
+    if (pair_from > 0) wide = M_tokens >= pair_from;
     const ResidueFamily tuned{kUMMA_T.id, tile_t, 16, tile_t / 16 + 1};
-    const ResidueFamily &f = wide ? kUMMA_T256 : (tile_t > 0 ? tuned : kUMMA_T);
+    const ResidueFamily wide_f{kUMMA_T256.id, t3, 16, t3 / 16 + 1};
+    const ResidueFamily &f = wide ? wide_f : (sched ? tuned : kUMMA_T);
     // split-K parks and receives fp32 [128 x t] slices in smem: only t <= 128 fits 227 KB
-    const int32_t cap = (!wide && tile_t > 0) ? (tile_t <= 128 ? split_max : 1) : default_split_cap(M_tokens, K);
+    const int32_t cap = sched ? (tile_t <= 128 ? split_max : 1) : default_split_cap(M_tokens, K);
     split_residue(f, M_tokens, d);
     d->residue_class = static_cast<int32_t>(cdiv(d->r, f.granule));
     d->variant = select_variant(f, d->residue_class);

@@ -74,9 +74,9 @@ struct Geo {
 template <int SM, int SN, int SK, int PAIR>
 __device__ __forceinline__ Geo make_geo(const UmmaParams &p) {
     if constexpr (SM > 0) {
-        // the DISPATCH.md rule at compile time: family 1 (t = 128) below 2048, else family 3
+        // the family the host's DISPATCH.md rule picked (PAIR): family 1 (t = 128) or family 3
         // (t = 256, CTA pairs: 256-row weight tiles, each CTA loads half of the token box)
-        constexpr int t = SM < 2048 ? 128 : 256;
+        constexpr int t = PAIR ? 256 : 128;
         constexpr int r = SM % t;
         constexpr int tiles_n = SM / t + (r ? 1 : 0);
         constexpr int n_tail = r ? 16 * ((r + 15) / 16) : t;

@@ -280,9 +280,10 @@ def test_static_twin_bitwise_equal(nb, orc):
                         torch.zeros((77, 3072), dtype=torch.bfloat16, device="cuda"))
 
 
-@pytest.mark.parametrize("M", [2048, 2049, 2300, 4111])
+@pytest.mark.parametrize("M", [3713, 3840, 4111, 4300])
 def test_bf16_large_m_cta_pairs(nb, orc, M):
-    # family 3: 2-CTA pairs (tcgen05 cta_group::2), each CTA loads half of the token tile
+    # family 3: 2-CTA pairs (tcgen05 cta_group::2), each CTA loads half of the token tile; at
+    # N = 640 the pairs need fewer waves than 128 x 128 tiles from M = 3713 (DISPATCH.md)
     N, K = 640, 256
     W = synth.normal((N, K), 0.05, 91)
     b = synth.normal((N,), 0.1, 92, torch.float32)

@@ -61,10 +61,12 @@ BENCH_SHAPES = [(3072, 1024, 1), (1024, 1024, 3), (4096, 1024, 2), (1024, 4096, 
 
 
 @pytest.mark.parametrize("N,K,epi", BENCH_SHAPES)
-@pytest.mark.parametrize("M", [2048, 2049, 2303, 17448])
+@pytest.mark.parametrize("M", [2048, 2049, 2303, 2561, 17448])
 def test_family3_bench_shapes_integer_exact(nb, orc, N, K, epi, M):
-    """The 2-CTA family at the bench's (N, K) and token counts incl. residues: sampled rows vs the
-    oracle bit for bit; every row vs exact integer arithmetic (fp64 products of small integers)."""
+    """The bench's (N, K) at token counts around the family-1 / family-3 crossover incl. residues
+    (DISPATCH.md wave rule: N = 1024 keeps family 1 up to M = 2432, N >= 3072 pairs from M < 2048):
+    sampled rows vs the oracle bit for bit; every row vs exact integer arithmetic (fp64 products
+    of small integers)."""
     W = synth.ternary((N, K), 31 + N, torch.bfloat16)
     b = synth.ternary((N,), 32 + N, torch.float32)
     x = synth.ternary((M, K), 40 + M, torch.bfloat16, max_nonzero_per_row=200)
@@ -74,7 +76,9 @@ def test_family3_bench_shapes_integer_exact(nb, orc, N, K, epi, M):
     nb.dense_dyn(xd, Wd, bd, y, epi=epi, residual=None if res is None else res.cuda(), M=M)
     torch.cuda.synchronize()
     d = nb.last_dispatch()
-    assert d == orc.dispatch_dense(M, N, K, 1)[1] and d["family"] == 3 and d["cluster"] == (2, 1, 1)
+    pairs = -(-(-(-N // 256) * -(-M // 256)) // 74) < -(-(-(-N // 128) * -(-M // 128)) // 148)
+    assert d == orc.dispatch_dense(M, N, K, 1)[1] and d["family"] == (3 if pairs else 1)
+    assert d["cluster"][0] == (2 if pairs else 1)
     assert torch.all(y[M:] == 7.0)
     rows = _sample_rows(M)
     ref, _ = orc.dense(x[rows].double().numpy(), W.double().numpy(), b.numpy(),
@@ -134,6 +138,39 @@ def test_bench_shapes_float_elementwise(nb, orc):
         ref, D = orc.dense(x[rows].double().numpy(), W.double().numpy(), b.numpy(),
                            None if res is None else res[rows].double().numpy(), epi)
         gate_bf16(y[torch.as_tensor(rows, device="cuda")], ref, D, ("bench float", N, K, epi))
+
+
+# ------------------------------------------------------------------ family 3 below M = 2048
+@pytest.mark.parametrize("N,M", [(3072, 1000), (3072, 1024), (3072, 1500), (4096, 768), (4096, 777)])
+def test_family3_below_2048_vs_oracle_and_family1(nb, orc, N, M):
+    """The wave rule (DISPATCH.md "Family 3") takes CTA pairs below M = 2048 where they need fewer
+    waves: the result is the oracle's within the bf16 gate, and equals family 1's (the same
+    operation under a (128, 1) schedule) bit for bit — residue families compute one function
+    (P:386-387)."""
+    K = 1024
+    W = synth.normal((N, K), 0.05, 61 + N)
+    b = synth.normal((N,), 0.1, 62 + N, torch.float32)
+    x = synth.normal((M, K), 1.0, 63 + M)
+    res = synth.normal((M, N), 1.0, 64 + M)
+    xd, Wd, bd, rd = x.cuda(), W.cuda(), b.cuda(), res.cuda()
+    for epi in (1, 2, 3):
+        y3 = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        nb.dense_dyn(xd, Wd, bd, y3, epi=epi, residual=rd if epi == 3 else None)
+        d = nb.last_dispatch()
+        assert d == orc.dispatch_dense(M, N, K, 1)[1] and d["family"] == 3 and d["cluster"] == (2, 1, 1)
+        nb.set_dense_schedule(N, K, 128, 1)
+        try:
+            y1 = torch.empty_like(y3)
+            nb.dense_dyn(xd, Wd, bd, y1, epi=epi, residual=rd if epi == 3 else None)
+            assert nb.last_dispatch()["family"] == 1
+        finally:
+            nb.set_dense_schedule(N, K, 0, 8)
+        torch.cuda.synchronize()
+        assert torch.equal(y1, y3), (N, M, epi)
+        rows = _sample_rows(M)
+        ref, D = orc.dense(x[rows].double().numpy(), W.double().numpy(), b.numpy(),
+                           res[rows].double().numpy() if epi == 3 else None, epi)
+        gate_bf16(y3[torch.as_tensor(rows, device="cuda")], ref, D, ("family 3 < 2048", N, M, epi))
 
 
 # ------------------------------------------------------------------ BERT-base with the tuned schedules

@@ -110,10 +110,41 @@ def test_dispatch_worked_examples(orc):
         assert (d["k"], d["r"], d["variant"]) == (int(k), int(r), int(v)), (M, c, d)
 
 
+def _pairs(M, N, batch=1):
+    """DISPATCH.md "Family 3": CTA pairs exactly when their 256 x 256 tiles need fewer waves
+    (74 pairs) than 128 x 128 tiles (148 CTAs)."""
+    waves_128 = -(-(-(-N // 128) * -(-M // 128) * batch) // 148)
+    waves_256 = -(-(-(-N // 256) * -(-M // 256) * batch) // 74)
+    return waves_256 < waves_128
+
+
+def test_dispatch_pair_rule_examples(orc):
+    # the measured crossovers DISPATCH.md cites (profiles/r02e_f1_vs_f3.jsonl): equal waves keep
+    # family 1 (2048 x 1024: 1 wave either way), fewer pair waves take family 3 at any M
+    for (M, N, K, fam) in [(2048, 1024, 1024, 1), (2304, 1024, 1024, 1), (2433, 1024, 1024, 3),
+                           (2560, 1024, 1024, 3), (2048, 1024, 4096, 1), (2560, 1024, 4096, 3),
+                           (1024, 3072, 1024, 3), (768, 3072, 1024, 1), (768, 4096, 1024, 3),
+                           (3072, 768, 768, 1), (4096, 768, 768, 3), (1536, 2304, 768, 3),
+                           (1024, 2304, 768, 1), (17448, 1024, 1024, 3), (2048, 3072, 1024, 3)]:
+        st, d = orc.dispatch_dense(M, N, K, 1)
+        assert st == 0 and d["family"] == fam and _pairs(M, N) == (fam == 3), (M, N, K, d)
+        assert d["cluster"][0] == (2 if fam == 3 else 1) and d["umma_m"] == (256 if fam == 3 else 128)
+        # padding M to a multiple of 128 keeps the family (pad-then-slice)
+        assert orc.dispatch_dense(128 * -(-M // 128), N, K, 1)[1]["family"] == fam
+    # a tuned schedule replaces the rule below M = 2048 only
+    assert orc.dispatch_dense(1024, 3072, 1024, 1, 0, 64, 1)[1]["family"] == 1
+    assert orc.dispatch_dense(4096, 3072, 1024, 1, 0, 64, 1)[1]["family"] == 3
+    assert orc.dispatch_dense(2048, 1024, 1024, 1, 0, 64, 1)[1]["tile_t"] == 128
+    # bmm: heads multiply the tile counts
+    assert orc.dispatch_bmm(16, 512, 512, 64, 0, 1)[1]["family"] == (3 if _pairs(512, 512, 16) else 1)
+    assert orc.dispatch_bmm(16, 2048, 2048, 64, 0, 1)[1]["family"] == 3
+
+
 @pytest.mark.parametrize("dt", [0, 1])
 def test_dispatch_invariants(orc, dt):
-    for M in list(range(1, 2049)) + [4095, 4096, 4097, 65535, 65536]:
-        t = 8 if dt == 0 else (128 if M < 2048 else 256)
+    for M in list(range(1, 2049)) + list(range(2400, 2600)) + [4095, 4096, 4097, 65535, 65536]:
+        wide = dt == 1 and _pairs(M, 1024)
+        t = 8 if dt == 0 else (256 if wide else 128)
         for c in (0, 1, 2, 5, 8, 9, 17):
             st, d = orc.dispatch_dense(M, 1024, 1024, dt, c)
             assert st == 0
@@ -140,11 +171,11 @@ def test_dispatch_invariants(orc, dt):
                 assert list(d["grid"]) == [8, 1, s] and s == 8             # min(16 k-blocks, 148 // 8, 8)
             elif dt == 1:
                 s = d["split_k"]
-                assert s in (1, 2, 4, 8) and d["cluster"] == ((1 if M < 2048 else 2), 1, s)
-                assert d["umma_m"] == (128 if M < 2048 else 256)
+                assert s in (1, 2, 4, 8) and d["cluster"] == ((2 if wide else 1), 1, s)
+                assert d["umma_m"] == (256 if wide else 128)
                 assert (1024 // 64) // s >= 4 or s == 1
-                assert d["family"] == (1 if M < 2048 else 3)
-                if M >= 2048:
+                assert d["family"] == (3 if wide else 1)
+                if wide:
                     assert s == 1
 
 
