@@ -362,8 +362,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       }
       __syncwarp();
     } else if (warp == 9) {
-      if (lane == 0) {
-        // ---------------- MMA issuer
+      {
+        // ---------------- MMA issuer: the whole warp runs the loop converged and one elected
+        // lane issues (warp-uniform descriptors, no per-MMA ELECT loop; umma_gemm.cu)
         const uint32_t idesc_s = ptx::idesc_bf16(128, 128, 0);
         const uint32_t idesc_o = ptx::idesc_bf16(128, 64, 1);
         const uint64_t qd = ptx::smem_desc_sw128(ptx::smem_u32(sQ), 0, 1024);
@@ -373,13 +374,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             if (ns > 0) ptx::mbar_wait(s_used, (ns - 1) & 1);      // softmax holds the previous S
             ptx::mbar_wait(k_full, ns & 1);
             ptx::tc_fence_after();
-            ATT_TRACE(ns, 6);
+            if (ptx::elect_one()) {
+                ATT_TRACE(ns, 6);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-                ptx::umma_bf16(tmem, qd + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idesc_s, kk > 0 ? 1u : 0u);
-            ptx::umma_commit(s_full);
-            ptx::umma_commit(k_empty);
-            if (j == nk_item - 1) ptx::umma_commit(q_empty);
+                for (int kk = 0; kk < 4; ++kk)
+                    ptx::umma_bf16(tmem, qd + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idesc_s, kk > 0 ? 1u : 0u);
+                ptx::umma_commit(s_full);
+                ptx::umma_commit(k_empty);
+                if (j == nk_item - 1) ptx::umma_commit(q_empty);
+            }
+            __syncwarp();
             ++ns;
         };
         int nk = 0;
@@ -408,17 +412,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 const int st = (int)(npv & 1);
                 ptx::mbar_wait(&v_full[st], (npv >> 1) & 1);
                 ptx::tc_fence_after();
-                ATT_TRACE(npv, 7);
+                if (ptx::elect_one()) {
+                    ATT_TRACE(npv, 7);
 #pragma unroll
-                for (int kb = 0; kb < 2; ++kb) {
-                    const uint64_t vd = ptx::smem_desc_sw128(ptx::smem_u32(sV + st * kTile + kb * kVBox), 8192, 1024);
+                    for (int kb = 0; kb < 2; ++kb) {
+                        const uint64_t vd = ptx::smem_desc_sw128(ptx::smem_u32(sV + st * kTile + kb * kVBox), 8192, 1024);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)            // P_j in TMEM cols [192, 256): 16 keys = 8 cols
-                        umma_bf16_ts(tmem + 128, tmem + kPCol + (uint32_t)(8 * (4 * kb + kk)), vd + (uint64_t)(kk * 128),
-                                     idesc_o, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < 4; ++kk)        // P_j in TMEM cols [192, 256): 16 keys = 8 cols
+                            umma_bf16_ts(tmem + 128, tmem + kPCol + (uint32_t)(8 * (4 * kb + kk)),
+                                         vd + (uint64_t)(kk * 128), idesc_o, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    ptx::umma_commit(pv_done);
+                    ptx::umma_commit(&v_empty[st]);
                 }
-                ptx::umma_commit(pv_done);
-                ptx::umma_commit(&v_empty[st]);
+                __syncwarp();
                 ++npv;
             }
             ATT_TRACE(384 + (int)nitem, 1);

@@ -38,6 +38,9 @@ namespace nimble {
 
 namespace {
 
+#ifndef NIMBLE_MMA_WARP
+#define NIMBLE_MMA_WARP 1      // 0: the round-1 lane-0-only issuer (experiment builds)
+#endif
 #ifndef NIMBLE_EPI_WARPS
 #define NIMBLE_EPI_WARPS 8
 #endif
@@ -446,8 +449,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ensure_wait();                  // total_tiles (devm) is final before the next tile test
         }
-    } else if (warp == kMmaWarp && lane == 0 && (!PAIR || prank == 0)) {
-        // ================= MMA issuer (single thread; the even CTA of a pair issues for both)
+    } else if (warp == kMmaWarp && (NIMBLE_MMA_WARP || lane == 0) && (!PAIR || prank == 0)) {
+        // ================= MMA issuer (the even CTA of a pair issues for both).  NIMBLE_MMA_WARP:
+        // the whole warp runs the loop converged and one elected lane issues, so the smem
+        // descriptors are warp-uniform (a lane-0-only role made ptxas wrap every tcgen05.mma in
+        // an ELECT / R2UR.BROADCAST x7 / BRA.U.ANY loop)
         if (devm) {
             ptx::pdl_wait();
             devm_geometry(p, g, total_tiles, false);
@@ -499,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (kb == w.kb_lo && it == 0) NIMBLE_TRACE(2);
                 const uint32_t sa0 = ptx::smem_u32(smem + stage * stage_bytes);
                 const int nkb = min(kd, w.kb_hi - kb);    // a partial last stage: its 2nd block is not ours
+                if (!NIMBLE_MMA_WARP || ptx::elect_one()) {
                 for (int j = 0; j < nkb; ++j) {
                     const uint32_t sa = sa0 + (uint32_t)(j * kABytes);
                     const uint32_t sb = sa0 + (uint32_t)(kd * kABytes + j * b_bytes);
@@ -517,10 +524,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (PAIR) ptx::umma_commit_pair(&empty_bar[stage], 0x3);   // frees the stage in both CTAs
                 else ptx::umma_commit(&empty_bar[stage]);    // smem stage free once these MMAs retire
+                }
+                if (NIMBLE_MMA_WARP) __syncwarp();
                 if (++stage == p.stages) { stage = 0; phase ^= 1; }
             }
-            if (PAIR) ptx::umma_commit_pair(&tfull[acc], 0x3);
-            else ptx::umma_commit(&tfull[acc]);              // accumulator complete
+            if (!NIMBLE_MMA_WARP || ptx::elect_one()) {
+                if (PAIR) ptx::umma_commit_pair(&tfull[acc], 0x3);
+                else ptx::umma_commit(&tfull[acc]);          // accumulator complete
+            }
+            if (NIMBLE_MMA_WARP) __syncwarp();
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }

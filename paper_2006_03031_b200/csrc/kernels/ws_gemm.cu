@@ -147,8 +147,10 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
             ptx::tma_load_3d(smem + s * stage_bytes, &tmA, &full[s], (kb0 + i) * kBK, mt * 128, 0);
             ptx::tma_load_3d(smem + s * stage_bytes + kAB, &tmB, &full[s], (kb0 + i) * kBK, tok0, 0);
         }
-    } else if (warp == 1 && lane == 0) {
-        // ---- MMA issuer
+    } else if (warp == 1) {
+        // ---- MMA issuer: the whole warp runs the loop converged, one elected lane issues (the
+        // descriptors stay in uniform registers; a lane-0-only role wraps every tcgen05.mma in an
+        // ELECT / R2UR.BROADCAST loop, umma_gemm.cu)
         const uint32_t idesc = ptx::idesc_bf16(128u, n_this, 0u);
         for (int i = 0; i < nkb; ++i) {
             const int s = i % p.stages;
@@ -157,13 +159,17 @@ __global__ void __launch_bounds__(kWsThreads, 2)    // two CTAs per SM: a PDL-ov
             const uint32_t sa = ptx::smem_u32(smem + s * stage_bytes);
             const uint64_t adesc = ptx::smem_desc_sw128(sa, 0, 1024);
             const uint64_t bdesc = ptx::smem_desc_sw128(sa + kAB, 0, 1024);
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk)
-                ptx::umma_bf16(tmem_base, adesc + (uint64_t)((kk * 32) >> 4), bdesc + (uint64_t)((kk * 32) >> 4), idesc,
-                               (i > 0 || kk > 0) ? 1u : 0u);
-            ptx::umma_commit(&empty[s]);
+                for (int kk = 0; kk < kBK / 16; ++kk)
+                    ptx::umma_bf16(tmem_base, adesc + (uint64_t)((kk * 32) >> 4), bdesc + (uint64_t)((kk * 32) >> 4),
+                                   idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                ptx::umma_commit(&empty[s]);
+            }
+            __syncwarp();
         }
-        ptx::umma_commit(tfull);
+        if (ptx::elect_one()) ptx::umma_commit(tfull);
+        __syncwarp();
     }
     __syncwarp();
     if (p.m_dev) Mt = *p.m_dev;                        // every thread has passed the dependency wait
