@@ -465,11 +465,9 @@ static int dense_impl(const void *x, int64_t ldx, const void *W, int64_t ldw, co
     const int out_box = L.p.half_stg ? L.p.box_n / 2 : L.p.box_n;
     // two k-blocks per pipeline stage where the operands tile K exactly (every BERT shape)
     L.p.kd = (kblock2_enabled() && K % 64 == 0 && K >= 128) ? 2 : 1;
-    // the 1-CTA family without split-K takes THREE k-blocks per stage (96 KB stages, two in the
-    // ring): fewer, larger TMA stages per tile (the per-stage completion pacing);
-    // measured 2-7 % faster at M = 256-1024 on every BERT shape, while the CTA-pair family is
-    // 2-9 % slower with it (profiles/r02c_kd3_sweep.jsonl)
-    if (L.p.kd == 2 && !L.pair && L.p.split == 1 && K >= 192) L.p.kd = 3;
+    // (the second session took kd = 3 for the 1-CTA family without split-K, 2-7 % faster with
+    // the lane-0 MMA issuer; with the converged-warp issuer kd = 2 is 0-5 % faster at every
+    // family-1 point, profiles/r02e_kd_ab.jsonl, so every family streams kd = 2 again)
     static const int kd_exp = [] { const char *e = std::getenv("NIMBLE_EXP_KD"); return e ? std::atoi(e) : 0; }();
     if (kd_exp >= 2 && L.p.kd >= 2) L.p.kd = kd_exp;   // experiment only: k-blocks per stage
     if (L.p.kd >= 2) {

@@ -309,6 +309,14 @@ __device__ __forceinline__ float2 gelu_erf2(float2 z) {
         h = ffma2(h, e, h);
     }
     h = fmul2(h, h); h = fmul2(h, h); h = fmul2(h, h); h = fmul2(h, h);
+#elif defined(NIMBLE_GELU_RCP2)
+    // one MUFU per TWO values: r = 1 / (p.x p.y), 1/p.x = r p.y, 1/p.y = r p.x (two more roundings:
+    // ~2^-22 relative on 1/p, x16 -> ~4e-6 on h; GELU(-1) is 2.5e-4 from a bf16 midpoint)
+    {
+        const float r = rcp_approx(p.x * p.y);
+        h = fmul2(f2(r), make_float2(p.y, p.x));
+    }
+    h = fmul2(h, h); h = fmul2(h, h); h = fmul2(h, h); h = fmul2(h, h);
 #elif !defined(NIMBLE_GELU_LG2EX2)
     // one MUFU per value and p^-16 by squaring: half the MUFU traffic of lg2 + ex2, which the
     // GELU GEMM's main loop felt (stage interval 1278 -> 1149 clk, FFN1 at M = 17448

@@ -2,15 +2,16 @@
 
 For a dense op with a symbolic token extent (Any) and static weights (N, K):
   1. tune with Any := 64: time every schedule of the space at M = 64;
-  2. keep the top-k schedules of step 1;
+  2. keep the top-k schedules of step 1 (plus the default rule);
   3. cross-evaluate the top-k on M in {1, 2, 4, ..., 256} (powers of two <= 256) and pick the
      schedule with the best average (mean over M of time / best-of-top-k time at that M).
 The schedule space is the tunable part of our bf16 kernel family 1 (DISPATCH.md): the token
 tile t in {32, 64, 128, 256} (the residue tile, t/16 + 1 residue variants) x the split-K
-cap in {1, 2, 4, 8} = 16 schedules, so k = 4 here (the paper keeps 100 of AutoTVM's
+cap in {1, 2, 4, 8} = 16 schedules, plus "no schedule" (the default rule, family 4 at
+M <= 128), so k = 4 here (the paper keeps 100 of AutoTVM's
 thousands of template configurations; reading 23).
 Held-out check: on M not used for tuning (3, 17, 48, 100, 200, 255, 384, 511) the tuned
-schedule is compared with the default (t = 128, cap 8) and with the per-M best of all 16.
+schedule is compared with the default rule (no schedule) and with the per-M best of all 16.
 
 Timing: a CUDA graph of 20 back-to-back nimble_dense_dyn launches (PDL chained), replayed
 5x after a warm-up, CUDA events; median of 3 such runs.  Writes gpurun_out/symbolic_tuning.json
@@ -30,11 +31,14 @@ SHAPES = {  # (N, K) of the BERT dense ops (weights [N x K])
     "base_qkv": (2304, 768), "base_o": (768, 768), "base_ffn1": (3072, 768), "base_ffn2": (768, 3072),
     "large_qkv": (3072, 1024), "large_o": (1024, 1024), "large_ffn1": (4096, 1024), "large_ffn2": (1024, 4096),
 }
-SPACE = list(itertools.product((32, 64, 128, 256), (1, 2, 4, 8)))
+# (0, 8) = no schedule: the default DISPATCH.md rule (family 4 weight streaming at one token
+# tile, family 1 / 3 above) competes with the 16 family-1 schedules (round 2: the round-1 space
+# predates family 4, and a schedule replaces the default rule below M = 2048)
+SPACE = [(0, 8)] + list(itertools.product((32, 64, 128, 256), (1, 2, 4, 8)))
 TOP_K = 4
 CROSS_M = [1, 2, 4, 8, 16, 32, 64, 128, 256]
 HELDOUT_M = [3, 17, 48, 100, 200, 255, 384, 511]
-DEFAULT = (128, 8)
+DEFAULT = (0, 8)
 
 
 class Bench:
@@ -74,6 +78,8 @@ def tune(name, N, K):
     bench = Bench(N, K)
     step1 = {f"{t},{s}": bench.time_us((t, s), 64) for (t, s) in SPACE}
     top = sorted(SPACE, key=lambda ts: step1[f"{ts[0]},{ts[1]}"])[:TOP_K]
+    if DEFAULT not in top:
+        top.append(DEFAULT)          # the default rule always reaches the cross-evaluation
     step3 = {f"{t},{s}": {M: bench.time_us((t, s), M) for M in CROSS_M} for (t, s) in top}
     best_at = {M: min(step3[k][M] for k in step3) for M in CROSS_M}
     score = {k: sum(v[M] / best_at[M] for M in CROSS_M) / len(CROSS_M) for k, v in step3.items()}

@@ -195,7 +195,8 @@ def test_bert_base_layer_tuned_schedules(nb, orc, tuned, L):
     d, H = cfg["d"], cfg["heads"]
     for e in tuned:                                       # the base schedules are the ones in force
         if e["N"] in (2304, 768, 3072) and e["K"] in (768, 3072):
-            assert nb.get_dense_schedule(e["N"], e["K"]) == (e["tile_t"], e["split_max"])
+            t, s = nb.get_dense_schedule(e["N"], e["K"])   # tile_t = 0: the default rule won the tuning
+            assert t == e["tile_t"] and (t == 0 or s == e["split_max"])
     w = synth.bert_weights(cfg, seed=0, layers=1)
     enc = BertEncoder(cfg, w, max_len=128)
     x = synth.bert_input(L, d, seed=900 + L).cuda()
