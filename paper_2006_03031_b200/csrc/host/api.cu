@@ -623,7 +623,9 @@ extern "C" int nimble_dense_dyn_dev(const void *x, int64_t ldx, const void *W, i
     // token tile, where the host rule's split (a function of the tile count) is the same for
     // every M <= M_max; otherwise the device dispatch runs split 1
     dispatch_umma_t(1, M_max, N, K, &d, t, cap);        // t = 0: the default rule (t = 128, K-dependent cap)
-    if (d.grid[1] != 1) dispatch_umma_t(1, M_max, N, K, &d, t > 0 ? t : 128, 1);   // launch geometry for the bound
+    // (family 3, which the wave rule can pick for a wide N, has no device-side geometry: the
+    // device path runs family 1 at t = 128 then too)
+    if (d.grid[1] != 1 || d.family == 3) dispatch_umma_t(1, M_max, N, K, &d, t > 0 ? t : 128, 1);   // geometry for the bound
     UmmaLaunch L;
     std::memset(&L, 0, sizeof(L));
     L.p.rows_a = (int32_t)N;
