@@ -22,7 +22,7 @@
 //                  O += P_j V_j into TMEM cols [128,192) once P_j is written.
 //   warps 0-7      softmax: row q = TMEM lane 32*(w%4)+lane, key half (w/4) of the block held
 //                  in registers; running max / sum in FFMA2 / FADD2 / FMNMX3, exp2 on MUFU
-//                  and (2 of 8 pairs) on the FMA pipes; unnormalised P_j written as bf16
+//                  and (3 of 8 pairs) on the FMA pipes; unnormalised P_j written as bf16
 //                  straight into the UMMA K-major swizzled smem layout; O rescaled in TMEM
 //                  only when a row max grew by more than 2^8 (lazy rescaling); epilogue
 //                  O / rowsum -> bf16.
@@ -135,7 +135,7 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
 #endif
 constexpr float kLazy = NIMBLE_ATTN_LAZY;
 #ifndef NIMBLE_ATTN_POLY
-#define NIMBLE_ATTN_POLY 2          // pairs out of every 8 whose exp2 runs on the FMA pipes
+#define NIMBLE_ATTN_POLY 3          // pairs out of every 8 whose exp2 runs on the FMA pipes (3: 65.3 vs 65.6 us, r02e_attn_poly_ab.txt)
 #endif
 
 __device__ __forceinline__ int qtiles_of(const int32_t *seq_off, int r) {
