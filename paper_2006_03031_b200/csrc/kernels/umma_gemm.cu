@@ -38,6 +38,9 @@ namespace nimble {
 
 namespace {
 
+#ifndef NIMBLE_TMA_WARP
+#define NIMBLE_TMA_WARP 1      // TMA producers converged over the warp, elect.sync issue (0: lane-0 producers)
+#endif
 #ifndef NIMBLE_MMA_WARP
 #define NIMBLE_MMA_WARP 1      // 0: the round-1 lane-0-only issuer (experiment builds)
 #endif
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::pdl_trigger();                            // the next kernel's prologue may start now
     if (threadIdx.x == 0) NIMBLE_TRACE(1);
 
-    if ((warp == kProdAWarp || warp == kProdBWarp) && lane == 0) {
+    if ((warp == kProdAWarp || warp == kProdBWarp) && (NIMBLE_TMA_WARP || lane == 0)) {
         // ================= TMA producers: warp 0 streams A (weights), warp 3 streams B (tokens).
         // One warp keeps only about one TMA stage in flight (measured: scripts/exp/tma_ingest.cu,
         // ~1k clk per stage per issuing warp), so the two operands are issued from two warps and a
@@ -413,8 +416,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ensure_wait();          // a ring's worth of early weights at most, then the dependencies
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
                 }
-                if (isA && (p.dbg & 4) && trace && cta_lin == 0 && nkb_p < 4096) p.trace[16384 + nkb_p] = clock64();
+                if (isA && (p.dbg & 4) && trace && cta_lin == 0 && nkb_p < 4096 && lane == 0) p.trace[16384 + nkb_p] = clock64();
                 ++nkb_p;
+                if (!NIMBLE_TMA_WARP || ptx::elect_one()) {
                 if (arms) ptx::mbar_arrive_expect_tx_relaxed(&full_bar[stage], tx);
                 const int32_t kc = kb * kBlockK;
                 uint8_t *sa = smem + stage * stage_bytes;
@@ -444,6 +448,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else if (p.b_batch_mid) ptx::tma_load_3d(sb, &tmB, &full_bar[stage], kc, bb, b_row);
                     else ptx::tma_load_3d(sb, &tmB, &full_bar[stage], kc, b_row, bb);
                 }
+                }
+                if (NIMBLE_TMA_WARP) __syncwarp();
                 ++nload;
                 if (++stage == p.stages) { stage = 0; phase ^= 1; }
             }
