@@ -3,17 +3,19 @@
 //
 // Tile = 128 (UMMA M) x n (UMMA N: the full tile width t, or the residue-specialised
 // tail width 16*ceil(r/16) the dispatch function picked) over K.
-// 384 threads, warp-specialised:
-//   warp 0 lane 0  TMA producer: A[128 x 64] + B[box_n x 64] bf16 tiles (128-B swizzle)
+// 384 threads, warp-specialised (the single-issuer roles sit on the highest warp ids,
+// kProdAWarp..kProdBWarp, and each role warp runs converged with one elect.sync lane issuing,
+// NIMBLE_TMA_WARP / NIMBLE_MMA_WARP):
+//   producers      TMA: A[128 x 64] (one warp) + B[box_n x 64] (another) bf16 tiles (128-B swizzle)
 //                  into a `stages`-deep smem ring (full/empty mbarriers).  Rows beyond
 //                  the symbolic extent are zero-filled by TMA bounds — the dynamic
 //                  dimension is never padded in memory.  With PDL the static weight
 //                  operand of the first tile is fetched BEFORE griddepcontrol.wait, so
 //                  the weight stream overlaps the previous kernel's tail.
-//   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (K = 16) per 64-wide k-block into one of
+//   MMA warp       4 x tcgen05.mma (K = 16) per 64-wide k-block into one of
 //                  two fp32 TMEM accumulators (double-buffered across tiles).
-//   warp 2         TMEM allocation / deallocation.
-//   warps 4..      epilogue: warp w reads TMEM lane quarter (w % 4), 16-column chunks
+//   alloc warp     TMEM allocation / deallocation.
+//   warps 0..7     epilogue: warp w reads TMEM lane quarter (w % 4), 16-column chunks
 //                  round-robin over the column groups; compile-time epilogue
 //                  (alpha | bias | bias+GELU | bias+residual | bias+residual+LayerNorm).
 //                  bf16 outputs: tcgen05.ld.16x256b fragments -> stmatrix.trans into two
